@@ -1,0 +1,382 @@
+"""Headline benchmark: fused forward+backward Gaussian-mixture interpolation.
+
+Workload (BASELINE.json configs[2], the one the metric is quoted on):
+B=64 images per GPU, N=262,144 points, C=3, output 1024x1024, sigma=1.5,
+cutoff 3*sigma = 4.5.  One "step" = gmi_forward + gmi_backward over the whole
+batch.  Synthetic inputs (positions U(-0.5, W-0.5), colours U[0,1), upstream
+U(-1,1)), generated on the device with torch (plumbing only).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+value    device-resident throughput (output Mpix/s, whole job)
+e2e      the same through the host-buffer C-ABI (gmi_forward_host /
+         gmi_backward_host): H2D of positions/colours/upstream and D2H of the
+         image and both gradients inside the timed region
+Timing: CUDA events on the library's stream, warm-up first, barrier +
+synchronize around the timed region, max over ranks.  Inputs (B*...) are far
+larger than L2 (126 MB), so no explicit flush is needed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = dict(B=64, N=262144, C=3, W=1024, H=1024, sigma=1.5, cutoff=4.5)
+METRIC = "output Mpixels/s fwd+bwd at 1024^2, N=262k pts, C=3 (1/2/4/8 B200) vs CPU"
+WORKLOAD = "B=64 x 1024^2, N=262144, C=3, sigma=1.5, cutoff=3sigma (BASELINE configs[2])"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return 6650.0, 1965.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()),
+                 default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 3 + k and s[3 + k].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "gmi" else "gloo"
+        dist.init_process_group(backend, init_method="env://")
+    return world, rank, local
+
+
+def cpu_reference_sample(cfg, seconds_budget: float, max_images: int, seed: int = 7):
+    """Times the UNMODIFIED reference CPU path (oracle/_ref, compiled from the
+    reference sources) — gmi::forward + gmi::backward per image with
+    num_workers = all host threads — on a bounded sample of the workload.
+    Returns (Mpix/s, images, threads, seconds, kind)."""
+    import numpy as np
+
+    import oracle
+
+    if oracle.reference_available():
+        impl, kind = oracle.Reference(), "reference"
+    else:
+        if not oracle.oracle_available():
+            oracle.build(with_reference=False)
+        impl, kind = oracle.Oracle(), "port"
+    threads = os.cpu_count() or 1
+    gen = oracle.Oracle() if oracle.oracle_available() else None
+    if gen is None:
+        oracle.build(with_reference=False)
+        gen = oracle.Oracle()
+    W, H, C = cfg["W"], cfg["H"], cfg["C"]
+    done, elapsed = 0, 0.0
+    while done < max_images and (done == 0 or elapsed < seconds_budget):
+        pos, col, up = gen.synth_batch(seed + done, 1, cfg["N"], C, W, H)
+        p64, c64, u64 = (pos[0].astype(np.float64), col[0].astype(np.float64),
+                         up[0].astype(np.float64))
+        t0 = time.perf_counter()
+        if kind == "reference":
+            impl.forward_backward(p64, c64, W, H, cfg["sigma"], cfg["cutoff"], u64, 0, threads)
+        else:
+            f = impl.forward(p64, c64, W, H, cfg["sigma"], cfg["cutoff"])
+            impl.backward(p64, c64, f, u64, cfg["sigma"], cfg["cutoff"])
+        elapsed += time.perf_counter() - t0
+        done += 1
+    threads_used = threads if kind == "reference" else 1
+    return done * W * H / elapsed / 1e6, done, threads_used, elapsed, kind
+
+
+def run_reference_arm(args, world, rank):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref)
+    on the box's host cores, rank 0 only; each step = one image of the
+    workload (bounded sample)."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+
+    cfg = CFG
+    if oracle.reference_available():
+        impl, kind = oracle.Reference(), "reference"
+    else:
+        impl, kind = None, "port"
+        if not oracle.oracle_available():
+            oracle.build(with_reference=False)
+    gen = oracle.Oracle()
+    threads = os.cpu_count() or 1
+    W, H = cfg["W"], cfg["H"]
+    times = []
+    for s in range(args.warmup + args.steps):
+        pos, col, up = gen.synth_batch(100 + s, 1, cfg["N"], cfg["C"], W, H)
+        p64, c64, u64 = (a[0].astype(np.float64) for a in (pos, col, up))
+        t0 = time.perf_counter()
+        if kind == "reference":
+            impl.forward_backward(p64, c64, W, H, cfg["sigma"], cfg["cutoff"], u64, 0, threads)
+        else:
+            f = gen.forward(p64, c64, W, H, cfg["sigma"], cfg["cutoff"])
+            gen.backward(p64, c64, f, u64, cfg["sigma"], cfg["cutoff"])
+        t = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(t)
+    total = sum(times)
+    value = args.steps * W * H / total / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "Mpix/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD + " — one image per step (bounded CPU sample)",
+                   "global_batch": 1, "parallelism": "cpu threads"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "Mpix/s", "cores": threads,
+                         "kind": kind, "sample": f"{args.steps} images of 1024^2 after {args.warmup} warm-up"},
+        "e2e": {"value": round(value, 4), "unit": "Mpix/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gmi", choices=["gmi", "reference"])
+    ap.add_argument("--batch", type=int, default=CFG["B"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2012_13257_b200 as gmi
+
+    assert args.warmup >= 3, "contract: at least 3 warm-up steps"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = dict(CFG, B=args.batch)
+    B, N, C, W, H = cfg["B"], cfg["N"], cfg["C"], cfg["W"], cfg["H"]
+    sigma, cutoff = cfg["sigma"], cfg["cutoff"]
+
+    stream = torch.cuda.Stream(device=dev)
+    ctx = gmi.Context(local)
+    ctx.set_stream(stream.cuda_stream)
+    ctx.set_flags(1)  # asynchronous validation errors; checked after the loop
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    with torch.cuda.stream(stream):
+        pos = torch.empty(B, N, 2, device=dev)
+        pos[..., 0].uniform_(-0.5, W - 0.5, generator=g)
+        pos[..., 1].uniform_(-0.5, H - 0.5, generator=g)
+        col = torch.rand(B, N, C, device=dev, generator=g)
+        up = torch.rand(B, H, W, C, device=dev, generator=g) * 2 - 1
+        img = torch.empty(B, H, W, C, device=dev)
+        dcol = torch.empty(B, N, C, device=dev)
+        dpos = torch.empty(B, N, 2, device=dev)
+    stream.synchronize()
+
+    def step():
+        cache = ctx.forward_device(pos, col, B, N, C, W, H, sigma, cutoff, 0, img)
+        ctx.backward_device(pos, col, B, N, C, W, H, sigma, cutoff, 0, cache, up, dcol, dpos)
+        return cache
+
+    for _ in range(args.warmup):
+        step()
+    ctx.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # ---- device-resident timed region ----
+    ctx.set_profiling(True)
+    ctx.phase_times(reset=True)
+    barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = ctx.launch_count
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    caches = []
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            caches.append(step())
+            if len(caches) > 2:
+                caches.pop(0)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = ev0.elapsed_time(ev1)
+    barrier()
+    launches = ctx.launch_count - launches0
+    ctx.synchronize()  # raises on any pending validation error
+    phase_ms, phase_calls = ctx.phase_times(reset=True)
+    ctx.set_profiling(False)
+    caches.clear()
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * B * W * H / (ms_step * 1e-3) / 1e6
+
+    # ---- pair count P (exact, counting instantiation of the same kernel) ----
+    cache = ctx.forward_device(pos[:1], col[:1], 1, N, C, W, H, sigma, cutoff, 0, img[:1])
+    P_img = int(gmi.forward_counts(cache).astype(np.int64).sum())
+    del cache
+
+    # ---- roofline of the dominant kernel (per launch = whole batch) ----
+    hbm_peak, sm_mhz, peak_kind = peaks()
+    per_call = {name: phase_ms[k] / max(1, phase_calls[k]) for k, name in enumerate(gmi.Context.PHASES)}
+    dom = max(("gather", "points_bwd"), key=lambda k: per_call[k])
+    pts_bytes = 4 * N * (2 + C)
+    img_bytes = 4 * H * W * C
+    alg_bytes = {"gather": B * (pts_bytes + img_bytes),            # points in, image out
+                 "points_bwd": B * (2 * pts_bytes + img_bytes)}   # points in, grads out, upstream in
+    alg_fp32 = {"gather": B * P_img * (6 + C), "points_bwd": B * P_img * (11 + 2 * C)}
+    t_dom = per_call[dom] * 1e-3
+    achieved = alg_bytes[dom] / t_dom / 1e9
+    fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # T FP32-instr/s
+    fp32_ach = alg_fp32[dom] / t_dom / 1e12
+    total_fp32 = B * P_img * (17 + 3 * C)
+    step_fp32_frac = total_fp32 / (ms_step * 1e-3) / 1e12 / fp32_peak
+
+    # ---- e2e through the host-buffer C-ABI ----
+    pinned = [pos.cpu().pin_memory(), col.cpu().pin_memory(), up.cpu().pin_memory(),
+              torch.empty(B, H, W, C).pin_memory(), torch.empty(B, N, C).pin_memory(),
+              torch.empty(B, N, 2).pin_memory()]
+    hpos, hcol, hup, himg, hdc, hdp = (t.numpy() for t in pinned)
+    import ctypes as Cty
+    fp = Cty.POINTER(Cty.c_float)
+    cfg_c = gmi._lib.GmiConfig(sigma, cutoff, 0, W, H)
+
+    def e2e_step():
+        h = Cty.c_void_p()
+        gmi._check(gmi.lib.gmi_forward_host(ctx.handle, hpos.ctypes.data_as(fp), hcol.ctypes.data_as(fp),
+                                            B, N, C, Cty.byref(cfg_c), himg.ctypes.data_as(fp), Cty.byref(h)))
+        gmi._check(gmi.lib.gmi_backward_host(ctx.handle, hpos.ctypes.data_as(fp), hcol.ctypes.data_as(fp),
+                                             B, N, C, Cty.byref(cfg_c), h, hup.ctypes.data_as(fp),
+                                             hdc.ctypes.data_as(fp), hdp.ctypes.data_as(fp)))
+        gmi.lib.gmi_cache_free(h)
+
+    e2e_step()
+    barrier()
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = world * B * W * H / (e2e_ms * 1e-3) / 1e6
+    h2d = B * N * 4 * (2 + C) * 2 + B * H * W * C * 4
+    d2h = B * H * W * C * 4 + B * N * 4 * (C + 2)
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "Mpix/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "batch_per_gpu": B, "global_batch": world * B,
+                   "points": N, "channels": C, "frame": [H, W], "sigma": sigma,
+                   "cutoff": cutoff, "pairs_per_image": P_img,
+                   "l2": "inputs > L2 (126 MB): no flush needed",
+                   "parallelism": f"batch-sharded x{world}, no collective"},
+        "phases_ms_per_step": {k: round(v, 4) for k, v in per_call.items()},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
+                     "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                     "traffic": None, "peak_kind": peak_kind,
+                     "note": "algorithmic bytes per launch / CUDA-event time; the path is FP32-pipe bound, see roofline_fp32"},
+        "roofline_fp32": {"bound": "fp32_pipe", "kernel": dom, "achieved": round(fp32_ach, 3),
+                          "peak": round(fp32_peak, 2), "unit": "T FP32-instr/s",
+                          "frac": round(fp32_ach / fp32_peak, 4),
+                          "step_frac": round(step_fp32_frac, 4),
+                          "counts": "fwd 6+C, bwd 11+2C FP32 instr per (pixel,point) pair (SURVEY §8d)"},
+        "e2e": {"value": round(e2e_value, 2), "unit": "Mpix/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3)},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if not args.no_cpu_baseline:
+        v, imgs, threads, secs, kind = cpu_reference_sample(cfg, args.cpu_seconds, 64)
+        line["cpu_baseline"] = {"value": round(v, 4), "unit": "Mpix/s", "cores": threads,
+                                "kind": kind,
+                                "sample": f"{imgs} image(s) of the workload, fwd+bwd, {secs:.1f} s"}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,512 @@
+// K1 — point binning: a device counting sort reproducing the reference's
+// build_bin_grid (bin_grid.cpp:38-82) bit for bit.
+//
+//   k_bbox_validate  bbox (exact fp32 min/max == the reference's f64 min/max
+//                    of widened fp32 values) + position finiteness
+//                    (core.cpp:73-79)
+//   host             origin / n_cols / n_rows in f64 (bin_grid.cpp:18-24,58-60)
+//   k_count          f64 cell of each point (bin_grid.cpp:28-36,66-67) and an
+//                    atomic arrival rank inside its cell
+//   scan             segmented exclusive scan -> bin_start (bin_grid.cpp:72-75)
+//   k_scatter        point -> bin_start[cell] + rank (unordered within a cell)
+//   k_cellsort_*     order each cell: by original index (reference export,
+//                    bin_grid.cpp:76-80) or, for the hot layout, by (fine
+//                    x-column, index) and emit the bin-ordered SoA copy
+//                    (x, y, index, colour planes) + colour validation
+//                    (core.cpp:80-92).
+#include <algorithm>
+
+#include "gmi_internal.cuh"
+
+using namespace gmi_dev;
+
+namespace {
+
+constexpr int kScanTile = 2048;   // ints per scan tile
+constexpr int kScanThreads = 256;
+constexpr int kSmallCell = 32;    // cells up to this size: one thread sorts
+constexpr int kBigSmemKeys = 8192;
+
+// ---------------------------------------------------------------------------
+__global__ void k_bbox_validate(const float2* __restrict__ pos, int N,
+                                uint32_t* __restrict__ bbox,
+                                unsigned long long* __restrict__ issue) {
+    const int b = blockIdx.y;
+    const float2* p = pos + static_cast<size_t>(b) * N;
+    float mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
+    unsigned long long bad = kNoIssue;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N;
+         i += gridDim.x * blockDim.x) {
+        const float2 v = p[i];
+        if (!is_finite_f(v.x) || !is_finite_f(v.y)) {
+            // NonFiniteValue (core.hpp:36) -> 1 + 0
+            bad = min(bad, (static_cast<unsigned long long>(i) << 8) | 1ull);
+            continue;
+        }
+        mnx = fminf(mnx, v.x);
+        mny = fminf(mny, v.y);
+        mxx = fmaxf(mxx, v.x);
+        mxy = fmaxf(mxy, v.y);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mnx = fminf(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+        mny = fminf(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+        mxx = fmaxf(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+        mxy = fmaxf(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+        bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        uint32_t* bb = bbox + 4 * b;
+        atomicMin(bb + 0, f2ord(mnx));
+        atomicMin(bb + 1, f2ord(mny));
+        atomicMax(bb + 2, f2ord(mxx));
+        atomicMax(bb + 3, f2ord(mxy));
+        if (bad != kNoIssue) atomicMin(issue + b, bad);
+    }
+}
+
+__global__ void k_bbox_init(uint32_t* bbox, unsigned long long* issue, int B) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < B) {
+        bbox[4 * b + 0] = 0xFFFFFFFFu;
+        bbox[4 * b + 1] = 0xFFFFFFFFu;
+        bbox[4 * b + 2] = 0u;
+        bbox[4 * b + 3] = 0u;
+        issue[b] = kNoIssue;
+    }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_count(const float2* __restrict__ pos, int N,
+                        const Geom* __restrict__ geom, int32_t* __restrict__ bins,
+                        int32_t* __restrict__ cellid, int32_t* __restrict__ rank) {
+    const int b = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const Geom g = geom[b];
+    const float2 v = pos[static_cast<size_t>(b) * N + i];
+    const int cx = cell_of(static_cast<double>(v.x), g.ox, g.cell, g.n_cols);
+    const int cy = cell_of(static_cast<double>(v.y), g.oy, g.cell, g.n_rows);
+    const int bin = cy * g.n_cols + cx;  // bin_grid.cpp:67
+    const int r = atomicAdd(bins + g.bin_off + bin, 1);
+    cellid[static_cast<size_t>(b) * N + i] = bin;
+    rank[static_cast<size_t>(b) * N + i] = r;
+}
+
+__global__ void k_scatter(int N, const Geom* __restrict__ geom,
+                          const int32_t* __restrict__ bins,
+                          const int32_t* __restrict__ cellid,
+                          const int32_t* __restrict__ rank,
+                          int32_t* __restrict__ tmp) {
+    const int b = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const size_t k = static_cast<size_t>(b) * N + i;
+    const int dst = bins[geom[b].bin_off + cellid[k]] + rank[k];
+    tmp[static_cast<size_t>(b) * N + dst] = i;
+}
+
+// ---------------------------------------------------------------------------
+// Segmented exclusive scan (one segment per image, length n_bins + 1).
+struct ScanTile {
+    int64_t start;
+    int32_t len;
+    int32_t seg;
+};
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot,
+                                                    int* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        int w = lane < nw ? warp_tot[lane] : 0;
+        int wi = w;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += t;
+        }
+        if (lane < nw) warp_tot[lane] = wi - w;
+        if (lane == nw - 1) *total = wi;
+    }
+    __syncthreads();
+    const int res = warp_tot[warp] + incl - v;
+    __syncthreads();
+    return res;
+}
+
+__global__ void k_scan_reduce(const int32_t* __restrict__ data,
+                              const ScanTile* __restrict__ tiles,
+                              int32_t* __restrict__ tile_sum) {
+    __shared__ int red[kScanThreads / 32];
+    const ScanTile t = tiles[blockIdx.x];
+    int s = 0;
+    for (int k = threadIdx.x; k < t.len; k += blockDim.x) s += data[t.start + k];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < kScanThreads / 32; ++w) tot += red[w];
+        tile_sum[blockIdx.x] = tot;
+    }
+}
+
+// one block per segment; tile sums of the segment scanned in place
+__global__ void k_scan_segments(int32_t* __restrict__ tile_sum,
+                                const int32_t* __restrict__ seg_tile_off) {
+    __shared__ int warp_tot[32];
+    __shared__ int total;
+    const int t0 = seg_tile_off[blockIdx.x], t1 = seg_tile_off[blockIdx.x + 1];
+    int carry = 0;
+    for (int base = t0; base < t1; base += blockDim.x) {
+        const int k = base + threadIdx.x;
+        const int v = k < t1 ? tile_sum[k] : 0;
+        const int ex = block_exclusive_scan(v, warp_tot, &total);
+        if (k < t1) tile_sum[k] = carry + ex;
+        carry += total;
+        __syncthreads();
+    }
+}
+
+__global__ void k_scan_apply(int32_t* __restrict__ data,
+                             const ScanTile* __restrict__ tiles,
+                             const int32_t* __restrict__ tile_off) {
+    __shared__ int buf[kScanTile];
+    __shared__ int warp_tot[32];
+    __shared__ int total;
+    const ScanTile t = tiles[blockIdx.x];
+    for (int k = threadIdx.x; k < kScanTile; k += blockDim.x)
+        buf[k] = k < t.len ? data[t.start + k] : 0;
+    __syncthreads();
+    constexpr int kPer = kScanTile / kScanThreads;
+    int v[kPer];
+    int s = 0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        v[j] = buf[threadIdx.x * kPer + j];
+        s += v[j];
+    }
+    int ex = block_exclusive_scan(s, warp_tot, &total) + tile_off[blockIdx.x];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        buf[threadIdx.x * kPer + j] = ex;
+        ex += v[j];
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < t.len; k += blockDim.x) data[t.start + k] = buf[k];
+}
+
+// ---------------------------------------------------------------------------
+// Within-cell ordering.
+struct SortOut {
+    bool hot;
+    // hot layout
+    float* sx;
+    float* sy;
+    int32_t* sidx;
+    float* scol;
+    const float* col;
+    int C;
+    unsigned long long* issue;
+    // reference export
+    int32_t* point_index;
+};
+
+__device__ __forceinline__ unsigned long long sort_key(bool hot, int i,
+                                                       const float2* p,
+                                                       const Geom& g) {
+    if (!hot) return static_cast<unsigned long long>(i);
+    const int fc = fine_col(p[i].x, g.qx0, g.qscale);
+    const uint32_t ufc = static_cast<uint32_t>(fc) ^ 0x80000000u;
+    return (static_cast<unsigned long long>(ufc) << 32) | static_cast<uint32_t>(i);
+}
+
+// Emits slot k (image-local) of the sorted layout for original point i.
+__device__ __forceinline__ void emit(const SortOut& o, int b, int N, int k,
+                                     int i, const float2* p) {
+    const size_t bk = static_cast<size_t>(b) * N + k;
+    if (!o.hot) {
+        o.point_index[bk] = i;
+        return;
+    }
+    const float2 v = p[i];
+    o.sx[bk] = v.x;
+    o.sy[bk] = v.y;
+    o.sidx[bk] = i;
+    const float* c = o.col + (static_cast<size_t>(b) * N + i) * o.C;
+    unsigned code = 0;
+    for (int ch = 0; ch < o.C; ++ch) {
+        const float cv = c[ch];
+        o.scol[(static_cast<size_t>(b) * o.C + ch) * N + k] = cv;
+        if (code == 0) {
+            if (!is_finite_f(cv)) code = 1;             // NonFiniteValue
+            else if (cv < 0.0f || cv > 1.0f) code = 2;  // ColorOutOfRange
+        }
+    }
+    if (code) atomicMin(o.issue + b, (static_cast<unsigned long long>(i) << 8) | code);
+}
+
+__global__ void k_cellsort_small(const float2* __restrict__ pos, int N,
+                                 const Geom* __restrict__ geom,
+                                 const int32_t* __restrict__ bins,
+                                 const int32_t* __restrict__ tmp, SortOut o,
+                                 int2* __restrict__ big, int32_t* big_count) {
+    const int b = blockIdx.y;
+    const Geom g = geom[b];
+    const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+    if (cell >= g.n_cols * g.n_rows) return;
+    const int s = bins[g.bin_off + cell], e = bins[g.bin_off + cell + 1];
+    const int n = e - s;
+    if (n == 0) return;
+    const float2* p = pos + static_cast<size_t>(b) * N;
+    const int32_t* t = tmp + static_cast<size_t>(b) * N;
+    if (n > kSmallCell) {
+        const int slot = atomicAdd(big_count, 1);
+        big[slot] = make_int2(b, cell);
+        return;
+    }
+    unsigned long long key[kSmallCell];
+    for (int k = 0; k < n; ++k) {
+        const unsigned long long v = sort_key(o.hot, t[s + k], p, g);
+        int j = k;
+        while (j > 0 && key[j - 1] > v) {
+            key[j] = key[j - 1];
+            --j;
+        }
+        key[j] = v;
+    }
+    for (int k = 0; k < n; ++k)
+        emit(o, b, N, s + k, static_cast<int>(key[k] & 0xffffffffu), p);
+}
+
+// One CTA per big cell (device-side list); bitonic sort in shared memory for
+// n <= kBigSmemKeys, otherwise an in-place global bitonic network over the
+// index array with keys recomputed on the fly (slow path for pathological
+// clusters).
+__global__ void k_cellsort_big(const float2* __restrict__ pos, int N,
+                               const Geom* __restrict__ geom,
+                               const int32_t* __restrict__ bins,
+                               int32_t* __restrict__ tmp, SortOut o,
+                               const int2* __restrict__ big,
+                               const int32_t* __restrict__ big_count) {
+    extern __shared__ unsigned long long skey[];
+    const int nbig = *big_count;
+    for (int job = blockIdx.x; job < nbig; job += gridDim.x) {
+        const int b = big[job].x, cell = big[job].y;
+        const Geom g = geom[b];
+        const int s = bins[g.bin_off + cell], e = bins[g.bin_off + cell + 1];
+        const int n = e - s;
+        const float2* p = pos + static_cast<size_t>(b) * N;
+        int32_t* t = tmp + static_cast<size_t>(b) * N + s;
+        int np2 = 1;
+        while (np2 < n) np2 <<= 1;
+        if (n <= kBigSmemKeys) {
+            for (int k = threadIdx.x; k < np2; k += blockDim.x)
+                skey[k] = k < n ? sort_key(o.hot, t[k], p, g) : ~0ull;
+            __syncthreads();
+            for (int size = 2; size <= np2; size <<= 1) {
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (int k = threadIdx.x; k < np2; k += blockDim.x) {
+                        const int partner = (stride == (size >> 1))
+                                                ? (k ^ (size - 1))
+                                                : (k ^ stride);
+                        if (partner > k) {
+                            const unsigned long long a = skey[k], c = skey[partner];
+                            if (a > c) {
+                                skey[k] = c;
+                                skey[partner] = a;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            for (int k = threadIdx.x; k < n; k += blockDim.x)
+                emit(o, b, N, s + k, static_cast<int>(skey[k] & 0xffffffffu), p);
+            __syncthreads();
+        } else {
+            // global in-place network over indices; +inf padding never moves
+            // below n with the flip formulation, so partners >= n are skipped.
+            for (int size = 2; size <= np2; size <<= 1) {
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (int k = threadIdx.x; k < np2; k += blockDim.x) {
+                        const int partner = (stride == (size >> 1))
+                                                ? (k ^ (size - 1))
+                                                : (k ^ stride);
+                        if (partner > k && partner < n) {
+                            const int ia = t[k], ic = t[partner];
+                            if (sort_key(o.hot, ia, p, g) > sort_key(o.hot, ic, p, g)) {
+                                t[k] = ic;
+                                t[partner] = ia;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            for (int k = threadIdx.x; k < n; k += blockDim.x) emit(o, b, N, s + k, t[k], p);
+            __syncthreads();
+        }
+    }
+}
+
+}  // namespace
+
+namespace gmi_host {
+
+// axis_cells (bin_grid.cpp:18-24) with a configurable cap
+int host_axis_cells(double span, double cell, int cap) {
+    const double ideal = std::ceil(span / cell) + 2.0;
+    if (!(ideal < static_cast<double>(cap))) return cap;
+    const int v = gmi_dev::x86_d2i(ideal);
+    return std::max(1, v);
+}
+
+void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
+                int cap, bool hot, int32_t* point_index_out,
+                unsigned long long* d_issue) {
+    const int B = c->B, N = c->N;
+    const double cell = c->cutoff;
+    cudaStream_t st = ctx->stream;
+    const float2* p2 = reinterpret_cast<const float2*>(pos);
+
+    // ---- bbox + position validation -> host (one sync: sizes are data
+    // dependent exactly as in the reference) ----
+    uint32_t* d_bbox = static_cast<uint32_t*>(dalloc(ctx, sizeof(uint32_t) * 4 * B));
+    k_bbox_init<<<(B + 127) / 128, 128, 0, st>>>(d_bbox, d_issue, B);
+    GMI_LAUNCHED(ctx);
+    {
+        const int per_img = std::max(1, std::min((N + 1023) / 1024,
+                                                 (4 * ctx->num_sms + B - 1) / B));
+        k_bbox_validate<<<dim3(per_img, B), 256, 0, st>>>(p2, N, d_bbox, d_issue);
+        GMI_LAUNCHED(ctx);
+    }
+    std::vector<uint32_t> bbox(4 * B);
+    std::vector<unsigned long long> issue(B);
+    GMI_CUDA(cudaMemcpyAsync(bbox.data(), d_bbox, sizeof(uint32_t) * 4 * B,
+                             cudaMemcpyDeviceToHost, st));
+    GMI_CUDA(cudaMemcpyAsync(issue.data(), d_issue, sizeof(unsigned long long) * B,
+                             cudaMemcpyDeviceToHost, st));
+    GMI_CUDA(cudaStreamSynchronize(st));
+    dfree(ctx, d_bbox);
+    for (int b = 0; b < B; ++b) {
+        if (issue[b] != kNoIssue) {
+            const long idx = static_cast<long>(issue[b] >> 8);
+            throw GmiFail{GMI_ERR_NON_FINITE_VALUE,
+                          "non-finite position at index " + std::to_string(idx) +
+                              (B > 1 ? " (image " + std::to_string(b) + ")" : "")};
+        }
+    }
+
+    // ---- geometry (bin_grid.cpp:45-60), f64 on the host (IEEE, same ops) ----
+    c->geom_h.resize(B);
+    int64_t off = 0;
+    int max_bins = 0;
+    for (int b = 0; b < B; ++b) {
+        const double mnx = ord2f(bbox[4 * b + 0]), mny = ord2f(bbox[4 * b + 1]);
+        const double mxx = ord2f(bbox[4 * b + 2]), mxy = ord2f(bbox[4 * b + 3]);
+        gmi_dev::Geom g{};
+        g.cell = cell;
+        g.ox = mnx - cell;
+        g.oy = mny - cell;
+        g.n_cols = host_axis_cells(mxx - mnx, cell, cap);
+        g.n_rows = host_axis_cells(mxy - mny, cell, cap);
+        g.capped = (g.n_cols >= cap || g.n_rows >= cap) ? 1 : 0;
+        g.bin_off = off;
+        g.qx0 = static_cast<float>(g.ox);
+        // fine x-columns: 2 per pixel unless the frame is so wide that the
+        // forward's column tables would overflow (see gmi_forward.cu)
+        g.qscale = 2.0f;
+        off += static_cast<int64_t>(g.n_cols) * g.n_rows + 1;
+        max_bins = std::max(max_bins, g.n_cols * g.n_rows);
+        c->geom_h[b] = g;
+    }
+    c->total_bins = off;
+    c->geom_d = static_cast<gmi_dev::Geom*>(cache_alloc(c, sizeof(gmi_dev::Geom) * B));
+    GMI_CUDA(cudaMemcpyAsync(c->geom_d, c->geom_h.data(), sizeof(gmi_dev::Geom) * B,
+                             cudaMemcpyHostToDevice, st));
+    c->bins = static_cast<int32_t*>(cache_alloc(c, sizeof(int32_t) * off));
+    GMI_CUDA(cudaMemsetAsync(c->bins, 0, sizeof(int32_t) * off, st));
+
+    // ---- count ----
+    const size_t BN = static_cast<size_t>(B) * N;
+    int32_t* cellid = static_cast<int32_t*>(dalloc(ctx, sizeof(int32_t) * BN));
+    int32_t* rank = static_cast<int32_t*>(dalloc(ctx, sizeof(int32_t) * BN));
+    const dim3 pgrid((N + 255) / 256, B);
+    k_count<<<pgrid, 256, 0, st>>>(p2, N, c->geom_d, c->bins, cellid, rank);
+    GMI_LAUNCHED(ctx);
+
+    // ---- segmented scan ----
+    std::vector<ScanTile> tiles;
+    std::vector<int32_t> seg_off(B + 1, 0);
+    for (int b = 0; b < B; ++b) {
+        const int64_t len = static_cast<int64_t>(c->geom_h[b].n_cols) * c->geom_h[b].n_rows + 1;
+        for (int64_t s = 0; s < len; s += kScanTile)
+            tiles.push_back({c->geom_h[b].bin_off + s,
+                             static_cast<int32_t>(std::min<int64_t>(kScanTile, len - s)), b});
+        seg_off[b + 1] = static_cast<int32_t>(tiles.size());
+    }
+    const int nt = static_cast<int>(tiles.size());
+    ScanTile* d_tiles = static_cast<ScanTile*>(dalloc(ctx, sizeof(ScanTile) * nt));
+    int32_t* d_tsum = static_cast<int32_t*>(dalloc(ctx, sizeof(int32_t) * nt));
+    int32_t* d_segoff = static_cast<int32_t*>(dalloc(ctx, sizeof(int32_t) * (B + 1)));
+    GMI_CUDA(cudaMemcpyAsync(d_tiles, tiles.data(), sizeof(ScanTile) * nt,
+                             cudaMemcpyHostToDevice, st));
+    GMI_CUDA(cudaMemcpyAsync(d_segoff, seg_off.data(), sizeof(int32_t) * (B + 1),
+                             cudaMemcpyHostToDevice, st));
+    k_scan_reduce<<<nt, kScanThreads, 0, st>>>(c->bins, d_tiles, d_tsum);
+    GMI_LAUNCHED(ctx);
+    k_scan_segments<<<B, 1024, 0, st>>>(d_tsum, d_segoff);
+    GMI_LAUNCHED(ctx);
+    k_scan_apply<<<nt, kScanThreads, 0, st>>>(c->bins, d_tiles, d_tsum);
+    GMI_LAUNCHED(ctx);
+
+    // ---- scatter + per-cell ordering ----
+    int32_t* tmp = static_cast<int32_t*>(dalloc(ctx, sizeof(int32_t) * BN));
+    k_scatter<<<pgrid, 256, 0, st>>>(N, c->geom_d, c->bins, cellid, rank, tmp);
+    GMI_LAUNCHED(ctx);
+
+    SortOut o{};
+    o.hot = hot;
+    if (hot) {
+        o.sx = c->sx;
+        o.sy = c->sy;
+        o.sidx = c->sidx;
+        o.scol = c->scol;
+        o.col = col;
+        o.C = c->C;
+        o.issue = d_issue;
+    } else {
+        o.point_index = point_index_out;
+    }
+    int2* d_big = static_cast<int2*>(dalloc(ctx, sizeof(int2) * std::max<size_t>(1, BN / (kSmallCell + 1) + 1)));
+    int32_t* d_bigcount = static_cast<int32_t*>(dalloc(ctx, sizeof(int32_t)));
+    GMI_CUDA(cudaMemsetAsync(d_bigcount, 0, sizeof(int32_t), st));
+    k_cellsort_small<<<dim3((max_bins + 127) / 128, B), 128, 0, st>>>(
+        p2, N, c->geom_d, c->bins, tmp, o, d_big, d_bigcount);
+    GMI_LAUNCHED(ctx);
+    const int smem = kBigSmemKeys * sizeof(unsigned long long);
+    GMI_CUDA(cudaFuncSetAttribute(k_cellsort_big,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_cellsort_big<<<ctx->num_sms, 1024, smem, st>>>(p2, N, c->geom_d, c->bins, tmp, o,
+                                                     d_big, d_bigcount);
+    GMI_LAUNCHED(ctx);
+
+    dfree(ctx, d_big);
+    dfree(ctx, d_bigcount);
+    dfree(ctx, tmp);
+    dfree(ctx, d_tiles);
+    dfree(ctx, d_tsum);
+    dfree(ctx, d_segoff);
+    dfree(ctx, cellid);
+    dfree(ctx, rank);
+}
+
+}  // namespace gmi_host

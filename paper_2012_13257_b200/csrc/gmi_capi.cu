@@ -1,0 +1,650 @@
+// The C-ABI (include/gmi_b200.h): argument checks with the reference's error
+// codes, the ForwardCache lifecycle and the orchestration of K1..K5 on one
+// stream.  No exception crosses the ABI; every failure becomes a status code
+// plus a thread-local message.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "gmi_internal.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        const int rc = f();
+        if (rc == GMI_OK) g_last_error.clear();
+        return rc;
+    } catch (const GmiFail& e) {
+        return fail(e.code, e.msg);
+    } catch (const std::exception& e) {
+        return fail(GMI_ERR_CUDA, e.what());
+    }
+}
+
+// core.cpp:104-113 (require_valid(InterpConfig)) and core.cpp:115-120
+int check_config(const gmi_config* cfg) {
+    if (cfg == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "config is null");
+    if (!std::isfinite(cfg->sigma) || cfg->sigma <= 0.0)
+        return fail(GMI_ERR_CONFIG_INVALID, "sigma must be positive and finite");
+    if (!std::isfinite(cfg->cutoff_radius) || cfg->cutoff_radius <= 0.0)
+        return fail(GMI_ERR_CONFIG_INVALID, "cutoff_radius must be positive and finite");
+    if (cfg->fallback != GMI_FALLBACK_NEAREST && cfg->fallback != GMI_FALLBACK_ZERO)
+        return fail(GMI_ERR_INVALID_ARGUMENT, "fallback must be NEAREST or ZERO");
+    if (cfg->width < 1 || cfg->height < 1)
+        return fail(GMI_ERR_INVALID_DIMENSIONS, "frame dimensions must be at least 1x1");
+    return GMI_OK;
+}
+
+// core.cpp:55-66 (shape part of validate_point_set; C relaxed to >= 1)
+int check_points(const float* pos, const float* col, int B, int N, int C) {
+    if (B < 1) return fail(GMI_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+    if (N <= 0) return fail(GMI_ERR_EMPTY_POINT_SET, "point set is empty");
+    if (C < 1) return fail(GMI_ERR_SHAPE_MISMATCH, "channels must be >= 1, got " + std::to_string(C));
+    if (pos == nullptr || col == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "null point arrays");
+    if (reinterpret_cast<uintptr_t>(pos) % 8 != 0)
+        return fail(GMI_ERR_INVALID_ARGUMENT, "positions must be 8-byte aligned");
+    if (static_cast<int64_t>(B) * N > (int64_t(1) << 31) - 1)
+        return fail(GMI_ERR_INVALID_ARGUMENT, "batch*num_points exceeds 2^31-1");
+    return GMI_OK;
+}
+
+// Hot-path cell cap: the reference's 2048 (bin_grid.cpp:14) unless the frame
+// itself needs more cells, in which case the cap grows so the output frame
+// is covered without clamping (the 2048 cap puts >1M
+// points in one bin at 8192^2 / r=3).  When the reference grid is not capped
+// the two are identical.
+int hot_cap(const gmi_config* cfg) {
+    const double span = std::max(cfg->width, cfg->height) + 2.0 * cfg->cutoff_radius;
+    const double need = std::ceil(span / cfg->cutoff_radius) + 8.0;
+    const double cap = std::min(8192.0, std::max(2048.0, need));
+    return static_cast<int>(cap);
+}
+
+void ensure_issue(gmi_ctx* ctx, int B) {
+    if (ctx->d_issue_cap < B) {
+        if (ctx->d_issue) cudaFree(ctx->d_issue);
+        if (ctx->h_issue) cudaFreeHost(ctx->h_issue);
+        GMI_CUDA(cudaMalloc(&ctx->d_issue, sizeof(unsigned long long) * B));
+        GMI_CUDA(cudaMallocHost(&ctx->h_issue, sizeof(unsigned long long) * B));
+        ctx->d_issue_cap = B;
+    }
+}
+
+// Reads the colour-validation keys (core.cpp:80-92) after the stream drained.
+int collect_issue(gmi_ctx* ctx, int B) {
+    GMI_CUDA(cudaMemcpyAsync(ctx->h_issue, ctx->d_issue, sizeof(unsigned long long) * B,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int b = 0; b < B; ++b) {
+        const unsigned long long k = ctx->h_issue[b];
+        if (k == gmi_dev::kNoIssue) continue;
+        const long idx = static_cast<long>(k >> 8);
+        const int code = static_cast<int>(k & 0xff);
+        const std::string where = " at index " + std::to_string(idx) +
+                                  (B > 1 ? " (image " + std::to_string(b) + ")" : "");
+        if (code == GMI_ERR_COLOR_OUT_OF_RANGE)
+            return fail(code, "color out of [0,1]" + where);
+        return fail(code, "non-finite value" + where);
+    }
+    return GMI_OK;
+}
+
+void free_cache_buffers(gmi_cache* c) {
+    for (auto& b : c->owned) cudaFreeAsync(b.p, c->ctx->stream);
+    c->owned.clear();
+}
+
+int do_forward(gmi_ctx* ctx, const float* pos, const float* col, int B, int N,
+               int C, const gmi_config* cfg, float* image, gmi_cache* c,
+               int32_t* counts) {
+    c->ctx = ctx;
+    c->B = B;
+    c->N = N;
+    c->C = C;
+    c->W = cfg->width;
+    c->H = cfg->height;
+    c->sigma = cfg->sigma;
+    c->cutoff = cfg->cutoff_radius;
+    c->fallback = cfg->fallback;
+    c->pos = pos;
+    c->col = col;
+    c->image = image;
+    const size_t BN = static_cast<size_t>(B) * N;
+    const size_t BHW = static_cast<size_t>(B) * c->H * c->W;
+    c->sx = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN));
+    c->sy = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN));
+    c->sidx = static_cast<int32_t*>(gmi_host::cache_alloc(c, sizeof(int32_t) * BN));
+    c->scol = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN * C));
+    c->wsum = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BHW));
+    c->special_cap = static_cast<int>(std::min<size_t>(BHW, size_t(1) << 22));
+    c->special = static_cast<Special*>(gmi_host::cache_alloc(c, sizeof(Special) * c->special_cap));
+    c->special_count_d = static_cast<int32_t*>(gmi_host::cache_alloc(c, sizeof(int32_t)));
+    ensure_issue(ctx, B);
+    {
+        PhaseScope ph(ctx, 0);
+        gmi_host::bin_points(ctx, c, pos, col, hot_cap(cfg), true, nullptr, ctx->d_issue);
+    }
+    {
+        PhaseScope ph(ctx, 1);
+        gmi_host::launch_forward(ctx, c, image, counts);
+    }
+    {
+        PhaseScope ph(ctx, 2);
+        gmi_host::launch_special_forward(ctx, c, image, counts);
+    }
+    if (!(ctx->flags & GMI_CTX_ASYNC_ERRORS) || counts != nullptr) {
+        int32_t nspec = 0;
+        GMI_CUDA(cudaMemcpyAsync(&nspec, c->special_count_d, sizeof(int32_t),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+        const int rc = collect_issue(ctx, B);
+        if (rc != GMI_OK) return rc;
+        if (nspec > c->special_cap)
+            return fail(GMI_ERR_OUT_OF_MEMORY,
+                        "more than " + std::to_string(c->special_cap) + " fallback pixels");
+        c->special_count = nspec;
+    }
+    return GMI_OK;
+}
+
+int backward_checks(const gmi_cache* c, int B, int N, int C, const gmi_config* cfg) {
+    // engine.cpp:243-250 (exact ==, including sigma and cutoff)
+    if (c == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "cache is null");
+    if (c->N != N || c->C != C || c->B != B || c->W != cfg->width || c->H != cfg->height ||
+        c->sigma != cfg->sigma || c->cutoff != cfg->cutoff_radius ||
+        c->fallback != cfg->fallback)
+        return fail(GMI_ERR_CACHE_MISMATCH, "forward cache does not match the given inputs");
+    return GMI_OK;
+}
+
+int do_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
+                float* d_colors, float* d_positions) {
+    {
+        PhaseScope ph(ctx, 3);
+        gmi_host::launch_backward(ctx, c, upstream, d_colors, d_positions);
+    }
+    {
+        PhaseScope ph(ctx, 4);
+        gmi_host::launch_special_backward(ctx, c, upstream, d_colors, d_positions);
+    }
+    if (!(ctx->flags & GMI_CTX_ASYNC_ERRORS)) GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+    return GMI_OK;
+}
+
+}  // namespace
+
+namespace gmi_host {
+
+void* dalloc(gmi_ctx* ctx, size_t bytes) {
+    void* p = nullptr;
+    GMI_CUDA(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), ctx->stream));
+    return p;
+}
+
+void dfree(gmi_ctx* ctx, void* p) {
+    if (p) cudaFreeAsync(p, ctx->stream);
+}
+
+void* cache_alloc(gmi_cache* c, size_t bytes) {
+    void* p = dalloc(c->ctx, bytes);
+    c->owned.push_back({p, bytes});
+    return p;
+}
+
+}  // namespace gmi_host
+
+extern "C" {
+
+const char* gmi_last_error(void) { return g_last_error.c_str(); }
+
+const char* gmi_version(void) { return "gmi_b200 0.1.0 (sm_100a)"; }
+
+const char* gmi_error_name(int code) {
+    // error_code_name (core.cpp:7-25), offset by one; B200-side codes after
+    switch (code) {
+        case GMI_OK: return "Ok";
+        case GMI_ERR_NON_FINITE_VALUE: return "NonFiniteValue";
+        case GMI_ERR_COLOR_OUT_OF_RANGE: return "ColorOutOfRange";
+        case GMI_ERR_EMPTY_POINT_SET: return "EmptyPointSet";
+        case GMI_ERR_SHAPE_MISMATCH: return "ShapeMismatch";
+        case GMI_ERR_INVALID_CELL_SIZE: return "InvalidCellSize";
+        case GMI_ERR_CONFIG_INVALID: return "ConfigInvalid";
+        case GMI_ERR_CACHE_MISMATCH: return "CacheMismatch";
+        case GMI_ERR_INVALID_DIMENSIONS: return "InvalidDimensions";
+        case GMI_ERR_CUDA: return "CudaError";
+        case GMI_ERR_INVALID_ARGUMENT: return "InvalidArgument";
+        case GMI_ERR_OUT_OF_MEMORY: return "OutOfMemory";
+    }
+    return "UnknownError";
+}
+
+double gmi_default_cutoff(double sigma) { return 3.0 * sigma; }
+
+double gmi_gaussian_weight(double qx, double qy, double mux, double muy, double sigma) {
+    const double dx = qx - mux;
+    const double dy = qy - muy;
+    return std::exp(-(dx * dx + dy * dy) / (2.0 * sigma * sigma));
+}
+
+int gmi_ctx_create(int device, gmi_ctx** out) {
+    return guarded([&]() -> int {
+        if (out == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "out is null");
+        int n = 0;
+        GMI_CUDA(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n)
+            return fail(GMI_ERR_INVALID_ARGUMENT, "no CUDA device " + std::to_string(device));
+        GMI_CUDA(cudaSetDevice(device));
+        auto* ctx = new gmi_ctx();
+        ctx->device = device;
+        GMI_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+        GMI_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        ctx->own_stream = true;
+        // keep freed stream-ordered memory cached between calls
+        cudaMemPool_t pool;
+        GMI_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thresh = UINT64_MAX;
+        GMI_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+        *out = ctx;
+        return GMI_OK;
+    });
+}
+
+int gmi_ctx_destroy(gmi_ctx* ctx) {
+    if (ctx == nullptr) return GMI_OK;
+    return guarded([&]() -> int {
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->d_issue) cudaFree(ctx->d_issue);
+        if (ctx->h_issue) cudaFreeHost(ctx->h_issue);
+        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        delete ctx;
+        return GMI_OK;
+    });
+}
+
+int gmi_ctx_set_stream(gmi_ctx* ctx, void* stream) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "ctx is null");
+        GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (stream == nullptr) {
+            if (!ctx->own_stream) {
+                GMI_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+                ctx->own_stream = true;
+            }
+            return GMI_OK;
+        }
+        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        ctx->stream = static_cast<cudaStream_t>(stream);
+        ctx->own_stream = false;
+        return GMI_OK;
+    });
+}
+
+void* gmi_ctx_stream(const gmi_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int gmi_ctx_set_flags(gmi_ctx* ctx, uint32_t flags) {
+    if (ctx == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "ctx is null");
+    ctx->flags = flags;
+    return GMI_OK;
+}
+
+int gmi_ctx_synchronize(gmi_ctx* ctx) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "ctx is null");
+        GMI_CUDA(cudaSetDevice(ctx->device));
+        GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (ctx->d_issue_cap > 0) return collect_issue(ctx, ctx->d_issue_cap);
+        return GMI_OK;
+    });
+}
+
+uint64_t gmi_ctx_launch_count(const gmi_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int gmi_ctx_set_profiling(gmi_ctx* ctx, int on) {
+    if (ctx == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "ctx is null");
+    ctx->profiling = on != 0;
+    return GMI_OK;
+}
+
+int gmi_ctx_phase_times(gmi_ctx* ctx, double* ms, uint64_t* calls, int reset) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "ctx is null");
+        GMI_CUDA(cudaSetDevice(ctx->device));
+        GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (auto& m : ctx->marks) {
+            float t = 0.f;
+            GMI_CUDA(cudaEventElapsedTime(&t, m.start, m.stop));
+            ctx->phase_ms[m.phase] += t;
+            ctx->phase_calls[m.phase] += 1;
+            cudaEventDestroy(m.start);
+            cudaEventDestroy(m.stop);
+        }
+        ctx->marks.clear();
+        for (int k = 0; k < GMI_NUM_PHASES; ++k) {
+            if (ms) ms[k] = ctx->phase_ms[k];
+            if (calls) calls[k] = ctx->phase_calls[k];
+            if (reset) {
+                ctx->phase_ms[k] = 0;
+                ctx->phase_calls[k] = 0;
+            }
+        }
+        return GMI_OK;
+    });
+}
+
+int gmi_forward(gmi_ctx* ctx, const float* positions, const float* colors, int32_t batch,
+                int32_t num_points, int32_t channels, const gmi_config* cfg, float* image,
+                gmi_cache** cache_out) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr || cache_out == nullptr || image == nullptr)
+            return fail(GMI_ERR_INVALID_ARGUMENT, "null argument");
+        int rc = check_points(positions, colors, batch, num_points, channels);
+        if (rc) return rc;
+        rc = check_config(cfg);
+        if (rc) return rc;
+        GMI_CUDA(cudaSetDevice(ctx->device));
+        auto* c = new gmi_cache();
+        c->ctx = ctx;
+        try {
+            rc = do_forward(ctx, positions, colors, batch, num_points, channels, cfg, image, c,
+                            nullptr);
+        } catch (...) {
+            free_cache_buffers(c);
+            delete c;
+            throw;
+        }
+        if (rc != GMI_OK) {
+            free_cache_buffers(c);
+            delete c;
+            return rc;
+        }
+        *cache_out = c;
+        return GMI_OK;
+    });
+}
+
+int gmi_backward(gmi_ctx* ctx, const float* positions, const float* colors, int32_t batch,
+                 int32_t num_points, int32_t channels, const gmi_config* cfg,
+                 const gmi_cache* cache, const float* upstream, float* d_colors,
+                 float* d_positions) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr || upstream == nullptr || d_colors == nullptr || d_positions == nullptr)
+            return fail(GMI_ERR_INVALID_ARGUMENT, "null argument");
+        int rc = check_points(positions, colors, batch, num_points, channels);
+        if (rc) return rc;
+        rc = check_config(cfg);
+        if (rc) return rc;
+        rc = backward_checks(cache, batch, num_points, channels, cfg);
+        if (rc) return rc;
+        GMI_CUDA(cudaSetDevice(ctx->device));
+        return do_backward(ctx, cache, upstream, d_colors, d_positions);
+    });
+}
+
+int gmi_forward_host(gmi_ctx* ctx, const float* positions, const float* colors, int32_t batch,
+                     int32_t num_points, int32_t channels, const gmi_config* cfg, float* image,
+                     gmi_cache** cache_out) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr || cache_out == nullptr || image == nullptr)
+            return fail(GMI_ERR_INVALID_ARGUMENT, "null argument");
+        int rc = check_points(positions, colors, batch, num_points, channels);
+        if (rc) return rc;
+        rc = check_config(cfg);
+        if (rc) return rc;
+        GMI_CUDA(cudaSetDevice(ctx->device));
+        auto* c = new gmi_cache();
+        c->ctx = ctx;
+        const size_t BN = static_cast<size_t>(batch) * num_points;
+        const size_t img = static_cast<size_t>(batch) * cfg->height * cfg->width * channels;
+        try {
+            float* dpos = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN * 2));
+            float* dcol = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN * channels));
+            float* dimg = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * img));
+            GMI_CUDA(cudaMemcpyAsync(dpos, positions, sizeof(float) * BN * 2,
+                                     cudaMemcpyHostToDevice, ctx->stream));
+            GMI_CUDA(cudaMemcpyAsync(dcol, colors, sizeof(float) * BN * channels,
+                                     cudaMemcpyHostToDevice, ctx->stream));
+            const uint32_t saved = ctx->flags;
+            ctx->flags &= ~GMI_CTX_ASYNC_ERRORS;
+            rc = do_forward(ctx, dpos, dcol, batch, num_points, channels, cfg, dimg, c, nullptr);
+            ctx->flags = saved;
+            if (rc == GMI_OK) {
+                GMI_CUDA(cudaMemcpyAsync(image, dimg, sizeof(float) * img, cudaMemcpyDeviceToHost,
+                                         ctx->stream));
+                GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+            }
+        } catch (...) {
+            free_cache_buffers(c);
+            delete c;
+            throw;
+        }
+        if (rc != GMI_OK) {
+            free_cache_buffers(c);
+            delete c;
+            return rc;
+        }
+        *cache_out = c;
+        return GMI_OK;
+    });
+}
+
+int gmi_backward_host(gmi_ctx* ctx, const float* positions, const float* colors, int32_t batch,
+                      int32_t num_points, int32_t channels, const gmi_config* cfg,
+                      const gmi_cache* cache, const float* upstream, float* d_colors,
+                      float* d_positions) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr || upstream == nullptr || d_colors == nullptr || d_positions == nullptr)
+            return fail(GMI_ERR_INVALID_ARGUMENT, "null argument");
+        int rc = check_points(positions, colors, batch, num_points, channels);
+        if (rc) return rc;
+        rc = check_config(cfg);
+        if (rc) return rc;
+        rc = backward_checks(cache, batch, num_points, channels, cfg);
+        if (rc) return rc;
+        GMI_CUDA(cudaSetDevice(ctx->device));
+        const size_t BN = static_cast<size_t>(batch) * num_points;
+        const size_t img = static_cast<size_t>(batch) * cfg->height * cfg->width * channels;
+        float* dup = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * img));
+        float* dc = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * BN * channels));
+        float* dp = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * BN * 2));
+        GMI_CUDA(cudaMemcpyAsync(dup, upstream, sizeof(float) * img, cudaMemcpyHostToDevice,
+                                 ctx->stream));
+        {
+            PhaseScope ph(ctx, 3);
+            gmi_host::launch_backward(ctx, cache, dup, dc, dp);
+        }
+        {
+            PhaseScope ph(ctx, 4);
+            gmi_host::launch_special_backward(ctx, cache, dup, dc, dp);
+        }
+        GMI_CUDA(cudaMemcpyAsync(d_colors, dc, sizeof(float) * BN * channels,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+        GMI_CUDA(cudaMemcpyAsync(d_positions, dp, sizeof(float) * BN * 2, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+        gmi_host::dfree(ctx, dup);
+        gmi_host::dfree(ctx, dc);
+        gmi_host::dfree(ctx, dp);
+        GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+        return GMI_OK;
+    });
+}
+
+void gmi_cache_free(gmi_cache* c) {
+    if (c == nullptr) return;
+    cudaSetDevice(c->ctx->device);
+    free_cache_buffers(c);
+    delete c;
+}
+
+int gmi_cache_shape(const gmi_cache* c, int32_t* batch, int32_t* num_points, int32_t* channels,
+                    int32_t* width, int32_t* height) {
+    if (c == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "cache is null");
+    if (batch) *batch = c->B;
+    if (num_points) *num_points = c->N;
+    if (channels) *channels = c->C;
+    if (width) *width = c->W;
+    if (height) *height = c->H;
+    return GMI_OK;
+}
+
+static int read_special(const gmi_cache* c, std::vector<Special>& sp) {
+    GMI_CUDA(cudaSetDevice(c->ctx->device));
+    int32_t n = 0;
+    GMI_CUDA(cudaMemcpyAsync(&n, c->special_count_d, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                             c->ctx->stream));
+    GMI_CUDA(cudaStreamSynchronize(c->ctx->stream));
+    n = std::min(n, c->special_cap);
+    sp.resize(n);
+    if (n > 0) {
+        GMI_CUDA(cudaMemcpyAsync(sp.data(), c->special, sizeof(Special) * n,
+                                 cudaMemcpyDeviceToHost, c->ctx->stream));
+        GMI_CUDA(cudaStreamSynchronize(c->ctx->stream));
+    }
+    return GMI_OK;
+}
+
+int gmi_cache_fallback_count(const gmi_cache* c, int64_t* out) {
+    return guarded([&]() -> int {
+        if (c == nullptr || out == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "null argument");
+        std::vector<Special> sp;
+        read_special(c, sp);
+        for (int b = 0; b < c->B; ++b) out[b] = 0;
+        for (const auto& s : sp)
+            if (s.kind == 1) out[s.b]++;
+        return GMI_OK;
+    });
+}
+
+int gmi_cache_copy_pixels(const gmi_cache* c, float* normalizer, uint8_t* fallback_flag,
+                          int32_t* nearest_index) {
+    return guarded([&]() -> int {
+        if (c == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "cache is null");
+        const size_t BHW = static_cast<size_t>(c->B) * c->H * c->W;
+        std::vector<Special> sp;
+        read_special(c, sp);
+        if (normalizer) {
+            GMI_CUDA(cudaMemcpyAsync(normalizer, c->wsum, sizeof(float) * BHW,
+                                     cudaMemcpyDeviceToHost, c->ctx->stream));
+            GMI_CUDA(cudaStreamSynchronize(c->ctx->stream));
+        }
+        if (fallback_flag) std::memset(fallback_flag, 0, BHW);
+        if (nearest_index)
+            for (size_t k = 0; k < BHW; ++k) nearest_index[k] = -1;
+        for (const auto& s : sp) {
+            const size_t k = static_cast<size_t>(s.b) * c->H * c->W + s.pix;
+            if (s.kind == 1) {
+                if (fallback_flag) fallback_flag[k] = 1;
+                if (nearest_index) nearest_index[k] = s.nearest;
+            } else if (s.kind == 2 && normalizer) {
+                normalizer[k] = NAN;  // exact (f64) pixel: normaliser not representable
+            }
+        }
+        return GMI_OK;
+    });
+}
+
+int gmi_forward_counts(gmi_ctx* ctx, const gmi_cache* cache, int32_t* counts) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr || cache == nullptr || counts == nullptr)
+            return fail(GMI_ERR_INVALID_ARGUMENT, "null argument");
+        GMI_CUDA(cudaSetDevice(ctx->device));
+        // Re-run the same forward pipeline with the counting instantiation of
+        // the gather kernel into scratch image/cache buffers.
+        const size_t BHW = static_cast<size_t>(cache->B) * cache->H * cache->W;
+        gmi_config cfg{cache->sigma, cache->cutoff, cache->fallback, cache->W, cache->H};
+        gmi_cache tmp;
+        tmp.ctx = ctx;
+        float* img = static_cast<float*>(gmi_host::cache_alloc(&tmp, sizeof(float) * BHW * cache->C));
+        int32_t* dcounts = static_cast<int32_t*>(gmi_host::cache_alloc(&tmp, sizeof(int32_t) * BHW));
+        int rc = do_forward(ctx, cache->pos, cache->col, cache->B, cache->N, cache->C, &cfg, img,
+                            &tmp, dcounts);
+        if (rc == GMI_OK) {
+            GMI_CUDA(cudaMemcpyAsync(counts, dcounts, sizeof(int32_t) * BHW, cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+            GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+        free_cache_buffers(&tmp);
+        return rc;
+    });
+}
+
+int gmi_bin_grid(gmi_ctx* ctx, const float* positions, int32_t batch, int32_t num_points,
+                 double cell_size, double* origin, int32_t* n_cols, int32_t* n_rows,
+                 int32_t* bin_start, int32_t* point_index) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr || positions == nullptr || origin == nullptr || n_cols == nullptr ||
+            n_rows == nullptr)
+            return fail(GMI_ERR_INVALID_ARGUMENT, "null argument");
+        if (batch < 1) return fail(GMI_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+        if (num_points <= 0) return fail(GMI_ERR_EMPTY_POINT_SET, "point set is empty");
+        // bin_grid.cpp:40-43
+        if (!std::isfinite(cell_size) || cell_size <= 0.0)
+            return fail(GMI_ERR_INVALID_CELL_SIZE, "cell_size must be positive and finite");
+        GMI_CUDA(cudaSetDevice(ctx->device));
+        gmi_cache c;
+        c.ctx = ctx;
+        c.B = batch;
+        c.N = num_points;
+        c.C = 1;
+        c.cutoff = cell_size;
+        ensure_issue(ctx, batch);
+        const size_t BN = static_cast<size_t>(batch) * num_points;
+        int32_t* d_pi = nullptr;
+        int rc = GMI_OK;
+        try {
+            d_pi = static_cast<int32_t*>(gmi_host::cache_alloc(&c, sizeof(int32_t) * BN));
+            gmi_host::bin_points(ctx, &c, positions, nullptr, 2048, false, d_pi, ctx->d_issue);
+            for (int b = 0; b < batch; ++b) {
+                origin[2 * b] = c.geom_h[b].ox;
+                origin[2 * b + 1] = c.geom_h[b].oy;
+                n_cols[b] = c.geom_h[b].n_cols;
+                n_rows[b] = c.geom_h[b].n_rows;
+            }
+            if (bin_start != nullptr) {
+                GMI_CUDA(cudaMemcpyAsync(bin_start, c.bins, sizeof(int32_t) * c.total_bins,
+                                         cudaMemcpyDeviceToHost, ctx->stream));
+            }
+            if (point_index != nullptr) {
+                GMI_CUDA(cudaMemcpyAsync(point_index, d_pi, sizeof(int32_t) * BN,
+                                         cudaMemcpyDeviceToHost, ctx->stream));
+            }
+            GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+            free_cache_buffers(&c);
+            throw;
+        }
+        free_cache_buffers(&c);
+        return rc;
+    });
+}
+
+int gmi_bin_grid_host(gmi_ctx* ctx, const float* positions, int32_t batch, int32_t num_points,
+                      double cell_size, double* origin, int32_t* n_cols, int32_t* n_rows,
+                      int32_t* bin_start, int32_t* point_index) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr || positions == nullptr)
+            return fail(GMI_ERR_INVALID_ARGUMENT, "null argument");
+        if (batch < 1) return fail(GMI_ERR_INVALID_ARGUMENT, "batch must be >= 1");
+        if (num_points <= 0) return fail(GMI_ERR_EMPTY_POINT_SET, "point set is empty");
+        GMI_CUDA(cudaSetDevice(ctx->device));
+        const size_t bytes = sizeof(float) * 2 * static_cast<size_t>(batch) * num_points;
+        float* d = static_cast<float*>(gmi_host::dalloc(ctx, bytes));
+        GMI_CUDA(cudaMemcpyAsync(d, positions, bytes, cudaMemcpyHostToDevice, ctx->stream));
+        const int rc = gmi_bin_grid(ctx, d, batch, num_points, cell_size, origin, n_cols, n_rows,
+                                    bin_start, point_index);
+        gmi_host::dfree(ctx, d);
+        GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+        return rc;
+    });
+}
+
+}  // extern "C"

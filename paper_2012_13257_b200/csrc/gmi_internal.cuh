@@ -1,0 +1,156 @@
+// Host-side internals shared by the .cu translation units: the context, the
+// ForwardCache analogue and the kernel launchers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "gmi_b200.h"
+#include "gmi_common.cuh"
+
+// Error carried from deep inside the launch code back to the C-ABI.
+struct GmiFail {
+    int code;
+    std::string msg;
+};
+
+#define GMI_CUDA(call)                                                    \
+    do {                                                                  \
+        cudaError_t e_ = (call);                                          \
+        if (e_ != cudaSuccess) {                                          \
+            throw GmiFail{e_ == cudaErrorMemoryAllocation ? GMI_ERR_OUT_OF_MEMORY \
+                                                          : GMI_ERR_CUDA, \
+                          std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+        }                                                                 \
+    } while (0)
+
+#define GMI_LAUNCHED(ctx)                                                 \
+    do {                                                                  \
+        (ctx)->launches++;                                                \
+        GMI_CUDA(cudaGetLastError());                                     \
+    } while (0)
+
+struct gmi_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    uint32_t flags = 0;
+    uint64_t launches = 0;
+    // pending asynchronous validation result (GMI_CTX_ASYNC_ERRORS)
+    unsigned long long* h_issue = nullptr;  // pinned, per image
+    int h_issue_cap = 0;
+    std::vector<int> pending_codes;
+    std::string pending_msg;
+    int pending_code = 0;
+    // device scratch for validation keys
+    unsigned long long* d_issue = nullptr;
+    int d_issue_cap = 0;
+    // optional per-phase CUDA-event timing (gmi_ctx_set_profiling)
+    bool profiling = false;
+    struct PhaseMark {
+        int phase;
+        cudaEvent_t start, stop;
+    };
+    std::vector<PhaseMark> marks;
+    double phase_ms[GMI_NUM_PHASES] = {0};
+    uint64_t phase_calls[GMI_NUM_PHASES] = {0};
+};
+
+// RAII phase marker: records an event pair on the ctx stream when profiling.
+struct PhaseScope {
+    gmi_ctx* ctx;
+    int phase;
+    cudaEvent_t start = nullptr;
+    PhaseScope(gmi_ctx* c, int ph) : ctx(c), phase(ph) {
+        if (ctx->profiling) {
+            cudaEventCreate(&start);
+            cudaEventRecord(start, ctx->stream);
+        }
+    }
+    ~PhaseScope() {
+        if (ctx->profiling && start) {
+            cudaEvent_t stop;
+            cudaEventCreate(&stop);
+            cudaEventRecord(stop, ctx->stream);
+            ctx->marks.push_back({phase, start, stop});
+        }
+    }
+};
+
+// A stream-ordered device allocation owned by a cache.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+// Per special pixel (fallback or exact-f64 pixel), produced by the forward.
+struct Special {
+    int32_t b;
+    int32_t pix;      // r * W + c
+    int32_t nearest;  // original point index (NearestPoint fallback) or -1
+    int32_t kind;     // 1 = fallback, 2 = exact (f64 weights)
+};
+
+struct gmi_cache {
+    gmi_ctx* ctx = nullptr;
+    int B = 0, N = 0, C = 0, W = 0, H = 0;
+    double sigma = 0, cutoff = 0;
+    int fallback = 0;
+    // borrowed device pointers (owned when host API was used)
+    const float* pos = nullptr;
+    const float* col = nullptr;
+    const float* image = nullptr;
+    std::vector<DevBuf> owned;
+    // binning
+    std::vector<gmi_dev::Geom> geom_h;
+    gmi_dev::Geom* geom_d = nullptr;
+    int32_t* bins = nullptr;  // concatenated bin_start per image
+    int64_t total_bins = 0;
+    // hot layout (sorted by cell, then fine x-column, then index)
+    float* sx = nullptr;      // [B][N]
+    float* sy = nullptr;      // [B][N]
+    int32_t* sidx = nullptr;  // [B][N] original point index
+    float* scol = nullptr;    // [B][C][N] channel-planar
+    // per pixel
+    float* wsum = nullptr;    // [B][H][W]; 0 => special pixel
+    // special pixels
+    Special* special = nullptr;
+    int32_t* special_count_d = nullptr;
+    int special_cap = 0;
+    int special_count = -1;   // host copy (-1 = not read yet)
+    bool special_overflow = false;
+};
+
+namespace gmi_host {
+
+// memory (stream-ordered)
+void* dalloc(gmi_ctx* ctx, size_t bytes);
+void dfree(gmi_ctx* ctx, void* p);
+void* cache_alloc(gmi_cache* c, size_t bytes);
+
+// ---- binning (gmi_bin.cu) ----
+// Validates positions, computes bbox, geometry (cap) and fills c->geom_*,
+// c->bins; when hot_layout, builds the sorted SoA (and validates colours),
+// else (reference export) writes point_index[B][N].
+void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
+                int cap, bool hot_layout, int32_t* point_index_out,
+                unsigned long long* d_issue);
+int host_axis_cells(double span, double cell, int cap);
+
+// ---- forward (gmi_forward.cu) ----
+void launch_forward(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts);
+void launch_special_forward(gmi_ctx* ctx, gmi_cache* c, float* image,
+                            int32_t* counts);
+
+// ---- backward (gmi_backward.cu) ----
+void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
+                     float* d_colors, float* d_positions);
+void launch_special_backward(gmi_ctx* ctx, const gmi_cache* c,
+                             const float* upstream, float* d_colors,
+                             float* d_positions);
+
+}  // namespace gmi_host

@@ -1,0 +1,253 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bit-exact: bin grid (origin, n_cols, n_rows, bin_start, point_index), fallback
+set, nearest indices, per-pixel contribution counts.  Tolerance (north star):
+|a-b| <= 1e-6 + 1e-5*max(|a|,|b|) for image, d_colors, d_positions.
+Inputs are fp32-representable so both sides see identical values.
+"""
+import numpy as np
+import pytest
+
+from conftest import assert_close
+
+pytestmark = pytest.mark.gpu
+
+
+def f32(a):
+    return np.asarray(a, np.float32).astype(np.float64)
+
+
+def run_gpu(gmi, ctx, pos, col, w, h, sigma, cutoff, up=None, fallback="nearest"):
+    pos = np.asarray(pos, np.float32).reshape(1, -1, 2)
+    col = np.asarray(col, np.float32).reshape(1, pos.shape[1], -1)
+    img, cache = gmi.forward_batch(pos, col, w, h, sigma, cutoff, fallback, ctx=ctx)
+    out = dict(image=img[0], cache=cache)
+    if up is not None:
+        dc, dp = gmi.backward_batch(pos, col, cache, np.asarray(up, np.float32)[None], sigma,
+                                    cutoff, fallback, ctx=ctx)
+        out.update(dc=dc[0], dp=dp[0])
+    return out
+
+
+def check_instance(gmi, ctx, orc, pos, col, w, h, sigma, cutoff, fallback=0, seed=0,
+                   counts=True):
+    pos = f32(pos)
+    col = f32(col)
+    rng = np.random.default_rng(seed)
+    up = f32(rng.uniform(-1, 1, (h, w, col.shape[1])))
+    fb = "nearest" if fallback == 0 else "zero"
+    g = run_gpu(gmi, ctx, pos, col, w, h, sigma, cutoff, up, fb)
+    r = orc.forward(pos, col, w, h, sigma, cutoff, fallback)
+    rdc, rdp = orc.backward(pos, col, r, up, sigma, cutoff, fallback)
+    norm, flag, near = g["cache"].pixels()
+    assert np.array_equal(flag[0], r["fallback_flag"]), "fallback set differs"
+    assert np.array_equal(near[0], np.where(r["fallback_flag"] == 1, r["nearest_index"], -1)
+                          if fallback == 0 else np.full_like(near[0], -1)), "nearest differs"
+    if counts:
+        cnt = gmi.forward_counts(g["cache"])
+        assert np.array_equal(cnt[0], r["counts"]), "per-pixel contribution counts differ"
+    assert_close(g["image"], r["image"], what="image")
+    ok = ~np.isnan(norm[0]) & (r["fallback_flag"] == 0)
+    assert_close(norm[0][ok], r["normalizer"][ok], what="normalizer")
+    assert_close(g["dc"], rdc, what="d_colors")
+    assert_close(g["dp"], rdp, what="d_positions")
+    return g, r
+
+
+# ---------------------------------------------------------------- KATs ----
+def test_three_point_mixture(gmi, ctx):
+    # test_engine.cpp:53-70: e^-0.25/(e^-0.25 + 2e^-1.25) at q=(0.5,0.5)
+    ps = gmi.PointSet([[-0.5, -0.5], [1.5, -0.5], [-0.5, 1.5]], [[1.0], [0.0], [0.0]])
+    img, cache = gmi.forward(ps, 1, 1, 1.0, radius=10.0)
+    assert img[0, 0, 0] == pytest.approx(0.5761168847658291, rel=1e-6)
+
+
+def test_single_point_paints_everywhere(gmi, ctx):
+    # test_engine.cpp:26-40
+    ps = gmi.PointSet([[3.7, -2.1]], [[0.7]])
+    img, cache = gmi.forward(ps, 5, 4, 1.0)
+    assert np.allclose(img, 0.7, rtol=1e-6, atol=0)
+    norm, flag, near = cache.pixels()
+    assert cache.fallback_count == int((flag == 1).sum())
+
+
+def test_equidistant_two_points(gmi, ctx):
+    # test_engine.cpp:42-51
+    ps = gmi.PointSet([[0, 1], [2, 1]], [[0.2], [0.8]])
+    img, _ = gmi.forward(ps, 3, 3, 1.0)
+    assert img[1, 1, 0] == pytest.approx(0.5, rel=1e-6)
+
+
+@pytest.mark.parametrize("fallback,value", [("nearest", 0.9), ("zero", 0.0)])
+def test_fallback_out_of_range(gmi, ctx, fallback, value):
+    # test_engine.cpp:217-239
+    ps = gmi.PointSet([[100, 100], [200, 200]], [[0.9], [0.1]])
+    img, cache = gmi.forward(ps, 4, 4, 1.0, radius=2.0, fallback=fallback)
+    assert cache.fallback_count == 16
+    assert np.all(img == np.float32(value).astype(np.float64))
+
+
+def test_total_underflow_falls_back(gmi, ctx):
+    # test_engine.cpp:241-249
+    ps = gmi.PointSet([[1000.0, 0.0]], [[0.6]])
+    img, cache = gmi.forward(ps, 1, 1, 0.5, radius=10000.0)
+    assert cache.fallback_count == 1
+    assert img[0, 0, 0] == np.float64(np.float32(0.6))
+
+
+def test_backward_single_point_unit_upstream(gmi, ctx):
+    # test_engine.cpp:302-311
+    ps = gmi.PointSet([[2, 2]], [[0.5]])
+    img, cache = gmi.forward(ps, 6, 5, 1.0, radius=100.0)
+    dc, dp = gmi.backward(ps, cache, np.ones((5, 6, 1)), 1.0, radius=100.0)
+    assert dc[0, 0] == pytest.approx(30.0, rel=1e-6)
+    assert abs(dp[0, 0]) < 1e-6 and abs(dp[0, 1]) < 1e-6
+
+
+def test_fallback_gradient_routing(gmi, ctx):
+    # test_engine.cpp:347-370
+    ps = gmi.PointSet([[-50, 0], [-60, 0]], [[0.3], [0.7]])
+    img, cache = gmi.forward(ps, 2, 2, 1.0, radius=3.0)
+    assert cache.fallback_count == 4
+    dc, dp = gmi.backward(ps, cache, np.ones((2, 2, 1)), 1.0, radius=3.0)
+    assert dc[0, 0] == 4.0 and dc[1, 0] == 0.0
+    assert np.all(dp == 0.0)
+    img0, cache0 = gmi.forward(ps, 2, 2, 1.0, radius=3.0, fallback="zero")
+    dc0, dp0 = gmi.backward(ps, cache0, np.ones((2, 2, 1)), 1.0, radius=3.0, fallback="zero")
+    assert np.all(dc0 == 0.0) and np.all(dp0 == 0.0)
+
+
+def test_cache_mismatch_and_validation(gmi, ctx):
+    # test_engine.cpp:372-400, core.cpp:55-120
+    ps = gmi.PointSet([[0.5, 0.5], [3.0, 1.0]], [[0.5], [0.25]])
+    img, cache = gmi.forward(ps, 4, 4, 1.0)
+    with pytest.raises(gmi.GmiError) as e:
+        gmi.backward(ps, cache, np.ones((4, 4, 1)), 2.0, radius=6.0)
+    assert e.value.name == "CacheMismatch"
+    with pytest.raises(gmi.GmiError):
+        gmi.backward(ps, cache, np.ones((5, 4, 1)), 1.0)
+    with pytest.raises(gmi.GmiError) as e:
+        gmi.forward(ps, 0, 5, 1.0)
+    assert e.value.name == "InvalidDimensions"
+    with pytest.raises(gmi.GmiError) as e:
+        gmi.forward(ps, 4, 4, -1.0, radius=3.0)
+    assert e.value.name == "ConfigInvalid"
+    # device-side validation of raw batch arrays
+    pos = np.zeros((1, 3, 2), np.float32)
+    col = np.full((1, 3, 1), 0.5, np.float32)
+    pos[0, 2, 0] = np.nan
+    with pytest.raises(gmi.GmiError) as e:
+        gmi.forward_batch(pos, col, 4, 4, 1.0, ctx=ctx)
+    assert e.value.name == "NonFiniteValue" and "index 2" in str(e.value)
+    pos[0, 2, 0] = 1.0
+    col[0, 1, 0] = 1.5
+    with pytest.raises(gmi.GmiError) as e:
+        gmi.forward_batch(pos, col, 4, 4, 1.0, ctx=ctx)
+    assert e.value.name == "ColorOutOfRange" and "index 1" in str(e.value)
+
+
+# ------------------------------------------------------------- binning ----
+@pytest.mark.parametrize("n,extent,cell", [(4096, 128, 3.0), (5000, 8192, 3.0), (1, 10, 1.0),
+                                           (3000, 64, 0.37), (20000, 300, 4.5)])
+def test_bin_grid_bit_exact(gmi, ctx, orc, n, extent, cell):
+    rng = np.random.default_rng(n)
+    pos = f32(rng.uniform(-0.5, extent - 0.5, (n, 2)))
+    got = gmi.bin_grid(pos, cell, ctx=ctx)
+    want = orc.bin_grid(pos, cell)
+    assert np.array_equal(got["origin"], want["origin"])
+    assert (got["n_cols"], got["n_rows"]) == (want["n_cols"], want["n_rows"])
+    assert np.array_equal(got["bin_start"], want["bin_start"])
+    assert np.array_equal(got["point_index"], want["point_index"])
+
+
+def test_bin_grid_clustered_big_cells(gmi, ctx, orc):
+    rng = np.random.default_rng(5)
+    pos = f32(np.concatenate([rng.uniform(0, 400, (3000, 2)), rng.uniform(100, 103, (9000, 2)),
+                              np.full((20, 2), 7.0)]))
+    got = gmi.bin_grid(pos, 12.0, ctx=ctx)
+    want = orc.bin_grid(pos, 12.0)
+    assert np.array_equal(got["bin_start"], want["bin_start"])
+    assert np.array_equal(got["point_index"], want["point_index"])
+
+
+# ------------------------------------------------- forward + backward ----
+@pytest.mark.parametrize("seed", [21, 22, 23, 24, 31, 77])
+def test_random_instances_truncated(gmi, ctx, orc, seed):
+    rng = np.random.default_rng(seed)
+    w, h = int(rng.integers(1, 30)), int(rng.integers(1, 30))
+    n = int(rng.integers(1, 60))
+    ch = int(rng.choice([1, 3]))
+    pos = np.stack([rng.uniform(-1, w, n), rng.uniform(-1, h, n)], 1)
+    col = rng.uniform(0, 1, (n, ch))
+    sigma = float(rng.uniform(0.5, 4.0))
+    for cutoff in (3 * sigma, 1.0, 2.5):
+        for fb in (0, 1):
+            check_instance(gmi, ctx, orc, pos, col, w, h, sigma, cutoff, fb, seed)
+
+
+def test_config1_shape(gmi, ctx, orc):
+    pos, col, up = orc.synth_batch(1, 1, 4096, 3, 128, 128)
+    check_instance(gmi, ctx, orc, pos[0], col[0], 128, 128, 1.0, 3.0)
+
+
+def test_sparse_with_many_fallbacks(gmi, ctx, orc):
+    pos, col, up = orc.synth_batch(3, 1, 2000, 3, 256, 256)
+    check_instance(gmi, ctx, orc, pos[0], col[0], 256, 256, 1.0, 3.0)
+
+
+@pytest.mark.parametrize("ch", [1, 2, 5, 9])
+def test_channel_counts(gmi, ctx, orc, ch):
+    pos, col, up = orc.synth_batch(9, 1, 3000, ch, 96, 80)
+    check_instance(gmi, ctx, orc, pos[0], col[0], 96, 80, 1.5, 4.5)
+
+
+def test_integer_lattice_exact_ties(gmi, ctx, orc):
+    # integer positions at r=3: d^2 == r^2 exactly for many pairs (closed ball)
+    xs, ys = np.meshgrid(np.arange(0, 40, 3), np.arange(0, 30, 3))
+    pos = np.stack([xs.ravel(), ys.ravel()], 1).astype(np.float64)
+    rng = np.random.default_rng(1)
+    col = rng.uniform(0, 1, (pos.shape[0], 3))
+    check_instance(gmi, ctx, orc, pos, col, 40, 30, 1.0, 3.0)
+    check_instance(gmi, ctx, orc, pos + 0.5, col, 40, 30, 1.0, 3.0)
+
+
+def test_duplicates_and_single_pixel(gmi, ctx, orc):
+    pos = np.array([[1, 1], [1, 1], [1, 1], [0.25, 0.75]], np.float64)
+    col = np.array([[0.1], [0.2], [0.3], [0.9]])
+    check_instance(gmi, ctx, orc, pos, col, 3, 3, 1.0, 2.0)
+    check_instance(gmi, ctx, orc, pos, col, 1, 1, 1.0, 2.0)
+
+
+def test_huge_cutoff_underflow_exact_path(gmi, ctx, orc):
+    # untruncated radius: fp32 weights underflow where f64 ones do not
+    rng = np.random.default_rng(4)
+    pos = np.stack([rng.uniform(-1, 24, 12), rng.uniform(-1, 20, 12)], 1)
+    col = rng.uniform(0, 1, (12, 3))
+    check_instance(gmi, ctx, orc, pos, col, 24, 20, 0.5, 60.0)
+
+
+def test_batch_equals_single_calls(gmi, ctx, orc):
+    pos, col, up = orc.synth_batch(11, 3, 3000, 3, 100, 90)
+    img, cache = gmi.forward_batch(pos, col, 100, 90, 1.0, 3.0, ctx=ctx)
+    dc, dp = gmi.backward_batch(pos, col, cache, up, 1.0, 3.0, ctx=ctx)
+    for b in range(3):
+        i1, c1 = gmi.forward_batch(pos[b:b + 1], col[b:b + 1], 100, 90, 1.0, 3.0, ctx=ctx)
+        d1, p1 = gmi.backward_batch(pos[b:b + 1], col[b:b + 1], c1, up[b:b + 1], 1.0, 3.0, ctx=ctx)
+        assert np.array_equal(img[b], i1[0])
+        assert np.array_equal(dc[b], d1[0]) and np.array_equal(dp[b], p1[0])
+
+
+def test_deterministic_repeat(gmi, ctx, orc):
+    pos, col, up = orc.synth_batch(12, 2, 20000, 3, 256, 256)
+    a = gmi.forward_batch(pos, col, 256, 256, 1.5, 4.5, ctx=ctx)
+    b = gmi.forward_batch(pos, col, 256, 256, 1.5, 4.5, ctx=ctx)
+    assert np.array_equal(a[0], b[0])
+    ga = gmi.backward_batch(pos, col, a[1], up, 1.5, 4.5, ctx=ctx)
+    gb = gmi.backward_batch(pos, col, b[1], up, 1.5, 4.5, ctx=ctx)
+    assert np.array_equal(ga[0], gb[0]) and np.array_equal(ga[1], gb[1])
+
+
+def test_smoke_entry():
+    import __graft_entry__
+
+    __graft_entry__.smoke()
