@@ -1,23 +1,30 @@
 // K4 — backward (engine.cpp:190-234 backward_rows, engine.cpp:238-309).
 //
-// Point-major and atomic-free: a CTA takes a block of reference cells, stages
-// the per-pixel quantities of the pixels those points can reach —
-//     u_c = upstream_c / W,   out_c
-// (0 on fallback / special pixels) — in shared memory, and every thread owns
-// whole points.  For its point a thread walks the exact disk row by row
-// (closed ball d^2 <= r^2 as the reference decides it in f64, bin_grid.cpp:98),
-// recomputing the Gaussian weight on the SFU instead of storing it, and
-// accumulates, in registers,
-//     d_col_c += w * u_c                       (= up_c * w/W, engine.cpp:222)
-//     d_pos   += w * (sum_c u_c (c_c - out_c)) * (q - mu) / sigma^2
-//                                   (= ratio * dot / sigma^2 * (q-mu), :223-230)
-// then writes the point's gradients once.  Each point has exactly one owner,
-// so the result is bit-deterministic with no atomics and no reduction pass.
+// Point-major and atomic-free.  A CTA takes a block of reference cells and
+// stages, for every pixel those points can reach,
+//     u_c = upstream_c / W      and      out_c
+// (both 0 on fallback pixels) in shared memory as interleaved PIXEL PAIRS
+// (x even, x+1) so that two pixels are processed per f32x2 instruction
+// (FFMA2 / FMUL2 / FADD2, sm_100).  Every thread owns whole points and walks
+// the point's exact disk row by row — the reference's closed ball d^2 <= r^2
+// (bin_grid.cpp:98; exact spans from one fp32 sqrt per row, or the f64
+// predicate for points K1 flagged as boundary-ambiguous) — recomputing the
+// Gaussian weight instead of storing it: two exp2 on the SFU start a row, then
+// the weights advance by the exact recurrence w(x+2) = w(x) * R(x),
+// R(x+2) = R(x) * 2^(8 nk), i.e. two FMUL2 per pixel pair.  Per pair it
+// accumulates in registers
+//     d_col_c += w * u_c                              (= up_c w/W, engine.cpp:222)
+//     d_pos   += w * sum_c u_c (c_ic - out_c) * (q - mu) / sigma^2
+//                              (= ratio * dot / sigma^2 * (q-mu), engine.cpp:219-230)
+// — c_ic - out_c is formed before weighting, exactly (Sterbenz), which keeps
+// d_positions accurate where the reference's value is a cancellation to ~0 —
+// and writes each point's gradients once.  One owner per point: the result
+// is bit-deterministic with no atomics and no reduction pass.
 //
-// K5 — special pixels: NearestPoint fallbacks route upstream to the nearest
-// colour (engine.cpp:200-211); pixels whose fp32 normaliser underflowed are
-// differentiated in f64 over the reference neighbour set.
+// K5 — fallback pixels under NearestPoint route their upstream to the nearest
+// point's colour (engine.cpp:200-211).
 #include <algorithm>
+#include <cmath>
 
 #include "gmi_internal.cuh"
 
@@ -25,15 +32,13 @@ using namespace gmi_dev;
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kCG = 4;                 // channels per pass
-constexpr int kSmemBudget = 64 * 1024;  // staged pixel bytes per CTA
+constexpr int kThreads = 128;
+constexpr int kSmemBudget = 48 * 1024;  // staged pixel bytes per CTA
 
 struct BwdParams {
     const Geom* geom;
     const int32_t* bins;
-    const int32_t* blk_off;  // [B+1] block offsets per image
-    const int32_t* blk_dims; // [B][2] (blocks per row, cells per block side)
+    const int32_t* blk_off;  // [B+1] CTA offsets per image
     const float* sx;
     const float* sy;
     const int32_t* sidx;
@@ -42,31 +47,36 @@ struct BwdParams {
     const float* image;     // [B][H][W][C]
     const float* upstream;  // [B][H][W][C]
     int B, N, C, W, H;
-    int bw, bh;             // cells per block
+    int bs;                 // cells per block side
     double r64, r2_64;
-    float r2f, guard, nk, inv_s2;
+    float nk;               // -log2(e) / (2 sigma^2)
+    float q8;               // 2^(8 nk): R(x+2)/R(x)
+    float inv_s2;
+    int use_rec;            // exp2 recurrence safe (no over/underflow of R)
     float* d_col;           // [B][N][C]
     float* d_pos;           // [B][N][2] or partial [G][B][N][2]
-    int groups;
 };
 
-__device__ __forceinline__ bool in_ref(int x, int y, float mx, float my,
-                                       double r2_64) {
-    return d2_ref(static_cast<double>(x), static_cast<double>(y),
-                  static_cast<double>(mx), static_cast<double>(my)) <= r2_64;
+__device__ __forceinline__ bool in_ref(int x, int y, float mx, float my, double r2_64) {
+    return d2_ref(static_cast<double>(x), static_cast<double>(y), static_cast<double>(mx),
+                  static_cast<double>(my)) <= r2_64;
 }
 
-__global__ void __launch_bounds__(kThreads)
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+template <int CG>
+__global__ void __launch_bounds__(kThreads, 4)
 k_backward_points(BwdParams p) {
-    extern __shared__ float s_pix[];  // [region_h][region_w][2*kCG]
-    __shared__ int s_run[65];
+    // [rows][pairs][CG] float4: (u0a,u0b,u1a,u1b, ..., o0a,o0b, ...) as 2*CG float2
+    extern __shared__ float4 s_pair[];
+    __shared__ int s_run[66];
     __shared__ float s_red[4][kThreads / 32];
     __shared__ int s_region[5];
 
-    // ---- which image / block ----
+    // ---- image / cell block of this CTA ----
     int b = 0;
     {
-        int lo = 0, hi = p.B;  // blk_off[b] <= blockIdx.x < blk_off[b+1]
+        int lo = 0, hi = p.B;
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
             if (p.blk_off[mid] <= static_cast<int>(blockIdx.x)) lo = mid;
@@ -76,20 +86,15 @@ k_backward_points(BwdParams p) {
     }
     const Geom g = p.geom[b];
     const int local = blockIdx.x - p.blk_off[b];
-    const int nbx = (g.n_cols + p.bw - 1) / p.bw;
-    const int cx0 = (local % nbx) * p.bw, cy0 = (local / nbx) * p.bh;
-    const int cx1 = min(cx0 + p.bw, g.n_cols), cy1 = min(cy0 + p.bh, g.n_rows);
-    const int cg = blockIdx.y, ch0 = cg * kCG, nch = min(kCG, p.C - ch0);
+    const int nbx = (g.n_cols + p.bs - 1) / p.bs;
+    const int cx0 = (local % nbx) * p.bs, cy0 = (local / nbx) * p.bs;
+    const int cx1 = min(cx0 + p.bs, g.n_cols), cy1 = min(cy0 + p.bs, g.n_rows);
+    const int cg = blockIdx.y, ch0 = cg * CG, nch = min(CG, p.C - ch0);
     const int tid = threadIdx.x;
     const size_t base = static_cast<size_t>(b) * p.N;
 
     // ---- point runs (one per cell row of the block) ----
     const int nrun = cy1 - cy0;
-    if (tid <= nrun) {
-        // s_run[k] = start of run k; s_run[nrun] = total
-        s_run[tid] = 0;
-    }
-    __syncthreads();
     if (tid == 0) {
         int tot = 0;
         for (int k = 0; k < nrun; ++k) {
@@ -102,14 +107,14 @@ k_backward_points(BwdParams p) {
     __syncthreads();
     const int total = s_run[nrun];
     if (total == 0) return;
-    auto slot_of = [&](int k) -> int {  // concatenated index -> SoA slot
+    auto slot_of = [&](int k) -> int {
         int r = 0;
         while (s_run[r + 1] <= k) ++r;
         const int64_t r0 = g.bin_off + static_cast<int64_t>(cy0 + r) * g.n_cols;
         return p.bins[r0 + cx0] + (k - s_run[r]);
     };
 
-    // ---- pixel region reached by the block's points ----
+    // ---- pixel region reached by the block's points (bbox + r) ----
     float mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
     for (int k = tid; k < total; k += kThreads) {
         const int s = slot_of(k);
@@ -140,25 +145,30 @@ k_backward_points(BwdParams p) {
             mxy = fmaxf(mxy, s_red[3][w]);
         }
         const float rr = static_cast<float>(p.r64) + 2.0f;
-        const int x0 = max(0, static_cast<int>(floorf(mnx - rr)));
+        int x0 = max(0, static_cast<int>(floorf(mnx - rr)));
         const int y0 = max(0, static_cast<int>(floorf(mny - rr)));
-        const int x1 = min(p.W - 1, static_cast<int>(ceilf(mxx + rr)));
+        int x1 = min(p.W - 1, static_cast<int>(ceilf(mxx + rr)));
         const int y1 = min(p.H - 1, static_cast<int>(ceilf(mxy + rr)));
+        x0 &= ~1;        // pairs start at even x
+        x1 |= 1;         // and end at odd x (may exceed the frame: zero-staged)
         s_region[0] = x0;
         s_region[1] = y0;
         s_region[2] = x1;
         s_region[3] = y1;
-        const long area = (x1 >= x0 && y1 >= y0)
-                              ? static_cast<long>(x1 - x0 + 1) * (y1 - y0 + 1)
-                              : 0;
-        s_region[4] = (area * (2 * kCG) * 4 <= kSmemBudget) ? 1 : 0;
+        const long npairs = (x1 >= x0) ? (x1 - x0 + 1) / 2 : 0;
+        const long area = (y1 >= y0) ? npairs * (y1 - y0 + 1) : 0;
+        s_region[4] = (mnx <= mxx && area > 0 &&
+                       area * CG * static_cast<long>(sizeof(float4)) <= kSmemBudget)
+                          ? 1
+                          : (area > 0 ? 0 : -1);
     }
     __syncthreads();
     const int rx0 = s_region[0], ry0 = s_region[1], rx1 = s_region[2], ry1 = s_region[3];
-    if (rx1 < rx0 || ry1 < ry0) {
-        // no pixel in the frame is reachable: all gradients are zero
+    const int mode = s_region[4];
+    if (mode < 0) {
+        // no frame pixel is reachable: gradients are zero
         for (int k = tid; k < total; k += kThreads) {
-            const int i = p.sidx[base + slot_of(k)];
+            const int i = p.sidx[base + slot_of(k)] & 0x7fffffff;
             for (int c = 0; c < nch; ++c) p.d_col[(base + i) * p.C + ch0 + c] = 0.f;
             float* dp = p.d_pos + (static_cast<size_t>(cg) * p.B * p.N + base + i) * 2;
             dp[0] = 0.f;
@@ -166,117 +176,192 @@ k_backward_points(BwdParams p) {
         }
         return;
     }
-    const bool staged = s_region[4] != 0;
-    const int rw = rx1 - rx0 + 1;
+    const bool staged = mode == 1;
+    const int npairs = (rx1 - rx0 + 1) / 2;
     const size_t img_base = static_cast<size_t>(b) * p.H * p.W;
 
-    // per-pixel quantities for this channel group (engine.cpp:213-222):
-    // q[c] = upstream_c / W and q[kCG + c] = out_c (0 on special pixels).
-    // Staging out (not sum_c u_c out_c) lets the point loop form c_ic - out_c
-    // exactly (Sterbenz) before weighting, which keeps d_positions accurate
-    // where the reference's value is a cancellation to ~0 (isolated points).
-    auto pixel_q = [&](int x, int y, float* q) {
+    // (u_c, out_c) of one pixel for this channel group; zero off-frame and on
+    // fallback pixels (W == 0: engine.cpp:200-211 handles them in K5).
+    auto pixel_q = [&](int x, int y, float* u, float* o) {
+#pragma unroll
+        for (int c = 0; c < CG; ++c) {
+            u[c] = 0.f;
+            o[c] = 0.f;
+        }
+        if (x < 0 || x >= p.W || y < 0 || y >= p.H) return;
         const size_t pix = img_base + static_cast<size_t>(y) * p.W + x;
         const float wv = p.wsum[pix];
-#pragma unroll
-        for (int c = 0; c < 2 * kCG; ++c) q[c] = 0.f;
         if (wv > 0.f) {
             const float inv = 1.0f / wv;
-            const float* up = p.upstream + pix * p.C + ch0;
-            const float* out = p.image + pix * p.C + ch0;
 #pragma unroll
-            for (int c = 0; c < kCG; ++c) {
+            for (int c = 0; c < CG; ++c) {
                 if (c < nch) {
-                    q[c] = up[c] * inv;
-                    q[kCG + c] = out[c];
+                    u[c] = p.upstream[pix * p.C + ch0 + c] * inv;
+                    o[c] = p.image[pix * p.C + ch0 + c];
                 }
             }
         }
     };
     if (staged) {
-        const int area = rw * (ry1 - ry0 + 1);
+        const int area = npairs * (ry1 - ry0 + 1);
         for (int k = tid; k < area; k += kThreads) {
-            float q[2 * kCG];
-            pixel_q(rx0 + k % rw, ry0 + k / rw, q);
+            const int pp = k % npairs, yy = ry0 + k / npairs;
+            float ua[CG], oa[CG], ub[CG], ob[CG];
+            pixel_q(rx0 + 2 * pp, yy, ua, oa);
+            pixel_q(rx0 + 2 * pp + 1, yy, ub, ob);
+            float2* dst = reinterpret_cast<float2*>(s_pair + static_cast<size_t>(k) * CG);
 #pragma unroll
-            for (int c = 0; c < 2 * kCG; ++c) s_pix[k * (2 * kCG) + c] = q[c];
+            for (int c = 0; c < CG; ++c) {
+                dst[c] = f2(ua[c], ub[c]);
+                dst[CG + c] = f2(oa[c], ob[c]);
+            }
         }
         __syncthreads();
     }
 
     // ---- per point ----
+    const float nk = p.nk, q8 = p.q8, inv_s2 = p.inv_s2;
+    const float r2f = static_cast<float>(p.r2_64), rf = static_cast<float>(p.r64);
+    const double r2_64 = p.r2_64;
+    const bool use_rec = p.use_rec != 0;
+    const int xmin = max(rx0, 0), xmax = min(rx1, p.W - 1);
+    const float2 nk2 = f2(nk, nk), q82 = f2(q8, q8), two = f2(2.f, 2.f);
     for (int k = tid; k < total; k += kThreads) {
         const int s = slot_of(k);
         const float mx = p.sx[base + s], my = p.sy[base + s];
-        const int i = p.sidx[base + s];
-        float cc[kCG];
+        const uint32_t raw = static_cast<uint32_t>(p.sidx[base + s]);
+        const int i = static_cast<int>(raw & 0x7fffffffu);
+        const bool unsafe = (raw & kUnsafeBit) != 0;
+        float cc[CG];
+        float2 cc2[CG];
 #pragma unroll
-        for (int c = 0; c < kCG; ++c)
+        for (int c = 0; c < CG; ++c) {
             cc[c] = c < nch ? p.scol[(static_cast<size_t>(b) * p.C + ch0 + c) * p.N + s] : 0.f;
-        float dcol[kCG];
+            cc2[c] = f2(cc[c], cc[c]);
+        }
+        float2 dcol[CG];
 #pragma unroll
-        for (int c = 0; c < kCG; ++c) dcol[c] = 0.f;
-        float gx = 0.f, gy = 0.f;
-        const float tx = truncf(mx);
-        const float fmu = mx - tx;  // exact
-        const int bx = static_cast<int>(tx);
-        const int ya = max(ry0, static_cast<int>(floorf(my - static_cast<float>(p.r64))) - 1);
-        const int yb = min(ry1, static_cast<int>(ceilf(my + static_cast<float>(p.r64))) + 1);
+        for (int c = 0; c < CG; ++c) dcol[c] = f2(0.f, 0.f);
+        float2 gx2 = f2(0.f, 0.f);
+        float gy = 0.f;
+        const float tx = truncf(mx), ty = truncf(my);
+        const float fmu = mx - tx, fmy = my - ty;  // exact
+        const int bx = static_cast<int>(tx), by = static_cast<int>(ty);
+        const int ya = max(ry0, static_cast<int>(floorf(my - rf)) - 1);
+        const int yb = min(ry1, static_cast<int>(ceilf(my + rf)) + 1);
+
         for (int y = ya; y <= yb; ++y) {
-            const double dy64 = __dsub_rn(static_cast<double>(y), static_cast<double>(my));
-            const double h2 = __dsub_rn(p.r2_64, __dmul_rn(dy64, dy64));
-            const float h2f = static_cast<float>(h2);
-            if (h2f < -p.guard) continue;  // row entirely outside the ball
-            const float sq = sqrtf(fmaxf(h2f, 0.f));
-            const float al = fmu - sq, ar = fmu + sq;
-            int xl = bx + static_cast<int>(ceilf(al));
-            int xr = bx + static_cast<int>(floorf(ar));
-            const float nl = rintf(al), nr = rintf(ar);
-            const float el = fmaf(nl - fmu, nl - fmu, -h2f);
-            const float er = fmaf(nr - fmu, nr - fmu, -h2f);
-            if (fabsf(el) <= p.guard || fabsf(er) <= p.guard) {
-                // boundary pixel within the guard band: decide in f64
+            float dy;
+            int xl, xr;
+            if (!unsafe) {
+                // safe point: fp32 row geometry decides the reference's ball
+                dy = static_cast<float>(y - by) - fmy;
+                const float h2f = fmaf(-dy, dy, r2f);
+                if (h2f < 0.f) continue;
+                const float sq = sqrtf(h2f);
+                xl = bx + static_cast<int>(ceilf(fmu - sq));
+                xr = bx + static_cast<int>(floorf(fmu + sq));
+            } else {
+                const double dy64 = __dsub_rn(static_cast<double>(y), static_cast<double>(my));
+                const double h2 = __dsub_rn(r2_64, __dmul_rn(dy64, dy64));
+                if (h2 < 0.0) continue;  // fl(dy^2) > r^2: no pixel of this row is in
+                const float sq = sqrtf(static_cast<float>(h2));
+                xl = bx + static_cast<int>(ceilf(fmu - sq));
+                xr = bx + static_cast<int>(floorf(fmu + sq));
                 int a = xl - 2;
-                while (a <= xl + 2 && !in_ref(a, y, mx, my, p.r2_64)) ++a;
+                while (a <= xl + 2 && !in_ref(a, y, mx, my, r2_64)) ++a;
                 int z = xr + 2;
-                while (z >= xr - 2 && !in_ref(z, y, mx, my, p.r2_64)) --z;
+                while (z >= xr - 2 && !in_ref(z, y, mx, my, r2_64)) --z;
                 xl = a;
                 xr = z;
+                dy = static_cast<float>(dy64);
             }
-            xl = max(xl, rx0);
-            xr = min(xr, rx1);
+            xl = max(xl, xmin);
+            xr = min(xr, xmax);
             if (xl > xr) continue;
-            const float dy = static_cast<float>(dy64);
             const float dy2 = dy * dy;
-            float gyr = 0.f;
-            float dx = static_cast<float>(xl - bx) - fmu;
-            for (int x = xl; x <= xr; ++x, dx += 1.0f) {
-                const float d2 = fmaf(dx, dx, dy2);
-                const float w = ex2(d2 * p.nk);
-                float q[2 * kCG];
-                if (staged) {
-                    const float* sp = s_pix + ((y - ry0) * rw + (x - rx0)) * (2 * kCG);
+            if (!staged) {
+                float gyr = 0.f;
+                for (int x = xl; x <= xr; ++x) {
+                    const float dx = static_cast<float>(x - bx) - fmu;
+                    const float w = ex2(fmaf(dx, dx, dy2) * nk);
+                    float u[CG], o[CG];
+                    pixel_q(x, y, u, o);
+                    float t = 0.f;
 #pragma unroll
-                    for (int c = 0; c < 2 * kCG; ++c) q[c] = sp[c];
-                } else {
-                    pixel_q(x, y, q);
+                    for (int c = 0; c < CG; ++c) t = fmaf(u[c], cc[c] - o[c], t);
+                    const float a = w * t;
+#pragma unroll
+                    for (int c = 0; c < CG; ++c) dcol[c].x = fmaf(w, u[c], dcol[c].x);
+                    gx2.x = fmaf(a, dx, gx2.x);
+                    gyr += a;
                 }
-                // dot/W = sum_c u_c (c_ic - out_c)   (engine.cpp:219-221)
-                float t = 0.f;
-#pragma unroll
-                for (int c = 0; c < kCG; ++c) t = fmaf(q[c], cc[c] - q[kCG + c], t);
-                const float a = w * t;
-#pragma unroll
-                for (int c = 0; c < kCG; ++c) dcol[c] = fmaf(w, q[c], dcol[c]);
-                gx = fmaf(a, dx, gx);
-                gyr += a;
+                gy = fmaf(gyr, dy, gy);
+                continue;
             }
-            gy = fmaf(gyr, dy, gy);
+            // pair-aligned span [xs, xe] (rx0 even); the end pixels outside
+            // [xl, xr] are masked out of the first / last pair
+            const int xs = xl - ((xl - rx0) & 1);
+            const int xe = xr + (((xr - rx0) & 1) ^ 1);
+            const int np = (xe - xs + 1) >> 1;
+            const float2 m_first = f2(((xl - rx0) & 1) ? 0.f : 1.f, 1.f);
+            const float2 m_last = f2(1.f, ((xr - rx0) & 1) ? 1.f : 0.f);
+            float2 dx = f2(static_cast<float>(xs - bx) - fmu, 0.f);
+            dx.y = dx.x + 1.0f;
+            const float2 dy22 = f2(dy2, dy2);
+            float2 w = __fmul2_rn(__ffma2_rn(dx, dx, dy22), nk2);
+            w = f2(ex2(w.x), ex2(w.y));
+            float2 R = f2(0.f, 0.f);
+            if (use_rec) {
+                // R(x) = w(x+2)/w(x) = 2^(nk (4 dx + 4))
+                R = __fmul2_rn(__ffma2_rn(f2(4.f, 4.f), dx, f2(4.f, 4.f)), nk2);
+                R = f2(ex2(R.x), ex2(R.y));
+            }
+            float2 gyr2 = f2(0.f, 0.f);
+            const float4* pr = s_pair + (static_cast<size_t>(y - ry0) * npairs + ((xs - rx0) >> 1)) * CG;
+            auto body = [&](float2 wm) {
+                float4 v[CG];
+#pragma unroll
+                for (int c = 0; c < CG; ++c) v[c] = pr[c];
+                const float2* q = reinterpret_cast<const float2*>(v);
+                // t = sum_c u_c (c_ic - out_c)
+                float2 t = __fmul2_rn(q[0], __fadd2_rn(cc2[0], f2(-q[CG].x, -q[CG].y)));
+#pragma unroll
+                for (int c = 1; c < CG; ++c)
+                    t = __ffma2_rn(q[c], __fadd2_rn(cc2[c], f2(-q[CG + c].x, -q[CG + c].y)), t);
+                const float2 a = __fmul2_rn(wm, t);
+#pragma unroll
+                for (int c = 0; c < CG; ++c) dcol[c] = __ffma2_rn(wm, q[c], dcol[c]);
+                gx2 = __ffma2_rn(a, dx, gx2);
+                gyr2 = __fadd2_rn(gyr2, a);
+            };
+            auto advance = [&]() {
+                dx = __fadd2_rn(dx, two);
+                pr += CG;
+                if (use_rec) {
+                    w = __fmul2_rn(w, R);
+                    R = __fmul2_rn(R, q82);
+                } else {
+                    const float2 arg = __fmul2_rn(__ffma2_rn(dx, dx, dy22), nk2);
+                    w = f2(ex2(arg.x), ex2(arg.y));
+                }
+            };
+            body(__fmul2_rn(w, np == 1 ? __fmul2_rn(m_first, m_last) : m_first));
+            if (np > 1) {
+                advance();
+                for (int j = 1; j < np - 1; ++j) {
+                    body(w);
+                    advance();
+                }
+                body(__fmul2_rn(w, m_last));
+            }
+            gy = fmaf(gyr2.x + gyr2.y, dy, gy);
         }
-        for (int c = 0; c < nch; ++c) p.d_col[(base + i) * p.C + ch0 + c] = dcol[c];
+        for (int c = 0; c < nch; ++c)
+            p.d_col[(base + i) * p.C + ch0 + c] = dcol[c].x + dcol[c].y;
         float* dp = p.d_pos + (static_cast<size_t>(cg) * p.B * p.N + base + i) * 2;
-        dp[0] = gx * p.inv_s2;
-        dp[1] = gy * p.inv_s2;
+        dp[0] = (gx2.x + gx2.y) * inv_s2;
+        dp[1] = gy * inv_s2;
     }
 }
 
@@ -290,88 +375,93 @@ __global__ void k_sum_groups(const float* __restrict__ part, float* __restrict__
     d_pos[k] = s;
 }
 
+// Precise mode (cutoff > 6 sigma): one thread per point, f64 weights and
+// ratios straight from the reference formulas (engine.cpp:213-231) against the
+// f64 normaliser; inclusion by the exact predicate.  A correctness path for
+// untruncated / wide-radius calls, not the hot path.
+constexpr int kCG64 = 4;
+__global__ void k_backward_points_f64(BwdParams p, const double* __restrict__ wsum64,
+                                      double inv2s2) {
+    const size_t total = static_cast<size_t>(p.B) * p.N;
+    const int cg = blockIdx.y, ch0 = cg * kCG64, nch = min(kCG64, p.C - ch0);
+    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < total;
+         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int b = static_cast<int>(k / p.N);
+        const size_t base = static_cast<size_t>(b) * p.N;
+        const double mx = p.sx[k], my = p.sy[k];
+        const int i = p.sidx[k] & 0x7fffffff;
+        const int s = static_cast<int>(k - base);
+        double dcol[kCG64] = {0, 0, 0, 0};
+        double gx = 0.0, gy = 0.0;
+        double cc[kCG64];
+        for (int c = 0; c < kCG64; ++c)
+            cc[c] = c < nch ? p.scol[(static_cast<size_t>(b) * p.C + ch0 + c) * p.N + s] : 0.0;
+        const int y0 = max(0, static_cast<int>(floor(my - p.r64)) - 1);
+        const int y1 = min(p.H - 1, static_cast<int>(ceil(my + p.r64)) + 1);
+        const int x0 = max(0, static_cast<int>(floor(mx - p.r64)) - 1);
+        const int x1 = min(p.W - 1, static_cast<int>(ceil(mx + p.r64)) + 1);
+        for (int y = y0; y <= y1; ++y) {
+            for (int x = x0; x <= x1; ++x) {
+                const double d2 = d2_ref(x, y, mx, my);
+                if (!(d2 <= p.r2_64)) continue;
+                const size_t pix = static_cast<size_t>(b) * p.H * p.W + static_cast<size_t>(y) * p.W + x;
+                const double W64 = wsum64[pix];
+                if (!(W64 > 0.0)) continue;
+                const double ratio = exp(-d2 * inv2s2) / W64;
+                double dot = 0.0;
+                for (int c = 0; c < nch; ++c) {
+                    const double u = p.upstream[pix * p.C + ch0 + c];
+                    dcol[c] += u * ratio;
+                    dot += u * (cc[c] - static_cast<double>(p.image[pix * p.C + ch0 + c]));
+                }
+                const double coef = ratio * dot;
+                gx += coef * (x - mx);
+                gy += coef * (y - my);
+            }
+        }
+        for (int c = 0; c < nch; ++c) p.d_col[(base + i) * p.C + ch0 + c] = static_cast<float>(dcol[c]);
+        float* dp = p.d_pos + (static_cast<size_t>(cg) * p.B * p.N + base + i) * 2;
+        dp[0] = static_cast<float>(gx * p.inv_s2);
+        dp[1] = static_cast<float>(gy * p.inv_s2);
+    }
+}
+
 // ---------------------------------------------------------------------------
 struct SpecBwdParams {
-    const Geom* geom;
-    const int32_t* bins;
-    const float* sx;
-    const float* sy;
-    const int32_t* sidx;
-    const float* scol;
-    const float* image;
     const float* upstream;
     const Special* special;
     const int32_t* special_count;
     int special_cap;
     int N, C, W, H;
-    double r64, r2_64, sigma;
     int fallback;
     float* d_col;
-    float* d_pos;
 };
 
+// engine.cpp:200-211: fallback pixels route their upstream to the nearest
+// point's colour only (no position gradient).
 __global__ void k_special_backward(SpecBwdParams p) {
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int n = min(*p.special_count, p.special_cap);
+    if (p.fallback != GMI_FALLBACK_NEAREST) return;
     for (int si = warp; si < n; si += nwarps) {
         const Special sp = p.special[si];
+        if (sp.kind != 1 || sp.nearest < 0) continue;
         const size_t pixb = static_cast<size_t>(sp.b) * p.H * p.W + sp.pix;
-        const float* up = p.upstream + pixb * p.C;
         const size_t base = static_cast<size_t>(sp.b) * p.N;
-        if (sp.kind == 1) {
-            // engine.cpp:200-211: colour-only routing to the nearest point
-            if (p.fallback == GMI_FALLBACK_NEAREST && sp.nearest >= 0) {
-                for (int c = lane; c < p.C; c += 32)
-                    atomicAdd(p.d_col + (base + sp.nearest) * p.C + c, up[c]);
-            }
-            continue;
-        }
-        if (sp.kind != 2) continue;
-        // f64 differentiation over the reference neighbour set
-        const Geom g = p.geom[sp.b];
-        const int pr = sp.pix / p.W, pc = sp.pix % p.W;
-        const double qx = pc, qy = pr;
-        const double inv2s2 = 1.0 / (2.0 * p.sigma * p.sigma);
-        const double inv_s2 = 1.0 / (p.sigma * p.sigma);
-        const int cx0 = cell_of(qx - p.r64, g.ox, g.cell, g.n_cols);
-        const int cx1 = cell_of(qx + p.r64, g.ox, g.cell, g.n_cols);
-        const int cy0 = cell_of(qy - p.r64, g.oy, g.cell, g.n_rows);
-        const int cy1 = cell_of(qy + p.r64, g.oy, g.cell, g.n_rows);
-        double W64 = 0.0;
-        for (int pass = 0; pass < 2; ++pass) {
-            for (int cy = cy0; cy <= cy1; ++cy) {
-                const int64_t r0 = g.bin_off + static_cast<int64_t>(cy) * g.n_cols;
-                const int s = p.bins[r0 + cx0], e = p.bins[r0 + cx1 + 1];
-                for (int k = s + lane; k < e; k += 32) {
-                    const double mx = p.sx[base + k], my = p.sy[base + k];
-                    const double d2 = d2_ref(qx, qy, mx, my);
-                    if (!(d2 <= p.r2_64)) continue;
-                    const double w = exp(-d2 * inv2s2);
-                    if (pass == 0) {
-                        W64 += w;
-                        continue;
-                    }
-                    const double ratio = w / W64;
-                    const int i = p.sidx[base + k];
-                    double dot = 0.0;
-                    for (int c = 0; c < p.C; ++c) {
-                        const double u = up[c];
-                        atomicAdd(p.d_col + (base + i) * p.C + c, static_cast<float>(u * ratio));
-                        dot += u * (static_cast<double>(
-                                        p.scol[(static_cast<size_t>(sp.b) * p.C + c) * p.N + k]) -
-                                    static_cast<double>(p.image[pixb * p.C + c]));
-                    }
-                    const double coef = ratio * dot * inv_s2;
-                    atomicAdd(p.d_pos + (base + i) * 2, static_cast<float>(coef * (qx - mx)));
-                    atomicAdd(p.d_pos + (base + i) * 2 + 1, static_cast<float>(coef * (qy - my)));
-                }
-            }
-            if (pass == 0)
-                for (int o = 16; o > 0; o >>= 1) W64 += __shfl_xor_sync(0xffffffffu, W64, o);
-        }
+        for (int c = lane; c < p.C; c += 32)
+            atomicAdd(p.d_col + (base + sp.nearest) * p.C + c, p.upstream[pixb * p.C + c]);
     }
+}
+
+template <int CG>
+void launch_points(gmi_ctx* ctx, const BwdParams& p, int nblocks, int groups) {
+    const int smem = kSmemBudget;
+    GMI_CUDA(cudaFuncSetAttribute(k_backward_points<CG>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_backward_points<CG><<<dim3(nblocks, groups), kThreads, smem, ctx->stream>>>(p);
+    GMI_LAUNCHED(ctx);
 }
 
 }  // namespace
@@ -381,11 +471,12 @@ namespace gmi_host {
 void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
                      float* d_colors, float* d_positions) {
     cudaStream_t st = ctx->stream;
-    const int groups = (c->C + kCG - 1) / kCG;
-    // cells per block side so that the staged pixel region fits the budget
+    const int CG = c->C <= 4 ? c->C : 4;
+    const int groups = (c->C + CG - 1) / CG;
+    // cells per block side so that the staged pixel pairs fit the budget
     const double cell = c->cutoff;
-    const double side_px = std::sqrt(static_cast<double>(kSmemBudget) / ((2 * kCG) * 4.0));
-    int bs = static_cast<int>(std::floor((side_px - 2.0 * cell - 6.0) / cell));
+    const double side_px = std::sqrt(static_cast<double>(kSmemBudget) / (8.0 * CG));
+    int bs = static_cast<int>(std::floor((side_px - 2.0 * cell - 8.0) / cell));
     bs = std::max(1, std::min(bs, 64));
     std::vector<int32_t> off(c->B + 1, 0);
     for (int b = 0; b < c->B; ++b) {
@@ -393,7 +484,7 @@ void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
         const int nb = ((g.n_cols + bs - 1) / bs) * ((g.n_rows + bs - 1) / bs);
         off[b + 1] = off[b] + nb;
     }
-    int32_t* d_off = static_cast<int32_t*>(dalloc(ctx, sizeof(int32_t) * (c->B + 1)));
+    int32_t* d_off = static_cast<int32_t*>(scratch(ctx, WS_BLKOFF, sizeof(int32_t) * (c->B + 1)));
     GMI_CUDA(cudaMemcpyAsync(d_off, off.data(), sizeof(int32_t) * (c->B + 1),
                              cudaMemcpyHostToDevice, st));
     BwdParams p{};
@@ -412,49 +503,57 @@ void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
     p.C = c->C;
     p.W = c->W;
     p.H = c->H;
-    p.bw = bs;
-    p.bh = bs;
+    p.bs = bs;
     p.r64 = c->cutoff;
     p.r2_64 = c->cutoff * c->cutoff;
-    p.r2f = static_cast<float>(p.r2_64);
-    p.guard = 4e-6f * p.r2f + 1e-30f;
-    p.nk = static_cast<float>(-1.4426950408889634 / (2.0 * c->sigma * c->sigma));
+    const double nk = -1.4426950408889634 / (2.0 * c->sigma * c->sigma);
+    p.nk = static_cast<float>(nk);
+    p.q8 = static_cast<float>(std::exp2(8.0 * nk));
+    // R = 2^(nk (4 dx + 4)), |dx| <= r: keep it (and w * R) well inside fp32
+    p.use_rec = (std::fabs(nk) * (4.0 * c->cutoff + 12.0) < 60.0) ? 1 : 0;
     p.inv_s2 = static_cast<float>(1.0 / (c->sigma * c->sigma));
     p.d_col = d_colors;
-    p.groups = groups;
-    float* part = nullptr;
     const size_t n2 = static_cast<size_t>(c->B) * c->N * 2;
+    float* part = nullptr;
     if (groups > 1) {
-        part = static_cast<float*>(dalloc(ctx, sizeof(float) * n2 * groups));
+        part = static_cast<float*>(scratch(ctx, WS_PART, sizeof(float) * n2 * groups));
         p.d_pos = part;
     } else {
         p.d_pos = d_positions;
     }
-    GMI_CUDA(cudaFuncSetAttribute(k_backward_points,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
-    if (off[c->B] > 0) {
-        k_backward_points<<<dim3(off[c->B], groups), kThreads, kSmemBudget, st>>>(p);
+    if (c->wsum64 != nullptr) {
+        const int g64 = (c->C + kCG64 - 1) / kCG64;
+        p.d_pos = d_positions;
+        if (g64 > 1) {
+            part = static_cast<float*>(scratch(ctx, WS_PART, sizeof(float) * n2 * g64));
+            p.d_pos = part;
+        }
+        k_backward_points_f64<<<dim3(4 * ctx->num_sms, g64), 128, 0, st>>>(
+            p, c->wsum64, 1.0 / (2.0 * c->sigma * c->sigma));
         GMI_LAUNCHED(ctx);
+        if (g64 > 1) {
+            k_sum_groups<<<static_cast<unsigned>((n2 + 255) / 256), 256, 0, st>>>(part, d_positions, n2, g64);
+            GMI_LAUNCHED(ctx);
+        }
+        return;
+    }
+    if (off[c->B] > 0) {
+        switch (CG) {
+            case 1: launch_points<1>(ctx, p, off[c->B], groups); break;
+            case 2: launch_points<2>(ctx, p, off[c->B], groups); break;
+            case 3: launch_points<3>(ctx, p, off[c->B], groups); break;
+            default: launch_points<4>(ctx, p, off[c->B], groups); break;
+        }
     }
     if (groups > 1) {
         k_sum_groups<<<static_cast<unsigned>((n2 + 255) / 256), 256, 0, st>>>(part, d_positions, n2, groups);
         GMI_LAUNCHED(ctx);
-        dfree(ctx, part);
     }
-    dfree(ctx, d_off);
 }
 
-void launch_special_backward(gmi_ctx* ctx, const gmi_cache* c,
-                             const float* upstream, float* d_colors,
-                             float* d_positions) {
+void launch_special_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
+                             float* d_colors, float* /*d_positions*/) {
     SpecBwdParams p{};
-    p.geom = c->geom_d;
-    p.bins = c->bins;
-    p.sx = c->sx;
-    p.sy = c->sy;
-    p.sidx = c->sidx;
-    p.scol = c->scol;
-    p.image = c->image;
     p.upstream = upstream;
     p.special = c->special;
     p.special_count = c->special_count_d;
@@ -463,12 +562,8 @@ void launch_special_backward(gmi_ctx* ctx, const gmi_cache* c,
     p.C = c->C;
     p.W = c->W;
     p.H = c->H;
-    p.r64 = c->cutoff;
-    p.r2_64 = c->cutoff * c->cutoff;
-    p.sigma = c->sigma;
     p.fallback = c->fallback;
     p.d_col = d_colors;
-    p.d_pos = d_positions;
     k_special_backward<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(p);
     GMI_LAUNCHED(ctx);
 }

@@ -215,6 +215,9 @@ struct SortOut {
     const float* col;
     int C;
     unsigned long long* issue;
+    int classify;      // 1: flag boundary-ambiguous points (kUnsafeBit)
+    double r64, r2_64;
+    float r2f;
     // reference export
     int32_t* point_index;
 };
@@ -239,7 +242,8 @@ __device__ __forceinline__ void emit(const SortOut& o, int b, int N, int k,
     const float2 v = p[i];
     o.sx[bk] = v.x;
     o.sy[bk] = v.y;
-    o.sidx[bk] = i;
+    const bool amb = o.classify && point_ambiguous(v.x, v.y, o.r64, o.r2_64, o.r2f);
+    o.sidx[bk] = static_cast<int32_t>(static_cast<uint32_t>(i) | (amb ? kUnsafeBit : 0u));
     const float* c = o.col + (static_cast<size_t>(b) * N + i) * o.C;
     unsigned code = 0;
     for (int ch = 0; ch < o.C; ++ch) {
@@ -379,7 +383,7 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
 
     // ---- bbox + position validation -> host (one sync: sizes are data
     // dependent exactly as in the reference) ----
-    uint32_t* d_bbox = static_cast<uint32_t*>(dalloc(ctx, sizeof(uint32_t) * 4 * B));
+    uint32_t* d_bbox = static_cast<uint32_t*>(scratch(ctx, WS_BBOX, sizeof(uint32_t) * 4 * B));
     k_bbox_init<<<(B + 127) / 128, 128, 0, st>>>(d_bbox, d_issue, B);
     GMI_LAUNCHED(ctx);
     {
@@ -394,8 +398,9 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
                              cudaMemcpyDeviceToHost, st));
     GMI_CUDA(cudaMemcpyAsync(issue.data(), d_issue, sizeof(unsigned long long) * B,
                              cudaMemcpyDeviceToHost, st));
+    host_trace("bin: launched bbox");
     GMI_CUDA(cudaStreamSynchronize(st));
-    dfree(ctx, d_bbox);
+    host_trace("bin: bbox sync");
     for (int b = 0; b < B; ++b) {
         if (issue[b] != kNoIssue) {
             const long idx = static_cast<long>(issue[b] >> 8);
@@ -437,11 +442,13 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
 
     // ---- count ----
     const size_t BN = static_cast<size_t>(B) * N;
-    int32_t* cellid = static_cast<int32_t*>(dalloc(ctx, sizeof(int32_t) * BN));
-    int32_t* rank = static_cast<int32_t*>(dalloc(ctx, sizeof(int32_t) * BN));
+    int32_t* cellid = static_cast<int32_t*>(scratch(ctx, WS_CELLID, sizeof(int32_t) * BN));
+    int32_t* rank = static_cast<int32_t*>(scratch(ctx, WS_RANK, sizeof(int32_t) * BN));
     const dim3 pgrid((N + 255) / 256, B);
+    host_trace("bin: geometry+allocs");
     k_count<<<pgrid, 256, 0, st>>>(p2, N, c->geom_d, c->bins, cellid, rank);
     GMI_LAUNCHED(ctx);
+    host_trace("bin: count launched");
 
     // ---- segmented scan ----
     std::vector<ScanTile> tiles;
@@ -454,9 +461,9 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
         seg_off[b + 1] = static_cast<int32_t>(tiles.size());
     }
     const int nt = static_cast<int>(tiles.size());
-    ScanTile* d_tiles = static_cast<ScanTile*>(dalloc(ctx, sizeof(ScanTile) * nt));
-    int32_t* d_tsum = static_cast<int32_t*>(dalloc(ctx, sizeof(int32_t) * nt));
-    int32_t* d_segoff = static_cast<int32_t*>(dalloc(ctx, sizeof(int32_t) * (B + 1)));
+    ScanTile* d_tiles = static_cast<ScanTile*>(scratch(ctx, WS_TILES, sizeof(ScanTile) * nt));
+    int32_t* d_tsum = static_cast<int32_t*>(scratch(ctx, WS_TSUM, sizeof(int32_t) * nt));
+    int32_t* d_segoff = static_cast<int32_t*>(scratch(ctx, WS_SEGOFF, sizeof(int32_t) * (B + 1)));
     GMI_CUDA(cudaMemcpyAsync(d_tiles, tiles.data(), sizeof(ScanTile) * nt,
                              cudaMemcpyHostToDevice, st));
     GMI_CUDA(cudaMemcpyAsync(d_segoff, seg_off.data(), sizeof(int32_t) * (B + 1),
@@ -469,7 +476,7 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
     GMI_LAUNCHED(ctx);
 
     // ---- scatter + per-cell ordering ----
-    int32_t* tmp = static_cast<int32_t*>(dalloc(ctx, sizeof(int32_t) * BN));
+    int32_t* tmp = static_cast<int32_t*>(scratch(ctx, WS_TMP, sizeof(int32_t) * BN));
     k_scatter<<<pgrid, 256, 0, st>>>(N, c->geom_d, c->bins, cellid, rank, tmp);
     GMI_LAUNCHED(ctx);
 
@@ -483,11 +490,16 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
         o.col = col;
         o.C = c->C;
         o.issue = d_issue;
+        // f64 weight mode decides every pair in f64: no classification needed
+        o.classify = c->wsum64 == nullptr ? 1 : 0;
+        o.r64 = c->cutoff;
+        o.r2_64 = c->cutoff * c->cutoff;
+        o.r2f = static_cast<float>(o.r2_64);
     } else {
         o.point_index = point_index_out;
     }
-    int2* d_big = static_cast<int2*>(dalloc(ctx, sizeof(int2) * std::max<size_t>(1, BN / (kSmallCell + 1) + 1)));
-    int32_t* d_bigcount = static_cast<int32_t*>(dalloc(ctx, sizeof(int32_t)));
+    int2* d_big = static_cast<int2*>(scratch(ctx, WS_BIG, sizeof(int2) * std::max<size_t>(1, BN / (kSmallCell + 1) + 1)));
+    int32_t* d_bigcount = static_cast<int32_t*>(scratch(ctx, WS_BIGCOUNT, sizeof(int32_t)));
     GMI_CUDA(cudaMemsetAsync(d_bigcount, 0, sizeof(int32_t), st));
     k_cellsort_small<<<dim3((max_bins + 127) / 128, B), 128, 0, st>>>(
         p2, N, c->geom_d, c->bins, tmp, o, d_big, d_bigcount);
@@ -499,14 +511,7 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
                                                      d_big, d_bigcount);
     GMI_LAUNCHED(ctx);
 
-    dfree(ctx, d_big);
-    dfree(ctx, d_bigcount);
-    dfree(ctx, tmp);
-    dfree(ctx, d_tiles);
-    dfree(ctx, d_tsum);
-    dfree(ctx, d_segoff);
-    dfree(ctx, cellid);
-    dfree(ctx, rank);
+    host_trace("bin: scan..cellsort launched");
 }
 
 }  // namespace gmi_host

@@ -3,6 +3,8 @@
 // stream.  No exception crosses the ABI; every failure becomes a status code
 // plus a thread-local message.
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -119,6 +121,7 @@ int do_forward(gmi_ctx* ctx, const float* pos, const float* col, int B, int N,
     c->pos = pos;
     c->col = col;
     c->image = image;
+    c->force_generic = std::getenv("GMI_GENERIC") != nullptr;
     const size_t BN = static_cast<size_t>(B) * N;
     const size_t BHW = static_cast<size_t>(B) * c->H * c->W;
     c->sx = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN));
@@ -126,10 +129,14 @@ int do_forward(gmi_ctx* ctx, const float* pos, const float* col, int B, int N,
     c->sidx = static_cast<int32_t*>(gmi_host::cache_alloc(c, sizeof(int32_t) * BN));
     c->scol = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN * C));
     c->wsum = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BHW));
+    // f64 weight mode beyond 6 sigma (see gmi_forward.cu)
+    if (cfg->cutoff_radius > 6.0 * cfg->sigma)
+        c->wsum64 = static_cast<double*>(gmi_host::cache_alloc(c, sizeof(double) * BHW));
     c->special_cap = static_cast<int>(std::min<size_t>(BHW, size_t(1) << 22));
     c->special = static_cast<Special*>(gmi_host::cache_alloc(c, sizeof(Special) * c->special_cap));
     c->special_count_d = static_cast<int32_t*>(gmi_host::cache_alloc(c, sizeof(int32_t)));
     ensure_issue(ctx, B);
+    host_trace("fwd: allocs");
     {
         PhaseScope ph(ctx, 0);
         gmi_host::bin_points(ctx, c, pos, col, hot_cap(cfg), true, nullptr, ctx->d_issue);
@@ -142,6 +149,7 @@ int do_forward(gmi_ctx* ctx, const float* pos, const float* col, int B, int N,
         PhaseScope ph(ctx, 2);
         gmi_host::launch_special_forward(ctx, c, image, counts);
     }
+    host_trace("fwd: gather+special launched");
     if (!(ctx->flags & GMI_CTX_ASYNC_ERRORS) || counts != nullptr) {
         int32_t nspec = 0;
         GMI_CUDA(cudaMemcpyAsync(&nspec, c->special_count_d, sizeof(int32_t),
@@ -182,6 +190,16 @@ int do_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
 
 }  // namespace
 
+void host_trace(const char* what) {
+    static const bool on = std::getenv("GMI_TRACE") != nullptr;
+    if (!on) return;
+    static auto last = std::chrono::steady_clock::now();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[gmi] %-28s %9.1f us\n", what,
+                 std::chrono::duration<double, std::micro>(now - last).count());
+    last = now;
+}
+
 namespace gmi_host {
 
 void* dalloc(gmi_ctx* ctx, size_t bytes) {
@@ -192,6 +210,17 @@ void* dalloc(gmi_ctx* ctx, size_t bytes) {
 
 void dfree(gmi_ctx* ctx, void* p) {
     if (p) cudaFreeAsync(p, ctx->stream);
+}
+
+void* scratch(gmi_ctx* ctx, int slot, size_t bytes) {
+    bytes = std::max<size_t>(bytes, 256);
+    if (ctx->ws_cap[slot] < bytes) {
+        if (ctx->ws_ptr[slot]) cudaFreeAsync(ctx->ws_ptr[slot], ctx->stream);
+        const size_t cap = bytes + bytes / 4;  // headroom for slowly growing sizes
+        GMI_CUDA(cudaMallocAsync(&ctx->ws_ptr[slot], cap, ctx->stream));
+        ctx->ws_cap[slot] = cap;
+    }
+    return ctx->ws_ptr[slot];
 }
 
 void* cache_alloc(gmi_cache* c, size_t bytes) {
@@ -531,7 +560,14 @@ int gmi_cache_copy_pixels(const gmi_cache* c, float* normalizer, uint8_t* fallba
         const size_t BHW = static_cast<size_t>(c->B) * c->H * c->W;
         std::vector<Special> sp;
         read_special(c, sp);
-        if (normalizer) {
+        if (normalizer && c->wsum64 != nullptr) {
+            // f64 weight mode: the normaliser lives in f64 (may underflow fp32)
+            std::vector<double> w64(BHW);
+            GMI_CUDA(cudaMemcpyAsync(w64.data(), c->wsum64, sizeof(double) * BHW,
+                                     cudaMemcpyDeviceToHost, c->ctx->stream));
+            GMI_CUDA(cudaStreamSynchronize(c->ctx->stream));
+            for (size_t k = 0; k < BHW; ++k) normalizer[k] = static_cast<float>(w64[k]);
+        } else if (normalizer) {
             GMI_CUDA(cudaMemcpyAsync(normalizer, c->wsum, sizeof(float) * BHW,
                                      cudaMemcpyDeviceToHost, c->ctx->stream));
             GMI_CUDA(cudaStreamSynchronize(c->ctx->stream));
@@ -544,8 +580,6 @@ int gmi_cache_copy_pixels(const gmi_cache* c, float* normalizer, uint8_t* fallba
             if (s.kind == 1) {
                 if (fallback_flag) fallback_flag[k] = 1;
                 if (nearest_index) nearest_index[k] = s.nearest;
-            } else if (s.kind == 2 && normalizer) {
-                normalizer[k] = NAN;  // exact (f64) pixel: normaliser not representable
             }
         }
         return GMI_OK;

@@ -53,6 +53,47 @@ __device__ __forceinline__ double d2_ref(double qx, double qy, double mx,
 }
 
 // ----------------------------------------------------------------------------
+// Exact inclusion with fp32 arithmetic.
+//
+// The reference includes point i in pixel q iff fl64(dx^2 + dy^2) <= r^2
+// (bin_grid.cpp:98).  A point is SAFE when every integer pixel q has
+// |d^2(q) - r^2| > kAmbRel * r^2.  For a safe point every fp32 evaluation of
+// d^2 used by the kernels (relative error < 1e-6) takes the reference's
+// decision, so the hot loops compare in fp32 with no guard band.  The few
+// AMBIGUOUS points (about 1e-4 of random inputs; all of them for integer
+// lattices at integer radii) are flagged once by K1 (bit 31 of the sorted
+// index) and decided with the f64 predicate d2_ref everywhere.
+//
+// Only the integer nearest to each row's two boundary crossings mu_x +- s,
+// s = sqrt(r^2 - dy^2), can be within the band: any other integer is >= 1/2
+// away from both crossings, so |dx^2 - s^2| >= 1/4.
+// ----------------------------------------------------------------------------
+constexpr float kAmbRel = 8e-6f;
+constexpr uint32_t kUnsafeBit = 0x80000000u;
+
+__device__ __forceinline__ bool point_ambiguous(float mx, float my, double r64,
+                                                double r2_64, float r2f) {
+    if (!(fabsf(mx) < 1048576.f && fabsf(my) < 1048576.f)) return true;
+    const float tau = kAmbRel * r2f;
+    const float tx = truncf(mx);
+    const float fmu = mx - tx;  // exact
+    const float rf = static_cast<float>(r64);
+    const int y0 = static_cast<int>(floorf(my - rf)) - 1;
+    const int y1 = static_cast<int>(ceilf(my + rf)) + 1;
+    for (int y = y0; y <= y1; ++y) {
+        const double dy = __dsub_rn(static_cast<double>(y), static_cast<double>(my));
+        const float h2f = static_cast<float>(__dsub_rn(r2_64, __dmul_rn(dy, dy)));
+        if (h2f < -tau) continue;
+        const float s = sqrtf(fmaxf(h2f, 0.f));
+        const float nl = rintf(fmu - s), nr = rintf(fmu + s);
+        const float el = fmaf(nl - fmu, nl - fmu, -h2f);
+        const float er = fmaf(nr - fmu, nr - fmu, -h2f);
+        if (fabsf(el) <= tau || fabsf(er) <= tau) return true;
+    }
+    return false;
+}
+
+// ----------------------------------------------------------------------------
 // Per-image grid geometry (BinGrid fields, bin_grid.hpp:17-28) plus the
 // hot-path extras.
 // ----------------------------------------------------------------------------

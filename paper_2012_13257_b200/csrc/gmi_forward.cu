@@ -28,7 +28,6 @@ constexpr int kTH = 8;        // tile height (pixels)
 constexpr int kThreads = kTW * kTH;
 constexpr int kCap = 1024;    // staged candidates per chunk
 constexpr int kCG = 4;        // channels per pass (grid.z = channel groups)
-constexpr float kWMin = 1e-20f;  // below: recompute the pixel in f64 (K3)
 
 struct FwdParams {
     const Geom* geom;
@@ -39,15 +38,21 @@ struct FwdParams {
     int N, C, W, H;
     double r64, r2_64;   // cutoff, cutoff^2 (f64, as the reference)
     float r2f, guard, nk;  // fp32 r^2, guard band, -log2(e)/(2 sigma^2)
+    double inv2s2;      // 1/(2 sigma^2) (f64 weight mode)
     float* image;       // [B][H][W][C]
     float* wsum;        // [B][H][W]
+    double* wsum64;     // [B][H][W] (f64 weight mode only)
     int32_t* counts;    // [B][H][W] or null
     Special* special;
     int32_t* special_count;
     int special_cap;
 };
 
-template <bool kCount>
+// kF64: weights and sums in f64 (gaussian_weight, core.cpp:49-53, exactly as
+// the reference evaluates it) — used when cutoff > 6 sigma, where the fp32
+// exponent argument (up to (r/sigma)^2/2) would carry more than the 1e-5
+// relative error budget and fp32 weights could underflow.
+template <bool kCount, bool kF64>
 __global__ void __launch_bounds__(kThreads)
 k_forward_tile(FwdParams p) {
     __shared__ float s_x[kCap];
@@ -87,8 +92,12 @@ k_forward_tile(FwdParams p) {
 
     float wsum = 0.f;
     float num[kCG];
+    double wsum64 = 0.0;
+    double num64[kF64 ? kCG : 1];
 #pragma unroll
     for (int c = 0; c < kCG; ++c) num[c] = 0.f;
+#pragma unroll
+    for (int c = 0; c < (kF64 ? kCG : 1); ++c) num64[c] = 0.0;
     int cnt = 0;
 
     if (tid == 0) s_n = 0;
@@ -97,6 +106,18 @@ k_forward_tile(FwdParams p) {
     auto consume = [&](int n) {
         for (int k = 0; k < n; ++k) {
             const float mx = s_x[k], my = s_y[k];
+            if constexpr (kF64) {
+                const double d2 = d2_ref(static_cast<double>(px), static_cast<double>(py),
+                                         static_cast<double>(mx), static_cast<double>(my));
+                if (d2 <= p.r2_64) {
+                    const double w = exp(-d2 * p.inv2s2);
+                    wsum64 += w;
+#pragma unroll
+                    for (int c = 0; c < kCG; ++c) num64[c] += w * static_cast<double>(s_c[c][k]);
+                    if (kCount) ++cnt;
+                }
+                continue;
+            }
             const float dx = fx - mx, dy = fy - my;
             const float d2 = fmaf(dx, dx, dy * dy);
             const float e = d2 - p.r2f;
@@ -165,7 +186,24 @@ k_forward_tile(FwdParams p) {
     const size_t pix = static_cast<size_t>(py) * p.W + px;
     const size_t bp = static_cast<size_t>(b) * p.H * p.W + pix;
     float* out = p.image + bp * p.C + ch0;
-    if (wsum >= kWMin) {
+    if constexpr (kF64) {
+        if (wsum64 > 0.0) {
+            for (int c = 0; c < nch; ++c) out[c] = static_cast<float>(num64[c] / wsum64);
+            if (cg == 0) {
+                p.wsum64[bp] = wsum64;
+                p.wsum[bp] = 1.0f;
+                if (kCount) p.counts[bp] = cnt;
+            }
+        } else if (cg == 0) {
+            p.wsum64[bp] = 0.0;
+            p.wsum[bp] = 0.f;
+            if (kCount) p.counts[bp] = 0;
+            const int slot = atomicAdd(p.special_count, 1);
+            if (slot < p.special_cap) p.special[slot] = Special{b, static_cast<int32_t>(pix), -1, 1};
+        }
+        return;
+    }
+    if (wsum > 0.f) {
         const float inv = 1.0f / wsum;
         for (int c = 0; c < nch; ++c) {
             // num/W with one Newton step: faithful quotient (engine.cpp:97-99)
@@ -177,11 +215,12 @@ k_forward_tile(FwdParams p) {
             if (kCount) p.counts[bp] = cnt;
         }
     } else if (cg == 0) {
-        // empty neighbourhood or fp32 underflow: K3 decides in f64
+        // empty neighbourhood (fp32 weights are >= e^-18 here, so W == 0
+        // exactly when the reference's wsum <= 0, engine.cpp:74-76)
         p.wsum[bp] = 0.f;
-        if (kCount) p.counts[bp] = cnt;
+        if (kCount) p.counts[bp] = 0;
         const int slot = atomicAdd(p.special_count, 1);
-        if (slot < p.special_cap) p.special[slot] = Special{b, static_cast<int32_t>(pix), -1, 0};
+        if (slot < p.special_cap) p.special[slot] = Special{b, static_cast<int32_t>(pix), -1, 1};
     }
 }
 
@@ -233,7 +272,7 @@ __device__ int nearest_exact(const SpecParams& p, const Geom& g, int b,
         for (int k = s + lane; k < e; k += 32) {
             const double d2 = d2_ref(qx, qy, static_cast<double>(p.sx[base + k]),
                                      static_cast<double>(p.sy[base + k]));
-            const int i = p.sidx[base + k];
+            const int i = p.sidx[base + k] & 0x7fffffff;
             if (d2 < best || (d2 == best && i < bi)) {
                 best = d2;
                 bi = i;
@@ -245,7 +284,7 @@ __device__ int nearest_exact(const SpecParams& p, const Geom& g, int b,
         for (int k = lane; k < p.N; k += 32) {
             const double d2 = d2_ref(qx, qy, static_cast<double>(p.sx[base + k]),
                                      static_cast<double>(p.sy[base + k]));
-            const int i = p.sidx[base + k];
+            const int i = p.sidx[base + k] & 0x7fffffff;
             if (d2 < best || (d2 == best && i < bi)) {
                 best = d2;
                 bi = i;
@@ -285,69 +324,21 @@ __device__ int nearest_exact(const SpecParams& p, const Geom& g, int b,
     return bi;
 }
 
+// Fallback pixel (engine.cpp:76-92): NearestPoint copies the colour of the
+// exact argmin (ties to the smallest index); Zero writes 0.
 __device__ void special_pixel(const SpecParams& p, int b, int pix, int slot) {
     const int lane = threadIdx.x & 31;
     const Geom g = p.geom[b];
     const int pr = pix / p.W, pc = pix % p.W;
     const double qx = pc, qy = pr;
     const size_t base = static_cast<size_t>(b) * p.N;
-    // f64 re-evaluation over the reference neighbour set (engine.cpp:59-72)
-    const int cx0 = cell_of(qx - p.r64, g.ox, g.cell, g.n_cols);
-    const int cx1 = cell_of(qx + p.r64, g.ox, g.cell, g.n_cols);
-    const int cy0 = cell_of(qy - p.r64, g.oy, g.cell, g.n_rows);
-    const int cy1 = cell_of(qy + p.r64, g.oy, g.cell, g.n_rows);
-    const double inv2s2 = 1.0 / (2.0 * p.sigma * p.sigma);
-    double W64 = 0.0;
-    double num[kCG];
     float* out = p.image + (static_cast<size_t>(b) * p.H * p.W + pix) * p.C;
-    for (int c0 = 0; c0 < p.C; c0 += kCG) {
-        W64 = 0.0;
-#pragma unroll
-        for (int c = 0; c < kCG; ++c) num[c] = 0.0;
-        for (int cy = cy0; cy <= cy1; ++cy) {
-            const int64_t r0 = g.bin_off + static_cast<int64_t>(cy) * g.n_cols;
-            const int s = p.bins[r0 + cx0], e = p.bins[r0 + cx1 + 1];
-            for (int k = s + lane; k < e; k += 32) {
-                const double mx = p.sx[base + k], my = p.sy[base + k];
-                const double d2 = d2_ref(qx, qy, mx, my);
-                if (d2 <= p.r2_64) {
-                    const double w = exp(-d2 * inv2s2);
-                    W64 += w;
-#pragma unroll
-                    for (int c = 0; c < kCG; ++c)
-                        if (c0 + c < p.C)
-                            num[c] += w * static_cast<double>(
-                                              p.scol[(static_cast<size_t>(b) * p.C + c0 + c) * p.N + k]);
-                }
-            }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            W64 += __shfl_xor_sync(0xffffffffu, W64, o);
-#pragma unroll
-            for (int c = 0; c < kCG; ++c) num[c] += __shfl_xor_sync(0xffffffffu, num[c], o);
-        }
-        if (W64 > 0.0 && lane == 0) {
-#pragma unroll
-            for (int c = 0; c < kCG; ++c)
-                if (c0 + c < p.C) out[c0 + c] = static_cast<float>(num[c] / W64);
-        }
-        if (!(W64 > 0.0)) break;
-    }
-    if (W64 > 0.0) {
-        if (lane == 0 && slot >= 0) p.special[slot].kind = 2;
-        return;
-    }
-    // wsum <= 0: fallback (engine.cpp:76-92)
     int nearest = -1;
     if (p.fallback == GMI_FALLBACK_NEAREST) nearest = nearest_exact(p, g, b, qx, qy);
     if (lane == 0) {
-        if (p.counts) p.counts[static_cast<size_t>(b) * p.H * p.W + pix] = 0;
         for (int c = 0; c < p.C; ++c)
             out[c] = nearest >= 0 ? p.col[(base + nearest) * p.C + c] : 0.0f;
-        if (slot >= 0) {
-            p.special[slot].kind = 1;
-            p.special[slot].nearest = nearest;
-        }
+        p.special[slot].nearest = nearest;
     }
 }
 
@@ -381,8 +372,10 @@ static FwdParams fwd_params(const gmi_cache* c, float* image, int32_t* counts) {
     p.r2f = static_cast<float>(p.r2_64);
     p.guard = 4e-6f * p.r2f + 1e-30f;
     p.nk = static_cast<float>(-1.4426950408889634 / (2.0 * c->sigma * c->sigma));
+    p.inv2s2 = 1.0 / (2.0 * c->sigma * c->sigma);
     p.image = image;
     p.wsum = c->wsum;
+    p.wsum64 = c->wsum64;
     p.counts = counts;
     p.special = c->special;
     p.special_count = c->special_count_d;
@@ -391,15 +384,21 @@ static FwdParams fwd_params(const gmi_cache* c, float* image, int32_t* counts) {
 }
 
 void launch_forward(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts) {
+    // fast path (gmi_gather.cu) unless f64 weights / C > 4 / very wide radius
+    if (!c->force_generic && launch_gather_fast(ctx, c, image, counts)) return;
     const FwdParams p = fwd_params(c, image, counts);
     const int tiles_x = (c->W + kTW - 1) / kTW;
     const int tiles_y = (c->H + kTH - 1) / kTH;
     const dim3 grid(tiles_x, tiles_y * c->B, (c->C + kCG - 1) / kCG);
     GMI_CUDA(cudaMemsetAsync(c->special_count_d, 0, sizeof(int32_t), ctx->stream));
-    if (counts)
-        k_forward_tile<true><<<grid, kThreads, 0, ctx->stream>>>(p);
-    else
-        k_forward_tile<false><<<grid, kThreads, 0, ctx->stream>>>(p);
+    const bool f64 = c->wsum64 != nullptr;
+    if (counts) {
+        if (f64) k_forward_tile<true, true><<<grid, kThreads, 0, ctx->stream>>>(p);
+        else k_forward_tile<true, false><<<grid, kThreads, 0, ctx->stream>>>(p);
+    } else {
+        if (f64) k_forward_tile<false, true><<<grid, kThreads, 0, ctx->stream>>>(p);
+        else k_forward_tile<false, false><<<grid, kThreads, 0, ctx->stream>>>(p);
+    }
     GMI_LAUNCHED(ctx);
 }
 

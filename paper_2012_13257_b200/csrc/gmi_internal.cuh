@@ -58,6 +58,15 @@ struct gmi_ctx {
     std::vector<PhaseMark> marks;
     double phase_ms[GMI_NUM_PHASES] = {0};
     uint64_t phase_calls[GMI_NUM_PHASES] = {0};
+    // grow-only per-call scratch (stream-ordered reuse on the ctx stream)
+    void* ws_ptr[16] = {nullptr};
+    size_t ws_cap[16] = {0};
+};
+
+// scratch slots
+enum WsSlot {
+    WS_BBOX = 0, WS_CELLID, WS_RANK, WS_TMP, WS_BIG, WS_BIGCOUNT, WS_TILES, WS_TSUM,
+    WS_SEGOFF, WS_BLKOFF, WS_PART, WS_HOST_IN0, WS_HOST_IN1, WS_HOST_IN2, WS_COUNT
 };
 
 // RAII phase marker: records an event pair on the ctx stream when profiling.
@@ -81,6 +90,9 @@ struct PhaseScope {
     }
 };
 
+// Host-side latency trace (GMI_TRACE=1): microseconds since the previous mark.
+void host_trace(const char* what);
+
 // A stream-ordered device allocation owned by a cache.
 struct DevBuf {
     void* p = nullptr;
@@ -92,7 +104,7 @@ struct Special {
     int32_t b;
     int32_t pix;      // r * W + c
     int32_t nearest;  // original point index (NearestPoint fallback) or -1
-    int32_t kind;     // 1 = fallback, 2 = exact (f64 weights)
+    int32_t kind;     // 1 = fallback
 };
 
 struct gmi_cache {
@@ -117,12 +129,14 @@ struct gmi_cache {
     float* scol = nullptr;    // [B][C][N] channel-planar
     // per pixel
     float* wsum = nullptr;    // [B][H][W]; 0 => special pixel
+    double* wsum64 = nullptr; // [B][H][W] f64 normaliser (precise mode only)
     // special pixels
     Special* special = nullptr;
     int32_t* special_count_d = nullptr;
     int special_cap = 0;
     int special_count = -1;   // host copy (-1 = not read yet)
     bool special_overflow = false;
+    bool force_generic = false;  // use the generic gather (tests / GMI_GENERIC)
 };
 
 namespace gmi_host {
@@ -130,6 +144,8 @@ namespace gmi_host {
 // memory (stream-ordered)
 void* dalloc(gmi_ctx* ctx, size_t bytes);
 void dfree(gmi_ctx* ctx, void* p);
+// ctx scratch slot of at least `bytes` (contents undefined)
+void* scratch(gmi_ctx* ctx, int slot, size_t bytes);
 void* cache_alloc(gmi_cache* c, size_t bytes);
 
 // ---- binning (gmi_bin.cu) ----
@@ -143,6 +159,7 @@ int host_axis_cells(double span, double cell, int cap);
 
 // ---- forward (gmi_forward.cu) ----
 void launch_forward(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts);
+bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts);
 void launch_special_forward(gmi_ctx* ctx, gmi_cache* c, float* image,
                             int32_t* counts);
 
