@@ -1,0 +1,75 @@
+"""CPU: the multi-GPU host logic with world_size 2 over gloo (the GPU runs use
+one process per GPU over NCCL; only the plumbing differs)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+from paper_2012_13257_b200 import dist as gdist  # noqa: E402
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # batch sharding of B=64 images (weak/strong): disjoint cover
+        s, e = gdist.shard_range(64, world, rank)
+        t = torch.zeros(64)
+        t[s:e] = 1.0
+        dist.all_reduce(t)
+        ok_cover = bool(torch.all(t == 1.0))
+        # device time: max over ranks (timing rule)
+        tmax = gdist.max_over_ranks(10.0 + rank)
+        # huge image: bands + halo-point partial gradients summed over ranks
+        rng = np.random.default_rng(0)
+        H, cutoff = 64, 3.0
+        pos_y = rng.uniform(-0.5, H - 0.5, 500)
+        r0, r1 = gdist.band_rows(H, world, rank)
+        mine = gdist.band_point_mask(pos_y, r0, r1, cutoff)
+        part = torch.tensor(mine.astype(np.float32))
+        gdist.sum_over_ranks(part)
+        nbands = gdist.halo_points(pos_y, H, world, cutoff)
+        ok_halo = bool(np.array_equal(part.numpy().astype(np.int32), nbands))
+        out[rank] = (ok_cover, tmax, ok_halo, int((nbands > 1).sum()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sharding_and_reductions():
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+    for r in range(world):
+        ok_cover, tmax, ok_halo, n_shared = out[r]
+        assert ok_cover
+        assert tmax == 11.0
+        assert ok_halo
+        assert n_shared > 0  # points near the band boundary are shared
+
+
+def test_shard_and_band_logic():
+    for total in (1, 7, 64, 65):
+        for world in (1, 2, 3, 8):
+            spans = [gdist.shard_range(total, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == total
+            assert all(spans[k][1] == spans[k + 1][0] for k in range(world - 1))
+            sizes = [e - s for s, e in spans]
+            assert max(sizes) - min(sizes) <= 1
+    assert gdist.bands_cover(8192, 8)
+    # a point exactly cutoff above a band still reaches its first row
+    assert gdist.band_point_mask(np.array([10.0 - 3.0, 10.0 - 4.1]), 10, 20, 3.0).tolist() == [True, False]
+    assert gdist.weak_scaling_units(64, 8) == 512
+    assert sum(gdist.strong_scaling_batch(64, 8, r) for r in range(8)) == 64
