@@ -33,8 +33,8 @@ using namespace gmi_dev;
 
 namespace {
 
-constexpr int kThreads = 128;
-constexpr int kSmemBudget = 48 * 1024;  // staged pixel bytes per CTA
+constexpr int kThreads = 256;
+constexpr int kSmemBudget = 96 * 1024;  // staged pixel bytes per CTA (2 CTAs/SM)
 
 struct BwdParams {
     const Geom* geom;
@@ -66,13 +66,14 @@ __device__ __forceinline__ bool in_ref(int x, int y, float mx, float my, double 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
 template <int CG>
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, 2)
 k_backward_points(BwdParams p) {
     // [rows][pairs][CG] float4: (u0a,u0b,u1a,u1b, ..., o0a,o0b, ...) as 2*CG float2
     extern __shared__ float4 s_pair[];
     __shared__ int s_run[66];
     __shared__ float s_red[4][kThreads / 32];
     __shared__ int s_region[5];
+    __shared__ int s_next;
 
     // ---- image / cell block of this CTA ----
     int b = 0;
@@ -205,11 +206,40 @@ k_backward_points(BwdParams p) {
     };
     if (staged) {
         const int area = npairs * (ry1 - ry0 + 1);
+        // 8-byte alignment of a pixel pair in W / upstream / image rows
+        const bool vec = (p.W % 2 == 0) && (CG == p.C);
         for (int k = tid; k < area; k += kThreads) {
             const int pp = k % npairs, yy = ry0 + k / npairs;
+            const int xa = rx0 + 2 * pp;
             float ua[CG], oa[CG], ub[CG], ob[CG];
-            pixel_q(rx0 + 2 * pp, yy, ua, oa);
-            pixel_q(rx0 + 2 * pp + 1, yy, ub, ob);
+            if (vec && xa + 1 < p.W) {
+                // both pixels in the frame: 64-bit loads of the pair
+                const size_t pix = img_base + static_cast<size_t>(yy) * p.W + xa;
+                const float2 wv = *reinterpret_cast<const float2*>(p.wsum + pix);
+                const float2* up2 = reinterpret_cast<const float2*>(p.upstream + pix * CG);
+                const float2* im2 = reinterpret_cast<const float2*>(p.image + pix * CG);
+                float upv[2 * CG], imv[2 * CG];
+#pragma unroll
+                for (int j = 0; j < CG; ++j) {
+                    const float2 a = up2[j], c2 = im2[j];
+                    upv[2 * j] = a.x;
+                    upv[2 * j + 1] = a.y;
+                    imv[2 * j] = c2.x;
+                    imv[2 * j + 1] = c2.y;
+                }
+                const float ia = wv.x > 0.f ? 1.0f / wv.x : 0.f;
+                const float ib = wv.y > 0.f ? 1.0f / wv.y : 0.f;
+#pragma unroll
+                for (int c = 0; c < CG; ++c) {
+                    ua[c] = upv[c] * ia;
+                    oa[c] = wv.x > 0.f ? imv[c] : 0.f;
+                    ub[c] = upv[CG + c] * ib;
+                    ob[c] = wv.y > 0.f ? imv[CG + c] : 0.f;
+                }
+            } else {
+                pixel_q(xa, yy, ua, oa);
+                pixel_q(xa + 1, yy, ub, ob);
+            }
             float2* dst = reinterpret_cast<float2*>(s_pair + static_cast<size_t>(k) * CG);
 #pragma unroll
             for (int c = 0; c < CG; ++c) {
@@ -227,7 +257,18 @@ k_backward_points(BwdParams p) {
     const bool use_rec = p.use_rec != 0;
     const int xmin = max(rx0, 0), xmax = min(rx1, p.W - 1);
     const float2 nk2 = f2(nk, nk), q82 = f2(q8, q8), two = f2(2.f, 2.f);
-    for (int k = tid; k < total; k += kThreads) {
+    // dynamic warp tasks of 32 consecutive points (bin order keeps a warp's
+    // points adjacent): balances the CTA's warps without idle tails
+    const int lane = tid & 31;
+    if (tid == 0) s_next = 0;
+    __syncthreads();
+    while (true) {
+        int kb = 0;
+        if (lane == 0) kb = atomicAdd(&s_next, 32);
+        kb = __shfl_sync(0xffffffffu, kb, 0);
+        if (kb >= total) break;
+        const int k = kb + lane;
+        if (k >= total) continue;
         const int s = slot_of(k);
         const float mx = p.sx[base + s], my = p.sy[base + s];
         const uint32_t raw = static_cast<uint32_t>(p.sidx[base + s]);
@@ -248,8 +289,13 @@ k_backward_points(BwdParams p) {
         const float tx = truncf(mx), ty = truncf(my);
         const float fmu = mx - tx, fmy = my - ty;  // exact
         const int bx = static_cast<int>(tx), by = static_cast<int>(ty);
-        const int ya = max(ry0, static_cast<int>(floorf(my - rf)) - 1);
-        const int yb = min(ry1, static_cast<int>(ceilf(my + rf)) + 1);
+        // rows that can hold an in-ball pixel: a safe point's boundary rows are
+        // decided by the fp32 test below, so a small pad (>> fp32 rounding of
+        // my +- r) suffices; flagged points keep a one-row margin for the f64
+        // predicate
+        const float pad = unsafe ? 1.0f : 1e-2f;
+        const int ya = max(ry0, static_cast<int>(ceilf(my - rf - pad)));
+        const int yb = min(ry1, static_cast<int>(floorf(my + rf + pad)));
 
         for (int y = ya; y <= yb; ++y) {
             float dy;
