@@ -97,14 +97,25 @@ k_backward_points(BwdParams p) {
 
     // ---- point runs (one per cell row of the block) ----
     const int nrun = cy1 - cy0;
-    if (tid == 0) {
-        int tot = 0;
-        for (int k = 0; k < nrun; ++k) {
-            const int64_t r0 = g.bin_off + static_cast<int64_t>(cy0 + k) * g.n_cols;
-            s_run[k] = tot;
-            tot += p.bins[r0 + cx1] - p.bins[r0 + cx0];
+    if (tid < 32) {
+        // run lengths loaded by one lane each, prefix-summed with shuffles
+        int carry = 0;
+        for (int k0 = 0; k0 < nrun; k0 += 32) {
+            const int k = k0 + tid;
+            int len = 0;
+            if (k < nrun) {
+                const int64_t r0 = g.bin_off + static_cast<int64_t>(cy0 + k) * g.n_cols;
+                len = p.bins[r0 + cx1] - p.bins[r0 + cx0];
+            }
+            int incl = len;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (tid >= o) incl += t;
+            }
+            if (k < nrun) s_run[k] = carry + incl - len;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
         }
-        s_run[nrun] = tot;
+        if (tid == 0) s_run[nrun] = carry;
     }
     __syncthreads();
     const int total = s_run[nrun];
@@ -251,12 +262,11 @@ k_backward_points(BwdParams p) {
     }
 
     // ---- per point ----
-    const float nk = p.nk, q8 = p.q8, inv_s2 = p.inv_s2;
+    const float nk = p.nk, inv_s2 = p.inv_s2;
     const float r2f = static_cast<float>(p.r2_64), rf = static_cast<float>(p.r64);
     const double r2_64 = p.r2_64;
-    const bool use_rec = p.use_rec != 0;
     const int xmin = max(rx0, 0), xmax = min(rx1, p.W - 1);
-    const float2 nk2 = f2(nk, nk), q82 = f2(q8, q8), two = f2(2.f, 2.f);
+    const float2 nk2 = f2(nk, nk), two = f2(2.f, 2.f);
     // dynamic warp tasks of 32 consecutive points (bin order keeps a warp's
     // points adjacent): balances the CTA's warps without idle tails
     const int lane = tid & 31;
@@ -346,61 +356,46 @@ k_backward_points(BwdParams p) {
                 gy = fmaf(gyr, dy, gy);
                 continue;
             }
-            // pair-aligned span [xs, xe] (rx0 even); the end pixels outside
-            // [xl, xr] are masked out of the first / last pair
+            // pair-aligned span (rx0 is even): pairs xs..xs+2(np-1); the end
+            // pixels outside [xl, xr] get weight 0 in the first / last pair
             const int xs = xl - ((xl - rx0) & 1);
-            const int xe = xr + (((xr - rx0) & 1) ^ 1);
-            const int np = (xe - xs + 1) >> 1;
-            const float2 m_first = f2(((xl - rx0) & 1) ? 0.f : 1.f, 1.f);
-            const float2 m_last = f2(1.f, ((xr - rx0) & 1) ? 1.f : 0.f);
+            const int np = ((xr - xs) >> 1) + 1;
+            const float mf = ((xl - rx0) & 1) ? 0.f : 1.f;
+            const float ml = ((xr - rx0) & 1) ? 1.f : 0.f;
             float2 dx = f2(static_cast<float>(xs - bx) - fmu, 0.f);
             dx.y = dx.x + 1.0f;
             const float2 dy22 = f2(dy2, dy2);
-            float2 w = __fmul2_rn(__ffma2_rn(dx, dx, dy22), nk2);
-            w = f2(ex2(w.x), ex2(w.y));
-            float2 R = f2(0.f, 0.f);
-            if (use_rec) {
-                // R(x) = w(x+2)/w(x) = 2^(nk (4 dx + 4))
-                R = __fmul2_rn(__ffma2_rn(f2(4.f, 4.f), dx, f2(4.f, 4.f)), nk2);
-                R = f2(ex2(R.x), ex2(R.y));
-            }
             float2 gyr2 = f2(0.f, 0.f);
             const float4* pr = s_pair + (static_cast<size_t>(y - ry0) * npairs + ((xs - rx0) >> 1)) * CG;
-            auto body = [&](float2 wm) {
-                float4 v[CG];
+            float4 v[CG];
 #pragma unroll
-                for (int c = 0; c < CG; ++c) v[c] = pr[c];
+            for (int c = 0; c < CG; ++c) v[c] = pr[c];
+            for (int j = 0; j < np; ++j) {
+                // prefetch the next pair while this one is evaluated
+                float4 vn[CG];
+                if (j + 1 < np) {
+#pragma unroll
+                    for (int c = 0; c < CG; ++c) vn[c] = pr[CG + c];
+                }
+                const float2 arg = __fmul2_rn(__ffma2_rn(dx, dx, dy22), nk2);
+                float2 w = f2(ex2(arg.x), ex2(arg.y));
+                if (j == 0) w.x *= mf;
+                if (j == np - 1) w.y *= ml;
                 const float2* q = reinterpret_cast<const float2*>(v);
                 // t = sum_c u_c (c_ic - out_c)
                 float2 t = __fmul2_rn(q[0], __fadd2_rn(cc2[0], f2(-q[CG].x, -q[CG].y)));
 #pragma unroll
                 for (int c = 1; c < CG; ++c)
                     t = __ffma2_rn(q[c], __fadd2_rn(cc2[c], f2(-q[CG + c].x, -q[CG + c].y)), t);
-                const float2 a = __fmul2_rn(wm, t);
+                const float2 a = __fmul2_rn(w, t);
 #pragma unroll
-                for (int c = 0; c < CG; ++c) dcol[c] = __ffma2_rn(wm, q[c], dcol[c]);
+                for (int c = 0; c < CG; ++c) dcol[c] = __ffma2_rn(w, q[c], dcol[c]);
                 gx2 = __ffma2_rn(a, dx, gx2);
                 gyr2 = __fadd2_rn(gyr2, a);
-            };
-            auto advance = [&]() {
                 dx = __fadd2_rn(dx, two);
                 pr += CG;
-                if (use_rec) {
-                    w = __fmul2_rn(w, R);
-                    R = __fmul2_rn(R, q82);
-                } else {
-                    const float2 arg = __fmul2_rn(__ffma2_rn(dx, dx, dy22), nk2);
-                    w = f2(ex2(arg.x), ex2(arg.y));
-                }
-            };
-            body(__fmul2_rn(w, np == 1 ? __fmul2_rn(m_first, m_last) : m_first));
-            if (np > 1) {
-                advance();
-                for (int j = 1; j < np - 1; ++j) {
-                    body(w);
-                    advance();
-                }
-                body(__fmul2_rn(w, m_last));
+#pragma unroll
+                for (int c = 0; c < CG; ++c) v[c] = vn[c];
             }
             gy = fmaf(gyr2.x + gyr2.y, dy, gy);
         }

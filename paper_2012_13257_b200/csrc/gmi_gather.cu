@@ -54,7 +54,7 @@ struct SmemGather {
     int run_g[kRsMax];
     int scan_w[kNT / 32];
     int n_runs, cur_cy, cur_off, done, any_flag;
-    int cx0, cx1, cy1;
+    int cx0, cx1, cy1, pre;
 };
 
 struct GatherParams {
@@ -124,19 +124,61 @@ k_gather(GatherParams p) {
     const int wq1 = min(nq - 1, fine_col(whi, g.qx0, g.qscale) - q_lo);
     const float band_lo = Y.x - p.rf - epsy, band_hi = Y.y + p.rf + epsy;
 
-    if (tid == 0) {
-        // the f64 cell rectangle is needed by thread 0 only (chunk builder)
-        S.cx0 = cell_of(xlo, g.ox, g.cell, g.n_cols);
-        S.cx1 = cell_of(xhi, g.ox, g.cell, g.n_cols);
-        S.cur_cy = cell_of(ylo, g.oy, g.cell, g.n_rows);
-        S.cy1 = cell_of(yhi, g.oy, g.cell, g.n_rows);
-        S.cur_off = 0;
-        S.done = 0;
+    if (warp == 0) {
+        // the f64 cell rectangle (four lanes in parallel)
+        int cv = 0;
+        if (lane == 0) cv = cell_of(xlo, g.ox, g.cell, g.n_cols);
+        if (lane == 1) cv = cell_of(xhi, g.ox, g.cell, g.n_cols);
+        if (lane == 2) cv = cell_of(ylo, g.oy, g.cell, g.n_rows);
+        if (lane == 3) cv = cell_of(yhi, g.oy, g.cell, g.n_rows);
+        const int cx0 = __shfl_sync(0xffffffffu, cv, 0), cx1 = __shfl_sync(0xffffffffu, cv, 1);
+        const int cy0 = __shfl_sync(0xffffffffu, cv, 2), cy1 = __shfl_sync(0xffffffffu, cv, 3);
+        // common case: <= 32 cell rows and <= kCap candidates -> one chunk,
+        // runs loaded by one lane each (no serial chain of dependent loads)
+        const int nrows = cy1 - cy0 + 1;
+        bool one = false;
+        if (nrows <= 32 && nrows <= kRsMax) {
+            int gs = 0, len = 0;
+            if (lane < nrows) {
+                const int64_t r0 = g.bin_off + static_cast<int64_t>(cy0 + lane) * g.n_cols;
+                gs = p.bins[r0 + cx0];
+                len = p.bins[r0 + cx1 + 1] - gs;
+            }
+            int incl = len;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            const int tot = __shfl_sync(0xffffffffu, incl, 31);
+            if (tot <= kCap) {
+                one = true;
+                if (lane < nrows) {
+                    S.run_g[lane] = gs;
+                    S.run_beg[lane] = incl - len;
+                }
+                if (lane == 0) {
+                    S.run_beg[nrows] = tot;
+                    S.n_runs = nrows;
+                    S.pre = 1;
+                }
+            }
+        }
+        if (lane == 0) {
+            S.cx0 = cx0;
+            S.cx1 = cx1;
+            S.cy1 = cy1;
+            S.cur_cy = one ? cy1 + 1 : cy0;
+            S.cur_off = 0;
+            S.done = one ? 1 : 0;
+            if (!one) S.pre = 0;
+        }
     }
     __syncthreads();
     while (true) {
         // ---- next chunk of runs (<= kRsMax runs, <= kCap candidates) ----
-        if (tid == 0) {
+        if (tid == 0 && S.pre) {
+            S.pre = 0;  // the single chunk was prepared above
+        } else if (tid == 0) {
             const int cx0 = S.cx0, cx1 = S.cx1, cy1 = S.cy1;
             int n = 0, tot = 0, cy = S.cur_cy, off = S.cur_off;
             while (cy <= cy1 && n < kRsMax && tot < kCap) {
