@@ -367,16 +367,10 @@ k_backward_points(BwdParams p) {
             const float2 dy22 = f2(dy2, dy2);
             float2 gyr2 = f2(0.f, 0.f);
             const float4* pr = s_pair + (static_cast<size_t>(y - ry0) * npairs + ((xs - rx0) >> 1)) * CG;
-            float4 v[CG];
-#pragma unroll
-            for (int c = 0; c < CG; ++c) v[c] = pr[c];
             for (int j = 0; j < np; ++j) {
-                // prefetch the next pair while this one is evaluated
-                float4 vn[CG];
-                if (j + 1 < np) {
+                float4 v[CG];
 #pragma unroll
-                    for (int c = 0; c < CG; ++c) vn[c] = pr[CG + c];
-                }
+                for (int c = 0; c < CG; ++c) v[c] = pr[c];
                 const float2 arg = __fmul2_rn(__ffma2_rn(dx, dx, dy22), nk2);
                 float2 w = f2(ex2(arg.x), ex2(arg.y));
                 if (j == 0) w.x *= mf;
@@ -394,8 +388,6 @@ k_backward_points(BwdParams p) {
                 gyr2 = __fadd2_rn(gyr2, a);
                 dx = __fadd2_rn(dx, two);
                 pr += CG;
-#pragma unroll
-                for (int c = 0; c < CG; ++c) v[c] = vn[c];
             }
             gy = fmaf(gyr2.x + gyr2.y, dy, gy);
         }

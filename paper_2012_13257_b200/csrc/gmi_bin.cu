@@ -9,11 +9,12 @@
 //                    atomic arrival rank inside its cell
 //   scan             segmented exclusive scan -> bin_start (bin_grid.cpp:72-75)
 //   k_scatter        point -> bin_start[cell] + rank (unordered within a cell)
-//   k_cellsort_*     order each cell: by original index (reference export,
-//                    bin_grid.cpp:76-80) or, for the hot layout, by (fine
-//                    x-column, index) and emit the bin-ordered SoA copy
-//                    (x, y, index, colour planes) + colour validation
-//                    (core.cpp:80-92).
+//   k_cellsort_*     order each cell by original index (bin_grid.cpp:76-80),
+//                    in place: this IS the reference's point_index
+//   k_emit           hot layout in that order, thread per slot: the
+//                    bin-ordered SoA (x, y, index|ambiguous-flag, colour
+//                    planes), boundary-ambiguity flags, colour validation
+//                    (core.cpp:80-92)
 #include <algorithm>
 
 #include "gmi_internal.cuh"
@@ -204,63 +205,19 @@ __global__ void k_scan_apply(int32_t* __restrict__ data,
 }
 
 // ---------------------------------------------------------------------------
-// Within-cell ordering.
-struct SortOut {
-    bool hot;
-    // hot layout
-    float* sx;
-    float* sy;
-    int32_t* sidx;
-    float* scol;
-    const float* col;
-    int C;
-    unsigned long long* issue;
-    int classify;      // 1: flag boundary-ambiguous points (kUnsafeBit)
-    double r64, r2_64;
-    float r2f;
-    // reference export
-    int32_t* point_index;
-};
+// Within-cell ordering: ascending original index (bin_grid.cpp:76-80), sorted
+// in place in the index array.  This is the reference's point_index; the hot
+// SoA is emitted in exactly this order (the gather re-orders by x itself).
+constexpr int kRegCell = 8;
 
-__device__ __forceinline__ unsigned long long sort_key(bool hot, int i,
-                                                       const float2* p,
-                                                       const Geom& g) {
-    if (!hot) return static_cast<unsigned long long>(i);
-    const int fc = fine_col(p[i].x, g.qx0, g.qscale);
-    const uint32_t ufc = static_cast<uint32_t>(fc) ^ 0x80000000u;
-    return (static_cast<unsigned long long>(ufc) << 32) | static_cast<uint32_t>(i);
+__device__ __forceinline__ void cswap(int& a, int& b) {
+    const int lo = min(a, b), hi = max(a, b);
+    a = lo;
+    b = hi;
 }
 
-// Emits slot k (image-local) of the sorted layout for original point i.
-__device__ __forceinline__ void emit(const SortOut& o, int b, int N, int k,
-                                     int i, const float2* p) {
-    const size_t bk = static_cast<size_t>(b) * N + k;
-    if (!o.hot) {
-        o.point_index[bk] = i;
-        return;
-    }
-    const float2 v = p[i];
-    o.sx[bk] = v.x;
-    o.sy[bk] = v.y;
-    const bool amb = o.classify && point_ambiguous(v.x, v.y, o.r64, o.r2_64, o.r2f);
-    o.sidx[bk] = static_cast<int32_t>(static_cast<uint32_t>(i) | (amb ? kUnsafeBit : 0u));
-    const float* c = o.col + (static_cast<size_t>(b) * N + i) * o.C;
-    unsigned code = 0;
-    for (int ch = 0; ch < o.C; ++ch) {
-        const float cv = c[ch];
-        o.scol[(static_cast<size_t>(b) * o.C + ch) * N + k] = cv;
-        if (code == 0) {
-            if (!is_finite_f(cv)) code = 1;             // NonFiniteValue
-            else if (cv < 0.0f || cv > 1.0f) code = 2;  // ColorOutOfRange
-        }
-    }
-    if (code) atomicMin(o.issue + b, (static_cast<unsigned long long>(i) << 8) | code);
-}
-
-__global__ void k_cellsort_small(const float2* __restrict__ pos, int N,
-                                 const Geom* __restrict__ geom,
-                                 const int32_t* __restrict__ bins,
-                                 const int32_t* __restrict__ tmp, SortOut o,
+__global__ void k_cellsort_small(int N, const Geom* __restrict__ geom,
+                                 const int32_t* __restrict__ bins, int32_t* __restrict__ tmp,
                                  int2* __restrict__ big, int32_t* big_count) {
     const int b = blockIdx.y;
     const Geom g = geom[b];
@@ -268,17 +225,33 @@ __global__ void k_cellsort_small(const float2* __restrict__ pos, int N,
     if (cell >= g.n_cols * g.n_rows) return;
     const int s = bins[g.bin_off + cell], e = bins[g.bin_off + cell + 1];
     const int n = e - s;
-    if (n == 0) return;
-    const float2* p = pos + static_cast<size_t>(b) * N;
-    const int32_t* t = tmp + static_cast<size_t>(b) * N;
+    if (n <= 1) return;
+    int32_t* t = tmp + static_cast<size_t>(b) * N + s;
+    if (n <= kRegCell) {
+        // sorting network on registers (padding sorts to the end)
+        int v[kRegCell];
+#pragma unroll
+        for (int k = 0; k < kRegCell; ++k) v[k] = k < n ? t[k] : INT32_MAX;
+        // Batcher odd-even merge network for 8 keys (19 comparators)
+        cswap(v[0], v[1]); cswap(v[2], v[3]); cswap(v[4], v[5]); cswap(v[6], v[7]);
+        cswap(v[0], v[2]); cswap(v[1], v[3]); cswap(v[4], v[6]); cswap(v[5], v[7]);
+        cswap(v[1], v[2]); cswap(v[5], v[6]);
+        cswap(v[0], v[4]); cswap(v[1], v[5]); cswap(v[2], v[6]); cswap(v[3], v[7]);
+        cswap(v[2], v[4]); cswap(v[3], v[5]);
+        cswap(v[1], v[2]); cswap(v[3], v[4]); cswap(v[5], v[6]);
+#pragma unroll
+        for (int k = 0; k < kRegCell; ++k)
+            if (k < n) t[k] = v[k];
+        return;
+    }
     if (n > kSmallCell) {
         const int slot = atomicAdd(big_count, 1);
         big[slot] = make_int2(b, cell);
         return;
     }
-    unsigned long long key[kSmallCell];
+    int key[kSmallCell];
     for (int k = 0; k < n; ++k) {
-        const unsigned long long v = sort_key(o.hot, t[s + k], p, g);
+        const int v = t[k];
         int j = k;
         while (j > 0 && key[j - 1] > v) {
             key[j] = key[j - 1];
@@ -286,79 +259,115 @@ __global__ void k_cellsort_small(const float2* __restrict__ pos, int N,
         }
         key[j] = v;
     }
-    for (int k = 0; k < n; ++k)
-        emit(o, b, N, s + k, static_cast<int>(key[k] & 0xffffffffu), p);
+    for (int k = 0; k < n; ++k) t[k] = key[k];
 }
 
-// One CTA per big cell (device-side list); bitonic sort in shared memory for
-// n <= kBigSmemKeys, otherwise an in-place global bitonic network over the
-// index array with keys recomputed on the fly (slow path for pathological
-// clusters).
-__global__ void k_cellsort_big(const float2* __restrict__ pos, int N,
-                               const Geom* __restrict__ geom,
-                               const int32_t* __restrict__ bins,
-                               int32_t* __restrict__ tmp, SortOut o,
-                               const int2* __restrict__ big,
-                               const int32_t* __restrict__ big_count) {
-    extern __shared__ unsigned long long skey[];
+// One CTA per big cell: bitonic sort of the cell's indices in shared memory
+// (n <= kBigSmemKeys) or in place in global memory (slow path).
+__global__ void k_cellsort_big(int N, const Geom* __restrict__ geom,
+                               const int32_t* __restrict__ bins, int32_t* __restrict__ tmp,
+                               const int2* __restrict__ big, const int32_t* __restrict__ big_count) {
+    extern __shared__ int skey[];
     const int nbig = *big_count;
     for (int job = blockIdx.x; job < nbig; job += gridDim.x) {
         const int b = big[job].x, cell = big[job].y;
         const Geom g = geom[b];
         const int s = bins[g.bin_off + cell], e = bins[g.bin_off + cell + 1];
         const int n = e - s;
-        const float2* p = pos + static_cast<size_t>(b) * N;
         int32_t* t = tmp + static_cast<size_t>(b) * N + s;
         int np2 = 1;
         while (np2 < n) np2 <<= 1;
-        if (n <= kBigSmemKeys) {
-            for (int k = threadIdx.x; k < np2; k += blockDim.x)
-                skey[k] = k < n ? sort_key(o.hot, t[k], p, g) : ~0ull;
+        const bool in_smem = n <= kBigSmemKeys;
+        int* key = in_smem ? skey : t;
+        if (in_smem) {
+            for (int k = threadIdx.x; k < np2; k += blockDim.x) skey[k] = k < n ? t[k] : INT32_MAX;
             __syncthreads();
-            for (int size = 2; size <= np2; size <<= 1) {
-                for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                    for (int k = threadIdx.x; k < np2; k += blockDim.x) {
-                        const int partner = (stride == (size >> 1))
-                                                ? (k ^ (size - 1))
-                                                : (k ^ stride);
-                        if (partner > k) {
-                            const unsigned long long a = skey[k], c = skey[partner];
-                            if (a > c) {
-                                skey[k] = c;
-                                skey[partner] = a;
-                            }
+        }
+        // flip formulation: all comparators ascending, so padding (+inf) never
+        // moves below n and partners >= n can be skipped in place
+        for (int size = 2; size <= np2; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int k = threadIdx.x; k < np2; k += blockDim.x) {
+                    const int partner = (stride == (size >> 1)) ? (k ^ (size - 1)) : (k ^ stride);
+                    if (partner > k && (in_smem || partner < n)) {
+                        const int a = key[k], c = key[partner];
+                        if (a > c) {
+                            key[k] = c;
+                            key[partner] = a;
                         }
                     }
-                    __syncthreads();
                 }
+                __syncthreads();
             }
-            for (int k = threadIdx.x; k < n; k += blockDim.x)
-                emit(o, b, N, s + k, static_cast<int>(skey[k] & 0xffffffffu), p);
-            __syncthreads();
-        } else {
-            // global in-place network over indices; +inf padding never moves
-            // below n with the flip formulation, so partners >= n are skipped.
-            for (int size = 2; size <= np2; size <<= 1) {
-                for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                    for (int k = threadIdx.x; k < np2; k += blockDim.x) {
-                        const int partner = (stride == (size >> 1))
-                                                ? (k ^ (size - 1))
-                                                : (k ^ stride);
-                        if (partner > k && partner < n) {
-                            const int ia = t[k], ic = t[partner];
-                            if (sort_key(o.hot, ia, p, g) > sort_key(o.hot, ic, p, g)) {
-                                t[k] = ic;
-                                t[partner] = ia;
-                            }
-                        }
-                    }
-                    __syncthreads();
-                }
-            }
-            for (int k = threadIdx.x; k < n; k += blockDim.x) emit(o, b, N, s + k, t[k], p);
+        }
+        if (in_smem) {
+            for (int k = threadIdx.x; k < n; k += blockDim.x) t[k] = skey[k];
             __syncthreads();
         }
     }
+}
+
+// Hot layout, thread per slot (coalesced writes): gather the point, classify
+// boundary ambiguity (kUnsafeBit, gmi_common.cuh), validate colours
+// (core.cpp:80-92, first violation by index via atomicMin).
+struct EmitParams {
+    const float2* pos;
+    const float* col;
+    const int32_t* tmp;
+    float* sx;
+    float* sy;
+    int32_t* sidx;
+    float* scol;
+    unsigned long long* issue;
+    int N, C;
+    int classify;
+    float rf, r2f;
+};
+
+__device__ __forceinline__ bool point_ambiguous_f32(float mx, float my, float rf, float r2f) {
+    if (!(fabsf(mx) < 1048576.f && fabsf(my) < 1048576.f)) return true;
+    const float tau = kAmbRel * r2f;
+    const float tx = truncf(mx), ty = truncf(my);
+    const float fmu = mx - tx, fmy = my - ty;  // exact
+    const int by = static_cast<int>(ty);
+    const int y0 = static_cast<int>(floorf(my - rf - 0.02f));
+    const int y1 = static_cast<int>(ceilf(my + rf + 0.02f));
+    for (int y = y0; y <= y1; ++y) {
+        // dy = y - my to ~1 ulp (|dy| <= r + 1); h2 error ~1e-7 r^2 << tau
+        const float dy = static_cast<float>(y - by) - fmy;
+        const float h2f = fmaf(-dy, dy, r2f);
+        if (h2f < -tau) continue;
+        const float s = sqrtf(fmaxf(h2f, 0.f));
+        const float nl = rintf(fmu - s), nr = rintf(fmu + s);
+        const float el = fmaf(nl - fmu, nl - fmu, -h2f);
+        const float er = fmaf(nr - fmu, nr - fmu, -h2f);
+        if (fabsf(el) <= tau || fabsf(er) <= tau) return true;
+    }
+    return false;
+}
+
+__global__ void k_emit(EmitParams p) {
+    const int b = blockIdx.y;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= p.N) return;
+    const size_t bk = static_cast<size_t>(b) * p.N + k;
+    const int i = p.tmp[bk];
+    const float2 v = p.pos[static_cast<size_t>(b) * p.N + i];
+    p.sx[bk] = v.x;
+    p.sy[bk] = v.y;
+    const bool amb = p.classify && point_ambiguous_f32(v.x, v.y, p.rf, p.r2f);
+    p.sidx[bk] = static_cast<int32_t>(static_cast<uint32_t>(i) | (amb ? kUnsafeBit : 0u));
+    const float* c = p.col + (static_cast<size_t>(b) * p.N + i) * p.C;
+    unsigned code = 0;
+    for (int ch = 0; ch < p.C; ++ch) {
+        const float cv = c[ch];
+        p.scol[(static_cast<size_t>(b) * p.C + ch) * p.N + k] = cv;
+        if (code == 0) {
+            if (!is_finite_f(cv)) code = 1;             // NonFiniteValue
+            else if (cv < 0.0f || cv > 1.0f) code = 2;  // ColorOutOfRange
+        }
+    }
+    if (code) atomicMin(p.issue + b, (static_cast<unsigned long long>(i) << 8) | code);
 }
 
 }  // namespace
@@ -480,37 +489,37 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
     k_scatter<<<pgrid, 256, 0, st>>>(N, c->geom_d, c->bins, cellid, rank, tmp);
     GMI_LAUNCHED(ctx);
 
-    SortOut o{};
-    o.hot = hot;
-    if (hot) {
-        o.sx = c->sx;
-        o.sy = c->sy;
-        o.sidx = c->sidx;
-        o.scol = c->scol;
-        o.col = col;
-        o.C = c->C;
-        o.issue = d_issue;
-        // f64 weight mode decides every pair in f64: no classification needed
-        o.classify = c->wsum64 == nullptr ? 1 : 0;
-        o.r64 = c->cutoff;
-        o.r2_64 = c->cutoff * c->cutoff;
-        o.r2f = static_cast<float>(o.r2_64);
-    } else {
-        o.point_index = point_index_out;
-    }
     int2* d_big = static_cast<int2*>(scratch(ctx, WS_BIG, sizeof(int2) * std::max<size_t>(1, BN / (kSmallCell + 1) + 1)));
     int32_t* d_bigcount = static_cast<int32_t*>(scratch(ctx, WS_BIGCOUNT, sizeof(int32_t)));
     GMI_CUDA(cudaMemsetAsync(d_bigcount, 0, sizeof(int32_t), st));
-    k_cellsort_small<<<dim3((max_bins + 127) / 128, B), 128, 0, st>>>(
-        p2, N, c->geom_d, c->bins, tmp, o, d_big, d_bigcount);
+    k_cellsort_small<<<dim3((max_bins + 127) / 128, B), 128, 0, st>>>(N, c->geom_d, c->bins, tmp,
+                                                                      d_big, d_bigcount);
     GMI_LAUNCHED(ctx);
-    const int smem = kBigSmemKeys * sizeof(unsigned long long);
-    GMI_CUDA(cudaFuncSetAttribute(k_cellsort_big,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    k_cellsort_big<<<ctx->num_sms, 1024, smem, st>>>(p2, N, c->geom_d, c->bins, tmp, o,
-                                                     d_big, d_bigcount);
+    const int smem = kBigSmemKeys * sizeof(int);
+    GMI_CUDA(cudaFuncSetAttribute(k_cellsort_big, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_cellsort_big<<<ctx->num_sms, 1024, smem, st>>>(N, c->geom_d, c->bins, tmp, d_big, d_bigcount);
     GMI_LAUNCHED(ctx);
-
+    if (!hot) {
+        GMI_CUDA(cudaMemcpyAsync(point_index_out, tmp, sizeof(int32_t) * BN, cudaMemcpyDeviceToDevice, st));
+    } else {
+        EmitParams e{};
+        e.pos = p2;
+        e.col = col;
+        e.tmp = tmp;
+        e.sx = c->sx;
+        e.sy = c->sy;
+        e.sidx = c->sidx;
+        e.scol = c->scol;
+        e.issue = d_issue;
+        e.N = N;
+        e.C = c->C;
+        // f64 weight mode decides every pair in f64: no classification needed
+        e.classify = c->wsum64 == nullptr ? 1 : 0;
+        e.rf = static_cast<float>(c->cutoff);
+        e.r2f = static_cast<float>(c->cutoff * c->cutoff);
+        k_emit<<<pgrid, 256, 0, st>>>(e);
+        GMI_LAUNCHED(ctx);
+    }
     host_trace("bin: scan..cellsort launched");
 }
 
