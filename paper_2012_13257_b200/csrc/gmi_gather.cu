@@ -328,18 +328,11 @@ k_gather(GatherParams p) {
 
         // ---- gather: 4 pixels per candidate, f32x2 ----
         const uint16_t* lst = S.list[warp];
-        // software-pipelined: the next candidate's record is loaded while the
-        // current one is evaluated (hides the LDS.U16 -> LDS.128 chain)
-        float4 a_nx = S.A[lst[min(ts, te - 1 < 0 ? 0 : te - 1)]];
-        float2 b_nx = CC > 2 ? S.Bc[lst[min(ts, te - 1 < 0 ? 0 : te - 1)]] : f2(0.f, 0.f);
+#pragma unroll 2
         for (int t = ts; t < te; ++t) {
-            const float4 a = a_nx;
-            const float2 bcur = b_nx;
-            {
-                const int kn = lst[t + 1 < te ? t + 1 : t];
-                a_nx = S.A[kn];
-                if (CC > 2) b_nx = S.Bc[kn];
-            }
+            const int kc = lst[t];
+            const float4 a = S.A[kc];
+            const float2 bcur = CC > 2 ? S.Bc[kc] : f2(0.f, 0.f);
             const float2 dx = __fadd2_rn(X, f2(-a.x, -a.x));
             const float2 dy = __fadd2_rn(Y, f2(-a.y, -a.y));
             const float2 sxx = __fmul2_rn(dx, dx);
