@@ -33,6 +33,18 @@ sys.path.insert(0, ROOT)
 CFG = dict(B=64, N=262144, C=3, W=1024, H=1024, sigma=1.5, cutoff=4.5)
 METRIC = "output Mpixels/s fwd+bwd at 1024^2, N=262k pts, C=3 (1/2/4/8 B200) vs CPU"
 WORKLOAD = "B=64 x 1024^2, N=262144, C=3, sigma=1.5, cutoff=3sigma (BASELINE configs[2])"
+# BASELINE.json configs (1-based); the headline line is config 3 (the default)
+CONFIGS = {
+    1: dict(B=1, N=4096, C=3, W=128, H=128, sigma=1.0, cutoff=3.0, fwd_only=True,
+            workload="B=1 x 128^2, N=4096, C=3, sigma=1, forward only (BASELINE configs[0])"),
+    2: dict(B=16, N=65536, C=3, W=512, H=512, sigma=1.0, cutoff=3.0,
+            workload="B=16 x 512^2, N=65536, C=3, sigma=1 (BASELINE configs[1])"),
+    3: dict(CFG, workload=WORKLOAD),
+    4: dict(B=1, N=16777216, C=3, W=8192, H=8192, sigma=1.0, cutoff=3.0,
+            workload="B=1 x 8192^2, N=16M, C=3, sigma=1, single GPU (BASELINE configs[3])"),
+    5: dict(B=8, N=1048576, C=64, W=2048, H=2048, sigma=4.0, cutoff=12.0, cluster=0.05,
+            workload="B=8 x 2048^2, N=1M (5% in a 32^2 cluster), C=64, sigma=4 (BASELINE configs[4])"),
+}
 
 
 def peaks():
@@ -198,7 +210,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gmi", choices=["gmi", "reference"])
-    ap.add_argument("--batch", type=int, default=CFG["B"])
+    ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS),
+                    help="BASELINE.json config (1-based); 3 is the headline")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -216,7 +230,10 @@ def main():
     assert args.warmup >= 3, "contract: at least 3 warm-up steps"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    cfg = dict(CFG, B=args.batch)
+    cfg = dict(CONFIGS[args.config])
+    if args.batch:
+        cfg["B"] = args.batch
+    fwd_only = cfg.get("fwd_only", False)
     B, N, C, W, H = cfg["B"], cfg["N"], cfg["C"], cfg["W"], cfg["H"]
     sigma, cutoff = cfg["sigma"], cfg["cutoff"]
 
@@ -231,6 +248,11 @@ def main():
         pos = torch.empty(B, N, 2, device=dev)
         pos[..., 0].uniform_(-0.5, W - 0.5, generator=g)
         pos[..., 1].uniform_(-0.5, H - 0.5, generator=g)
+        nc = int(cfg.get("cluster", 0.0) * N)
+        if nc:
+            # configs[4]: the first 5% of the points in one 32x32-pixel square
+            corner = torch.rand(B, 1, 2, device=dev, generator=g) * torch.tensor([W - 32.0, H - 32.0], device=dev)
+            pos[:, :nc] = corner + torch.rand(B, nc, 2, device=dev, generator=g) * 32.0
         col = torch.rand(B, N, C, device=dev, generator=g)
         up = torch.rand(B, H, W, C, device=dev, generator=g) * 2 - 1
         img = torch.empty(B, H, W, C, device=dev)
@@ -240,7 +262,8 @@ def main():
 
     def step():
         cache = ctx.forward_device(pos, col, B, N, C, W, H, sigma, cutoff, 0, img)
-        ctx.backward_device(pos, col, B, N, C, W, H, sigma, cutoff, 0, cache, up, dcol, dpos)
+        if not fwd_only:
+            ctx.backward_device(pos, col, B, N, C, W, H, sigma, cutoff, 0, cache, up, dcol, dpos)
         return cache
 
     # warm-up mirrors the timed loop (two caches kept alive) so the
@@ -297,7 +320,7 @@ def main():
     # ---- roofline of the dominant kernel (per launch = whole batch) ----
     hbm_peak, sm_mhz, peak_kind = peaks()
     per_call = {name: phase_ms[k] / max(1, phase_calls[k]) for k, name in enumerate(gmi.Context.PHASES)}
-    dom = max(("gather", "points_bwd"), key=lambda k: per_call[k])
+    dom = "gather" if fwd_only else max(("gather", "points_bwd"), key=lambda k: per_call[k])
     pts_bytes = 4 * N * (2 + C)
     img_bytes = 4 * H * W * C
     alg_bytes = {"gather": B * (pts_bytes + img_bytes),            # points in, image out
@@ -307,55 +330,61 @@ def main():
     achieved = alg_bytes[dom] / t_dom / 1e9
     fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # T FP32-instr/s
     fp32_ach = alg_fp32[dom] / t_dom / 1e12
-    total_fp32 = B * P_img * (17 + 3 * C)
+    total_fp32 = B * P_img * ((6 + C) if fwd_only else (17 + 3 * C))
     step_fp32_frac = total_fp32 / (ms_step * 1e-3) / 1e12 / fp32_peak
 
-    # ---- e2e through the host-buffer C-ABI ----
-    pinned = [pos.cpu().pin_memory(), col.cpu().pin_memory(), up.cpu().pin_memory(),
-              torch.empty(B, H, W, C).pin_memory(), torch.empty(B, N, C).pin_memory(),
-              torch.empty(B, N, 2).pin_memory()]
-    hpos, hcol, hup, himg, hdc, hdp = (t.numpy() for t in pinned)
-    import ctypes as Cty
-    fp = Cty.POINTER(Cty.c_float)
-    cfg_c = gmi._lib.GmiConfig(sigma, cutoff, 0, W, H)
+    e2e_ms = None
+    if args.e2e_steps > 0:
+        pinned = [pos.cpu().pin_memory(), col.cpu().pin_memory(), up.cpu().pin_memory(),
+                  torch.empty(B, H, W, C).pin_memory(), torch.empty(B, N, C).pin_memory(),
+                  torch.empty(B, N, 2).pin_memory()]
+        hpos, hcol, hup, himg, hdc, hdp = (t.numpy() for t in pinned)
+        import ctypes as Cty
+        fp = Cty.POINTER(Cty.c_float)
+        cfg_c = gmi._lib.GmiConfig(sigma, cutoff, 0, W, H)
 
-    def e2e_step():
-        h = Cty.c_void_p()
-        gmi._check(gmi.lib.gmi_forward_host(ctx.handle, hpos.ctypes.data_as(fp), hcol.ctypes.data_as(fp),
-                                            B, N, C, Cty.byref(cfg_c), himg.ctypes.data_as(fp), Cty.byref(h)))
-        gmi._check(gmi.lib.gmi_backward_host(ctx.handle, hpos.ctypes.data_as(fp), hcol.ctypes.data_as(fp),
-                                             B, N, C, Cty.byref(cfg_c), h, hup.ctypes.data_as(fp),
-                                             hdc.ctypes.data_as(fp), hdp.ctypes.data_as(fp)))
-        gmi.lib.gmi_cache_free(h)
+        def e2e_step():
+            h = Cty.c_void_p()
+            gmi._check(gmi.lib.gmi_forward_host(ctx.handle, hpos.ctypes.data_as(fp), hcol.ctypes.data_as(fp),
+                                                B, N, C, Cty.byref(cfg_c), himg.ctypes.data_as(fp), Cty.byref(h)))
+            if not fwd_only:
+                gmi._check(gmi.lib.gmi_backward_host(ctx.handle, hpos.ctypes.data_as(fp),
+                                                     hcol.ctypes.data_as(fp), B, N, C, Cty.byref(cfg_c), h,
+                                                     hup.ctypes.data_as(fp), hdc.ctypes.data_as(fp),
+                                                     hdp.ctypes.data_as(fp)))
+            gmi.lib.gmi_cache_free(h)
 
-    e2e_step()
-    barrier()
-    torch.cuda.synchronize(dev)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.e2e_steps):
         e2e_step()
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = world * B * W * H / (e2e_ms * 1e-3) / 1e6
-    h2d = B * N * 4 * (2 + C) * 2 + B * H * W * C * 4
-    d2h = B * H * W * C * 4 + B * N * 4 * (C + 2)
+        barrier()
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e_value = world * B * W * H / (e2e_ms * 1e-3) / 1e6
+    # forward_host uploads positions+colours and downloads the image;
+    # backward_host uploads upstream and downloads both gradients
+    h2d = B * N * 4 * (2 + C) + (0 if fwd_only else B * H * W * C * 4)
+    d2h = B * H * W * C * 4 + (0 if fwd_only else B * N * 4 * (C + 2))
 
     if rank != 0:
         return
     line = {
-        "metric": METRIC, "value": round(value, 2), "unit": "Mpix/s", "n_gpus": world,
+        "metric": METRIC if args.config == 3 else METRIC.replace("1024^2, N=262k pts, C=3", cfg["workload"]),
+        "value": round(value, 2), "unit": "Mpix/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD, "batch_per_gpu": B, "global_batch": world * B,
+        "config": {"workload": cfg["workload"], "batch_per_gpu": B, "global_batch": world * B,
                    "points": N, "channels": C, "frame": [H, W], "sigma": sigma,
                    "cutoff": cutoff, "pairs_per_image": P_img,
                    "l2": "inputs > L2 (126 MB): no flush needed",
@@ -370,12 +399,12 @@ def main():
                           "frac": round(fp32_ach / fp32_peak, 4),
                           "step_frac": round(step_fp32_frac, 4),
                           "counts": "fwd 6+C, bwd 11+2C FP32 instr per (pixel,point) pair (SURVEY §8d)"},
-        "e2e": {"value": round(e2e_value, 2), "unit": "Mpix/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3)},
+        "e2e": ({"value": round(e2e_value, 2), "unit": "Mpix/s", "h2d_bytes_per_step": h2d,
+                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3)} if e2e_ms else None),
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and args.config == 3:
         v, imgs, threads, secs, kind = cpu_reference_sample(cfg, args.cpu_seconds, 64)
         line["cpu_baseline"] = {"value": round(v, 4), "unit": "Mpix/s", "cores": threads,
                                 "kind": kind,

@@ -84,6 +84,9 @@ k_gather(GatherParams p) {
     SmemGather<CC>& S = *reinterpret_cast<SmemGather<CC>*>(smem_raw);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // channel group of this CTA (C > 4: grid.z groups, weights recomputed per
+    // group; group 0 owns W, counts and the fallback list)
+    const int ch0 = blockIdx.z * CC, nch = min(CC, p.C - ch0);
     const int tiles_y = (p.H + kTH - 1) / kTH;
     const int b = blockIdx.y / tiles_y;
     const int y0 = (blockIdx.y % tiles_y) * kTH;
@@ -282,7 +285,8 @@ k_gather(GatherParams p) {
                 float c[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int ch = 0; ch < CC; ++ch)
-                    c[ch] = p.scol[(static_cast<size_t>(b) * p.C + ch) * p.N + gs + j];
+                    if (ch < nch)
+                        c[ch] = p.scol[(static_cast<size_t>(b) * p.C + ch0 + ch) * p.N + gs + j];
                 S.A[dst] = make_float4(mx, my, c[0], c[1]);
                 if (CC > 2) S.Bc[dst] = f2(c[2], c[3]);
                 const uint8_t fl = static_cast<uint8_t>(static_cast<uint32_t>(p.sidx[slot]) >> 31);
@@ -428,18 +432,21 @@ k_gather(GatherParams p) {
             if (qx >= p.W || qy >= p.H) continue;
             const float w = py ? (px ? Wb.y : Wb.x) : (px ? Wa.y : Wa.x);
             const size_t bp = (static_cast<size_t>(b) * p.H + qy) * p.W + qx;
-            float* out = p.image + bp * p.C;
+            float* out = p.image + bp * p.C + ch0;
             if (w > 0.f) {
                 const float inv = 1.0f / w;
 #pragma unroll
                 for (int c = 0; c < CC; ++c) {
+                    if (c >= nch) continue;
                     const float num = py ? (px ? Nb[c].y : Nb[c].x) : (px ? Na[c].y : Na[c].x);
                     const float q0 = num * inv;
                     out[c] = fmaf(fmaf(-q0, w, num), inv, q0);
                 }
-                p.wsum[bp] = w;
-                if (kCount) p.counts[bp] = py ? (px ? cnt11 : cnt10) : (px ? cnt01 : cnt00);
-            } else {
+                if (blockIdx.z == 0) {
+                    p.wsum[bp] = w;
+                    if (kCount) p.counts[bp] = py ? (px ? cnt11 : cnt10) : (px ? cnt01 : cnt00);
+                }
+            } else if (blockIdx.z == 0) {
                 // empty neighbourhood: fallback pixel (K3)
                 p.wsum[bp] = 0.f;
                 if (kCount) p.counts[bp] = 0;
@@ -468,7 +475,7 @@ namespace gmi_host {
 // (f64 weight mode, C > 4, or a radius whose fine-column window exceeds the
 // staging tables).
 bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts) {
-    if (c->wsum64 != nullptr || c->C > 4) return false;
+    if (c->wsum64 != nullptr) return false;
     const double need_cols = 2.0 * (kTW - 1 + 2.0 * c->cutoff + 0.05) + 4.0;
     if (need_cols > kNqMax) return false;
     GatherParams p{};
@@ -493,10 +500,11 @@ bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* count
     p.special = c->special;
     p.special_count = c->special_count_d;
     p.special_cap = c->special_cap;
-    const dim3 grid((c->W + kTW - 1) / kTW, ((c->H + kTH - 1) / kTH) * c->B);
+    const int cc = c->C <= 4 ? c->C : 4;
+    const dim3 grid((c->W + kTW - 1) / kTW, ((c->H + kTH - 1) / kTH) * c->B, (c->C + cc - 1) / cc);
     GMI_CUDA(cudaMemsetAsync(c->special_count_d, 0, sizeof(int32_t), ctx->stream));
     const bool cnt = counts != nullptr;
-    switch (c->C) {
+    switch (cc) {
         case 1: cnt ? launch_cc<1, true>(ctx, p, grid) : launch_cc<1, false>(ctx, p, grid); break;
         case 2: cnt ? launch_cc<2, true>(ctx, p, grid) : launch_cc<2, false>(ctx, p, grid); break;
         case 3: cnt ? launch_cc<3, true>(ctx, p, grid) : launch_cc<3, false>(ctx, p, grid); break;
