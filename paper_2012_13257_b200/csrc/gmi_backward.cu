@@ -2,22 +2,19 @@
 //
 // Point-major and atomic-free.  A CTA takes a block of reference cells and
 // stages, for every pixel those points can reach,
-//     u_c = upstream_c / W      and      out_c
-// (both 0 on fallback pixels) in shared memory as interleaved PIXEL PAIRS
-// (x even, x+1) so that two pixels are processed per f32x2 instruction
-// (FFMA2 / FMUL2 / FADD2, sm_100).  Every thread owns whole points and walks
-// the point's exact disk row by row — the reference's closed ball d^2 <= r^2
-// (bin_grid.cpp:98; exact spans from one fp32 sqrt per row, or the f64
-// predicate for points K1 flagged as boundary-ambiguous) — recomputing the
-// Gaussian weight instead of storing it: two exp2 on the SFU start a row, then
-// the weights advance by the exact recurrence w(x+2) = w(x) * R(x),
-// R(x+2) = R(x) * 2^(8 nk), i.e. two FMUL2 per pixel pair.  Per pair it
-// accumulates in registers
-//     d_col_c += w * u_c                              (= up_c w/W, engine.cpp:222)
-//     d_pos   += w * sum_c u_c (c_ic - out_c) * (q - mu) / sigma^2
-//                              (= ratio * dot / sigma^2 * (q-mu), engine.cpp:219-230)
-// — c_ic - out_c is formed before weighting, exactly (Sterbenz), which keeps
-// d_positions accurate where the reference's value is a cancellation to ~0 —
+//     u_c = upstream_c / W      and      -v = -sum_c u_c out_c
+// (zeros on fallback pixels) in shared memory as interleaved PIXEL PAIRS
+// (x even, x+1): (CG + 1) float2 = 16 bytes per pixel for C = 3, so two
+// pixels are processed per f32x2 instruction (FFMA2 / FMUL2 / FADD2, sm_100).
+// Every thread owns whole points and walks the point's exact disk row by row
+// — the reference's closed ball d^2 <= r^2 (bin_grid.cpp:98; exact spans from
+// one fp32 reciprocal-sqrt per row, or the f64 predicate for points K1
+// flagged as boundary-ambiguous) — recomputing the Gaussian weight with the
+// forward's own fp32 operations (bit-identical to the weight summed into W)
+// instead of storing it.  Per pair it accumulates in registers
+//     d_col_c += w * u_c                         (= up_c w/W, engine.cpp:222)
+//     d_pos   += w * (sum_c c_ic u_c - v) * (q - mu) / sigma^2
+//                                     (= ratio * dot / sigma^2 * (q-mu), engine.cpp:219-230)
 // and writes each point's gradients once.  One owner per point: the result
 // is bit-deterministic with no atomics and no reduction pass.
 //
@@ -34,7 +31,8 @@ using namespace gmi_dev;
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kSmemBudget = 96 * 1024;  // staged pixel bytes per CTA (2 CTAs/SM)
+constexpr int kSmemBudget = 52 * 1024;  // staged pixel bytes per CTA (4 CTAs/SM)
+constexpr int kRunMax = 64;             // cell rows per block
 
 struct BwdParams {
     const Geom* geom;
@@ -51,9 +49,7 @@ struct BwdParams {
     int bs;                 // cells per block side
     double r64, r2_64;
     float nk;               // -log2(e) / (2 sigma^2)
-    float q8;               // 2^(8 nk): R(x+2)/R(x)
     float inv_s2;
-    int use_rec;            // exp2 recurrence safe (no over/underflow of R)
     float* d_col;           // [B][N][C]
     float* d_pos;           // [B][N][2] or partial [G][B][N][2]
 };
@@ -65,12 +61,45 @@ __device__ __forceinline__ bool in_ref(int x, int y, float mx, float my, double 
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
+// float4 slots per staged pixel pair: CG u-pairs + the (-v) pair, as float2
 template <int CG>
-__global__ void __launch_bounds__(kThreads, 2)
+struct PairLayout {
+    static constexpr int kF2 = CG + 1;
+    static constexpr int kF4 = (kF2 + 1) / 2;
+};
+
+// Per-pixel terms of the backward (engine.cpp:213-231), for this channel
+// group:  u_c = up_c / W  and  v = sum_c u_c * out_c, so that per pair
+//     ratio * up_c = w * u_c,   ratio * dot = w * (sum_c c_ic u_c - v).
+// Fallback pixels (W == 0) and off-frame pixels stage zeros (K5 routes the
+// fallback upstream).
+template <int CG>
+__device__ __forceinline__ void pixel_terms(const BwdParams& p, size_t img_base, int ch0, int nch,
+                                            int x, int y, float* u, float& v) {
+#pragma unroll
+    for (int c = 0; c < CG; ++c) u[c] = 0.f;
+    v = 0.f;
+    if (x < 0 || x >= p.W || y < 0 || y >= p.H) return;
+    const size_t pix = img_base + static_cast<size_t>(y) * p.W + x;
+    const float wv = p.wsum[pix];
+    if (!(wv > 0.f)) return;
+    const float inv = 1.0f / wv;
+#pragma unroll
+    for (int c = 0; c < CG; ++c) {
+        if (c < nch) {
+            u[c] = p.upstream[pix * p.C + ch0 + c] * inv;
+            v = fmaf(u[c], p.image[pix * p.C + ch0 + c], v);
+        }
+    }
+}
+
+template <int CG>
+__global__ void __launch_bounds__(kThreads, 4)
 k_backward_points(BwdParams p) {
-    // [rows][pairs][CG] float4: (u0a,u0b,u1a,u1b, ..., o0a,o0b, ...) as 2*CG float2
-    extern __shared__ float4 s_pair[];
-    __shared__ int s_run[66];
+    using L = PairLayout<CG>;
+    extern __shared__ float4 s_pair[];   // [rows][pairs][L::kF4]
+    __shared__ int s_run[kRunMax + 1];   // prefix of the block's cell-row runs
+    __shared__ int s_rung[kRunMax];      // first slot of each run
     __shared__ float s_red[4][kThreads / 32];
     __shared__ int s_region[5];
     __shared__ int s_next;
@@ -92,27 +121,30 @@ k_backward_points(BwdParams p) {
     const int cx0 = (local % nbx) * p.bs, cy0 = (local / nbx) * p.bs;
     const int cx1 = min(cx0 + p.bs, g.n_cols), cy1 = min(cy0 + p.bs, g.n_rows);
     const int cg = blockIdx.y, ch0 = cg * CG, nch = min(CG, p.C - ch0);
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31;
     const size_t base = static_cast<size_t>(b) * p.N;
 
     // ---- point runs (one per cell row of the block) ----
     const int nrun = cy1 - cy0;
     if (tid < 32) {
-        // run lengths loaded by one lane each, prefix-summed with shuffles
         int carry = 0;
         for (int k0 = 0; k0 < nrun; k0 += 32) {
             const int k = k0 + tid;
-            int len = 0;
+            int len = 0, gs = 0;
             if (k < nrun) {
                 const int64_t r0 = g.bin_off + static_cast<int64_t>(cy0 + k) * g.n_cols;
-                len = p.bins[r0 + cx1] - p.bins[r0 + cx0];
+                gs = p.bins[r0 + cx0];
+                len = p.bins[r0 + cx1] - gs;
             }
             int incl = len;
             for (int o = 1; o < 32; o <<= 1) {
                 const int t = __shfl_up_sync(0xffffffffu, incl, o);
                 if (tid >= o) incl += t;
             }
-            if (k < nrun) s_run[k] = carry + incl - len;
+            if (k < nrun) {
+                s_run[k] = carry + incl - len;
+                s_rung[k] = gs;
+            }
             carry += __shfl_sync(0xffffffffu, incl, 31);
         }
         if (tid == 0) s_run[nrun] = carry;
@@ -120,11 +152,15 @@ k_backward_points(BwdParams p) {
     __syncthreads();
     const int total = s_run[nrun];
     if (total == 0) return;
+    // k-th point of the block -> slot (binary search over the runs)
     auto slot_of = [&](int k) -> int {
-        int r = 0;
-        while (s_run[r + 1] <= k) ++r;
-        const int64_t r0 = g.bin_off + static_cast<int64_t>(cy0 + r) * g.n_cols;
-        return p.bins[r0 + cx0] + (k - s_run[r]);
+        int lo = 0, hi = nrun;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_run[mid] <= k) lo = mid;
+            else hi = mid;
+        }
+        return s_rung[lo] + (k - s_run[lo]);
     };
 
     // ---- pixel region reached by the block's points (bbox + r) ----
@@ -143,7 +179,7 @@ k_backward_points(BwdParams p) {
         mxx = fmaxf(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
         mxy = fmaxf(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
     }
-    if ((tid & 31) == 0) {
+    if (lane == 0) {
         s_red[0][tid >> 5] = mnx;
         s_red[1][tid >> 5] = mny;
         s_red[2][tid >> 5] = mxx;
@@ -158,10 +194,10 @@ k_backward_points(BwdParams p) {
             mxy = fmaxf(mxy, s_red[3][w]);
         }
         const float rr = static_cast<float>(p.r64) + 2.0f;
-        int x0 = max(0, static_cast<int>(floorf(mnx - rr)));
-        const int y0 = max(0, static_cast<int>(floorf(mny - rr)));
-        int x1 = min(p.W - 1, static_cast<int>(ceilf(mxx + rr)));
-        const int y1 = min(p.H - 1, static_cast<int>(ceilf(mxy + rr)));
+        int x0 = max(0, static_cast<int>(floorf(fmaxf(mnx - rr, -1.0e9f))));
+        const int y0 = max(0, static_cast<int>(floorf(fmaxf(mny - rr, -1.0e9f))));
+        int x1 = min(p.W - 1, static_cast<int>(ceilf(fminf(mxx + rr, 1.0e9f))));
+        const int y1 = min(p.H - 1, static_cast<int>(ceilf(fminf(mxy + rr, 1.0e9f))));
         x0 &= ~1;        // pairs start at even x
         x1 |= 1;         // and end at odd x (may exceed the frame: zero-staged)
         s_region[0] = x0;
@@ -171,7 +207,7 @@ k_backward_points(BwdParams p) {
         const long npairs = (x1 >= x0) ? (x1 - x0 + 1) / 2 : 0;
         const long area = (y1 >= y0) ? npairs * (y1 - y0 + 1) : 0;
         s_region[4] = (mnx <= mxx && area > 0 &&
-                       area * CG * static_cast<long>(sizeof(float4)) <= kSmemBudget)
+                       area * L::kF4 * static_cast<long>(sizeof(float4)) <= kSmemBudget)
                           ? 1
                           : (area > 0 ? 0 : -1);
     }
@@ -193,37 +229,16 @@ k_backward_points(BwdParams p) {
     const int npairs = (rx1 - rx0 + 1) / 2;
     const size_t img_base = static_cast<size_t>(b) * p.H * p.W;
 
-    // (u_c, out_c) of one pixel for this channel group; zero off-frame and on
-    // fallback pixels (W == 0: engine.cpp:200-211 handles them in K5).
-    auto pixel_q = [&](int x, int y, float* u, float* o) {
-#pragma unroll
-        for (int c = 0; c < CG; ++c) {
-            u[c] = 0.f;
-            o[c] = 0.f;
-        }
-        if (x < 0 || x >= p.W || y < 0 || y >= p.H) return;
-        const size_t pix = img_base + static_cast<size_t>(y) * p.W + x;
-        const float wv = p.wsum[pix];
-        if (wv > 0.f) {
-            const float inv = 1.0f / wv;
-#pragma unroll
-            for (int c = 0; c < CG; ++c) {
-                if (c < nch) {
-                    u[c] = p.upstream[pix * p.C + ch0 + c] * inv;
-                    o[c] = p.image[pix * p.C + ch0 + c];
-                }
-            }
-        }
-    };
     if (staged) {
         const int area = npairs * (ry1 - ry0 + 1);
         // 8-byte alignment of a pixel pair in W / upstream / image rows
         const bool vec = (p.W % 2 == 0) && (CG == p.C);
         for (int k = tid; k < area; k += kThreads) {
-            const int pp = k % npairs, yy = ry0 + k / npairs;
+            const int row = k / npairs;
+            const int pp = k - row * npairs, yy = ry0 + row;
             const int xa = rx0 + 2 * pp;
-            float ua[CG], oa[CG], ub[CG], ob[CG];
-            if (vec && xa + 1 < p.W) {
+            float ua[CG], ub[CG], va = 0.f, vb = 0.f;
+            if (vec && xa >= 0 && xa + 1 < p.W && yy < p.H) {
                 // both pixels in the frame: 64-bit loads of the pair
                 const size_t pix = img_base + static_cast<size_t>(yy) * p.W + xa;
                 const float2 wv = *reinterpret_cast<const float2*>(p.wsum + pix);
@@ -243,20 +258,24 @@ k_backward_points(BwdParams p) {
 #pragma unroll
                 for (int c = 0; c < CG; ++c) {
                     ua[c] = upv[c] * ia;
-                    oa[c] = wv.x > 0.f ? imv[c] : 0.f;
                     ub[c] = upv[CG + c] * ib;
-                    ob[c] = wv.y > 0.f ? imv[CG + c] : 0.f;
+                    va = fmaf(ua[c], imv[c], va);
+                    vb = fmaf(ub[c], imv[CG + c], vb);
                 }
             } else {
-                pixel_q(xa, yy, ua, oa);
-                pixel_q(xa + 1, yy, ub, ob);
+                pixel_terms<CG>(p, img_base, ch0, nch, xa, yy, ua, va);
+                pixel_terms<CG>(p, img_base, ch0, nch, xa + 1, yy, ub, vb);
             }
-            float2* dst = reinterpret_cast<float2*>(s_pair + static_cast<size_t>(k) * CG);
+            float2 e[2 * L::kF4];
 #pragma unroll
-            for (int c = 0; c < CG; ++c) {
-                dst[c] = f2(ua[c], ub[c]);
-                dst[CG + c] = f2(oa[c], ob[c]);
-            }
+            for (int c = 0; c < CG; ++c) e[c] = f2(ua[c], ub[c]);
+            e[CG] = f2(-va, -vb);
+#pragma unroll
+            for (int c = CG + 1; c < 2 * L::kF4; ++c) e[c] = f2(0.f, 0.f);
+            float4* dst = s_pair + static_cast<size_t>(k) * L::kF4;
+#pragma unroll
+            for (int j = 0; j < L::kF4; ++j)
+                dst[j] = make_float4(e[2 * j].x, e[2 * j].y, e[2 * j + 1].x, e[2 * j + 1].y);
         }
         __syncthreads();
     }
@@ -269,7 +288,6 @@ k_backward_points(BwdParams p) {
     const float2 nk2 = f2(nk, nk), two = f2(2.f, 2.f);
     // dynamic warp tasks of 32 consecutive points (bin order keeps a warp's
     // points adjacent): balances the CTA's warps without idle tails
-    const int lane = tid & 31;
     if (tid == 0) s_next = 0;
     __syncthreads();
     while (true) {
@@ -285,12 +303,9 @@ k_backward_points(BwdParams p) {
         const int i = static_cast<int>(raw & 0x7fffffffu);
         const bool unsafe = (raw & kUnsafeBit) != 0;
         float cc[CG];
-        float2 cc2[CG];
 #pragma unroll
-        for (int c = 0; c < CG; ++c) {
+        for (int c = 0; c < CG; ++c)
             cc[c] = c < nch ? p.scol[(static_cast<size_t>(b) * p.C + ch0 + c) * p.N + s] : 0.f;
-            cc2[c] = f2(cc[c], cc[c]);
-        }
         float2 dcol[CG];
 #pragma unroll
         for (int c = 0; c < CG; ++c) dcol[c] = f2(0.f, 0.f);
@@ -315,7 +330,8 @@ k_backward_points(BwdParams p) {
                 dy = static_cast<float>(y - by) - fmy;
                 const float h2f = fmaf(-dy, dy, r2f);
                 if (h2f < 0.f) continue;
-                const float sq = sqrtf(h2f);
+                // ~2 ulp: a safe point's row ends are >= 8e-6 r^2 from the ball
+                const float sq = h2f * rsqrtf(fmaxf(h2f, 1e-30f));
                 xl = bx + static_cast<int>(ceilf(fmu - sq));
                 xr = bx + static_cast<int>(floorf(fmu + sq));
             } else {
@@ -336,17 +352,19 @@ k_backward_points(BwdParams p) {
             xl = max(xl, xmin);
             xr = min(xr, xmax);
             if (xl > xr) continue;
-            const float dy2 = dy * dy;
+            // e = nk dx^2 + nk dy^2 with the forward's fp32 operations, so a
+            // pair's weight is bit-identical to the one summed into W
+            const float ey = (dy * nk) * dy;
             if (!staged) {
                 float gyr = 0.f;
                 for (int x = xl; x <= xr; ++x) {
-                    const float dx = static_cast<float>(x - bx) - fmu;
-                    const float w = ex2(fmaf(dx, dx, dy2) * nk);
-                    float u[CG], o[CG];
-                    pixel_q(x, y, u, o);
-                    float t = 0.f;
+                    const float dx = static_cast<float>(x) - mx;
+                    const float w = ex2(fmaf(dx * nk, dx, ey));
+                    float u[CG], v;
+                    pixel_terms<CG>(p, img_base, ch0, nch, x, y, u, v);
+                    float t = -v;
 #pragma unroll
-                    for (int c = 0; c < CG; ++c) t = fmaf(u[c], cc[c] - o[c], t);
+                    for (int c = 0; c < CG; ++c) t = fmaf(u[c], cc[c], t);
                     const float a = w * t;
 #pragma unroll
                     for (int c = 0; c < CG; ++c) dcol[c].x = fmaf(w, u[c], dcol[c].x);
@@ -362,32 +380,31 @@ k_backward_points(BwdParams p) {
             const int np = ((xr - xs) >> 1) + 1;
             const float mf = ((xl - rx0) & 1) ? 0.f : 1.f;
             const float ml = ((xr - rx0) & 1) ? 1.f : 0.f;
-            float2 dx = f2(static_cast<float>(xs - bx) - fmu, 0.f);
-            dx.y = dx.x + 1.0f;
-            const float2 dy22 = f2(dy2, dy2);
+            float2 X = f2(static_cast<float>(xs), static_cast<float>(xs + 1));
+            const float2 ey2 = f2(ey, ey), mmx = f2(-mx, -mx);
             float2 gyr2 = f2(0.f, 0.f);
-            const float4* pr = s_pair + (static_cast<size_t>(y - ry0) * npairs + ((xs - rx0) >> 1)) * CG;
+            const float4* pr = s_pair + (static_cast<size_t>(y - ry0) * npairs + ((xs - rx0) >> 1)) * L::kF4;
             for (int j = 0; j < np; ++j) {
-                float4 v[CG];
+                float4 q4[L::kF4];
 #pragma unroll
-                for (int c = 0; c < CG; ++c) v[c] = pr[c];
-                const float2 arg = __fmul2_rn(__ffma2_rn(dx, dx, dy22), nk2);
+                for (int c = 0; c < L::kF4; ++c) q4[c] = pr[c];
+                const float2* q = reinterpret_cast<const float2*>(q4);
+                const float2 dx = __fadd2_rn(X, mmx);
+                const float2 arg = __ffma2_rn(__fmul2_rn(dx, nk2), dx, ey2);
                 float2 w = f2(ex2(arg.x), ex2(arg.y));
                 if (j == 0) w.x *= mf;
                 if (j == np - 1) w.y *= ml;
-                const float2* q = reinterpret_cast<const float2*>(v);
-                // t = sum_c u_c (c_ic - out_c)
-                float2 t = __fmul2_rn(q[0], __fadd2_rn(cc2[0], f2(-q[CG].x, -q[CG].y)));
+                // t = sum_c c_ic u_c - v  (= dot / W, engine.cpp:219-221)
+                float2 t = q[CG];
 #pragma unroll
-                for (int c = 1; c < CG; ++c)
-                    t = __ffma2_rn(q[c], __fadd2_rn(cc2[c], f2(-q[CG + c].x, -q[CG + c].y)), t);
+                for (int c = 0; c < CG; ++c) t = __ffma2_rn(q[c], f2(cc[c], cc[c]), t);
                 const float2 a = __fmul2_rn(w, t);
 #pragma unroll
                 for (int c = 0; c < CG; ++c) dcol[c] = __ffma2_rn(w, q[c], dcol[c]);
                 gx2 = __ffma2_rn(a, dx, gx2);
                 gyr2 = __fadd2_rn(gyr2, a);
-                dx = __fadd2_rn(dx, two);
-                pr += CG;
+                X = __fadd2_rn(X, two);
+                pr += L::kF4;
             }
             gy = fmaf(gyr2.x + gyr2.y, dy, gy);
         }
@@ -489,6 +506,9 @@ __global__ void k_special_backward(SpecBwdParams p) {
     }
 }
 
+// float4 slots of one staged pixel pair (PairLayout<CG>::kF4)
+inline int pair_f4(int cg) { return (cg + 2) / 2; }
+
 template <int CG>
 void launch_points(gmi_ctx* ctx, const BwdParams& p, int nblocks, int groups) {
     const int smem = kSmemBudget;
@@ -509,9 +529,10 @@ void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
     const int groups = (c->C + CG - 1) / CG;
     // cells per block side so that the staged pixel pairs fit the budget
     const double cell = c->cutoff;
-    const double side_px = std::sqrt(static_cast<double>(kSmemBudget) / (8.0 * CG));
+    const double pix_bytes = 8.0 * pair_f4(CG);  // staged bytes per pixel
+    const double side_px = std::sqrt(static_cast<double>(kSmemBudget) / pix_bytes);
     int bs = static_cast<int>(std::floor((side_px - 2.0 * cell - 8.0) / cell));
-    bs = std::max(1, std::min(bs, 64));
+    bs = std::max(1, std::min(bs, kRunMax));
     std::vector<int32_t> off(c->B + 1, 0);
     for (int b = 0; b < c->B; ++b) {
         const auto& g = c->geom_h[b];
@@ -542,15 +563,6 @@ void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
     p.r2_64 = c->cutoff * c->cutoff;
     const double nk = -1.4426950408889634 / (2.0 * c->sigma * c->sigma);
     p.nk = static_cast<float>(nk);
-    p.q8 = static_cast<float>(std::exp2(8.0 * nk));
-    // The exp2 recurrence (w *= R, R *= 2^(8 nk)) saves two SFU ops per pair
-    // but its rounding error grows with the span (~3 ulp per step); with
-    // sparse inputs d_colors is a cancellation of O(1) terms and the
-    // accumulated error reaches the 1e-6 absolute budget.  Direct exp2 per
-    // pixel keeps every weight within 2 ulp, so it is the default; the
-    // recurrence stays available (GMI_BWD_RECURRENCE=1) for dense inputs.
-    const bool rec_ok = std::fabs(nk) * (4.0 * c->cutoff + 12.0) < 60.0;
-    p.use_rec = (rec_ok && std::getenv("GMI_BWD_RECURRENCE") != nullptr) ? 1 : 0;
     p.inv_s2 = static_cast<float>(1.0 / (c->sigma * c->sigma));
     p.d_col = d_colors;
     const size_t n2 = static_cast<size_t>(c->B) * c->N * 2;

@@ -127,7 +127,9 @@ k_forward_tile(FwdParams p) {
                             static_cast<double>(mx), static_cast<double>(my)) <= p.r2_64;
             }
             if (in) {
-                const float w = ex2(d2 * p.nk);
+                // e = nk dx^2 + nk dy^2, the same fp32 operations as the
+                // fast gather and the backward (bit-identical weights)
+                const float w = ex2(fmaf(dx * p.nk, dx, (dy * p.nk) * dy));
                 wsum += w;
 #pragma unroll
                 for (int c = 0; c < kCG; ++c) num[c] = fmaf(w, s_c[c][k], num[c]);

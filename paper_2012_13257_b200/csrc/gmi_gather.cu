@@ -7,23 +7,27 @@
 // whose normaliser W and numerators live in f32x2 registers.
 //
 //  stage  The candidate points of the tile (reference cells overlapping the
-//         tile grown by r) come from the bin-ordered SoA.  Inside a cell row
-//         the SoA is sorted by fine x-column (K1), so each cell row is an
-//         x-sorted run.  The runs are merged COLUMN-MAJOR into shared memory
-//         — position = column start + earlier rows in that column + rank —
-//         with deterministic ranks (__match_any_sync), no sort and no atomics.
-//  band   Each warp compacts (ballot) the candidates of its row pair's band
-//         |y - mu_y| <= r into an x-sorted index list.
-//  window Each lane's candidates are then ONE contiguous range of that list:
-//         mu_x in [x - r, x + 1 + r], found from the column starts and the
-//         warp's ballot words — no per-lane search.
-//  gather Per candidate, 4 pixels with f32x2 ops: d^2, in-ball test (fp32 is
-//         exact for points K1 did not flag, see gmi_common.cuh), 4 MUFU.EX2,
-//         W and C numerators.  Flagged (boundary-ambiguous) points take the f64
-//         predicate in a separate warp-uniform pass.
+//         tile grown by r, one run per cell row) are counting-sorted in shared
+//         memory by (1-px column, row-pair) bin.  Bin geometry is exact (f64
+//         differences of fp32 positions against integer / f64 anchors), so a
+//         point that can reach the tile lands in the bins its pixels read.
+//         Within a bin the order is canonicalised by original index, so the
+//         summation order — and the result — is independent of K1's atomic
+//         arrival order.
+//  lists  Warp w needs the row-pair bins [w, w + dyb] of every column: per
+//         column one contiguous piece of the sorted array.  Lane-per-column
+//         prefix sums give the warp's column-major index list and its column
+//         starts; a lane's candidates (mu_x in (xa - r, xa + 1 + r)) are then
+//         ONE contiguous range of that list.
+//  gather Per candidate, 4 pixels with f32x2 ops: e = nk d^2 (7 FP2), in-ball
+//         test e >= nk r^2 (exact in fp32 for points K1 did not flag, see
+//         gmi_common.cuh), 4 MUFU.EX2, W and C numerators.  Flagged
+//         (boundary-ambiguous) points sit in one extra bin and take the f64
+//         predicate in a warp-uniform pass.
 //  store  out = num/W with one Newton step, W kept for the backward; pixels
 //         with W == 0 go to the fallback list (K3).
 #include <algorithm>
+#include <cmath>
 
 #include "gmi_internal.cuh"
 
@@ -36,25 +40,28 @@ constexpr int kNW = kTH / 2;       // warps (row pairs)
 constexpr int kNT = kNW * 32;      // threads
 constexpr int kCap = 1024;         // staged candidates per chunk
 constexpr int kRsMax = 32;         // cell-row runs per chunk
-constexpr int kNqMax = 256;        // fine x-columns across the tile's region
-constexpr int kChunks = kCap / 32;
+constexpr int kColMax = 128;       // 1-px columns across the tile's reach
+constexpr int kBinMax = 2048;      // (column, row-pair) bins (+1 flag bin)
 
 template <int CC>
 struct SmemGather {
-    float4 A[kCap];                        // mu_x, mu_y, c0, c1
+    float4 A[kCap];                        // mu_x, mu_y, c0, c1   (bin order)
     float2 Bc[CC > 2 ? kCap : 1];          // c2, c3
-    uint8_t flag[kCap];                    // boundary-ambiguous point
-    uint16_t cnt[kRsMax][kNqMax];          // per (run, column) count -> offset
-    int colstart[kNqMax + 1];
-    uint16_t srank[kCap];
-    uint16_t list[kNW][kCap];
-    uint32_t bal[kNW][kChunks + 1];
-    uint16_t balpre[kNW][kChunks + 1];
+    int idx[kCap];                         // original index (+ flag bit)
+    union {
+        struct {
+            int key[kCap];                 // bin of staged candidate k (-1: dropped)
+            int slot[kCap];                // its slot in the image's SoA
+        } st;
+        uint16_t wl[kNW][kCap];            // per-warp column-major lists
+    } u;
+    int bin[kBinMax + 2];                  // counts -> inclusive ends -> starts
+    uint16_t wcs[kNW][kColMax + 1];        // per-warp column starts in wl
     int run_beg[kRsMax + 1];
     int run_g[kRsMax];
-    int scan_w[kNT / 32];
-    int n_runs, cur_cy, cur_off, done, any_flag;
-    int cx0, cx1, cy1, pre;
+    int scan_w[kNW];
+    int n_runs, cur_cy, cur_off, done, pre;
+    int cx0, cx1, cy1;
 };
 
 struct GatherParams {
@@ -65,8 +72,9 @@ struct GatherParams {
     const int32_t* sidx;
     const float* scol;  // [B][C][N]
     int N, C, W, H;
+    int ncol, nyb, dyb, rc;   // bin geometry (see launch_gather_fast)
     double r64, r2_64;
-    float rf, r2f, nk;
+    float r2f, nk, thr;
     float* image;
     float* wsum;
     int32_t* counts;
@@ -78,7 +86,7 @@ struct GatherParams {
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
 template <int CC, bool kCount>
-__global__ void __launch_bounds__(kNT)
+__global__ void __launch_bounds__(kNT, 3)
 k_gather(GatherParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SmemGather<CC>& S = *reinterpret_cast<SmemGather<CC>*>(smem_raw);
@@ -93,26 +101,23 @@ k_gather(GatherParams p) {
     const int x0 = blockIdx.x * kTW;
     const Geom g = p.geom[b];
     const size_t base = static_cast<size_t>(b) * p.N;
-    const unsigned lt = (1u << lane) - 1u;
+    const int ncol = p.ncol, nyb = p.nyb, nbins = ncol * nyb;
+    // bin anchors: column = floor(mu_x - cxo), row pair = floor((mu_y - cyo)/2)
+    const double cxo = static_cast<double>(x0 - p.rc);
+    const double cyo = static_cast<double>(y0) - p.r64;
 
     // tile region and its reference cells (bin_grid.cpp:88-91 for the tile)
     const double xlo = static_cast<double>(x0) - p.r64;
     const double xhi = static_cast<double>(x0 + kTW - 1) + p.r64;
     const double ylo = static_cast<double>(y0) - p.r64;
     const double yhi = static_cast<double>(y0 + kTH - 1) + p.r64;
-    // fp32 region bounds, padded outward (monotone filters stay supersets)
-    const float epsx = 2e-3f + 1e-6f * fabsf(static_cast<float>(xhi));
-    const float epsy = 2e-3f + 1e-6f * fabsf(static_cast<float>(yhi));
-    const float fxlo = static_cast<float>(xlo) - epsx, fxhi = static_cast<float>(xhi) + epsx;
-    const float fylo = static_cast<float>(ylo) - epsy, fyhi = static_cast<float>(yhi) + epsy;
-    const int q_lo = fine_col(fxlo, g.qx0, g.qscale);
-    const int nq = min(kNqMax, fine_col(fxhi, g.qx0, g.qscale) - q_lo + 1);
 
     // this thread's 2x2 pixels
     const int ya = y0 + 2 * warp, xa = x0 + 2 * lane;
     const float2 X = f2(static_cast<float>(xa), static_cast<float>(xa + 1));
     const float2 Y = f2(static_cast<float>(ya), static_cast<float>(ya + 1));
     const float2 nk2 = f2(p.nk, p.nk);
+    const float thr = p.thr;
     float2 Wa = f2(0.f, 0.f), Wb = f2(0.f, 0.f);  // rows ya, ya+1; (xa, xa+1)
     float2 Na[CC], Nb[CC];
 #pragma unroll
@@ -121,11 +126,12 @@ k_gather(GatherParams p) {
         Nb[c] = f2(0.f, 0.f);
     }
     int cnt00 = 0, cnt01 = 0, cnt10 = 0, cnt11 = 0;
-    // lane window in fine columns: mu_x in [xa - r, xa + 1 + r]
-    const float wlo = X.x - p.rf - epsx, whi = X.y + p.rf + epsx;
-    const int wq0 = max(0, fine_col(wlo, g.qx0, g.qscale) - q_lo);
-    const int wq1 = min(nq - 1, fine_col(whi, g.qx0, g.qscale) - q_lo);
-    const float band_lo = Y.x - p.rf - epsy, band_hi = Y.y + p.rf + epsy;
+    // lane window: columns of mu_x in (xa - r, xa + 1 + r) (exact in f64)
+    const int q_lo = max(0, static_cast<int>(floor(static_cast<double>(2 * lane + p.rc) - p.r64)));
+    const int q_hi = min(ncol - 1, static_cast<int>(ceil(static_cast<double>(2 * lane + p.rc + 1) + p.r64)) - 1);
+    // flagged points: generous band test (decided exactly by the f64 predicate)
+    const float fb_lo = static_cast<float>(ya) - static_cast<float>(p.r64) - 1.0f;
+    const float fb_hi = static_cast<float>(ya + 1) + static_cast<float>(p.r64) + 1.0f;
 
     if (warp == 0) {
         // the f64 cell rectangle (four lanes in parallel)
@@ -137,7 +143,7 @@ k_gather(GatherParams p) {
         const int cx0 = __shfl_sync(0xffffffffu, cv, 0), cx1 = __shfl_sync(0xffffffffu, cv, 1);
         const int cy0 = __shfl_sync(0xffffffffu, cv, 2), cy1 = __shfl_sync(0xffffffffu, cv, 3);
         // common case: <= 32 cell rows and <= kCap candidates -> one chunk,
-        // runs loaded by one lane each (no serial chain of dependent loads)
+        // runs loaded by one lane each
         const int nrows = cy1 - cy0 + 1;
         bool one = false;
         if (nrows <= 32 && nrows <= kRsMax) {
@@ -210,183 +216,193 @@ k_gather(GatherParams p) {
             S.cur_off = off;
             S.done = cy > cy1;
         }
+        for (int k = tid; k <= nbins + 1; k += kNT) S.bin[k] = 0;
         __syncthreads();
         const int n_runs = S.n_runs;
         if (n_runs == 0) break;
-        for (int k = tid; k < n_runs * kNqMax; k += kNT) (&S.cnt[0][0])[k] = 0;
-        if (tid == 0) S.any_flag = 0;
-        __syncthreads();
+        const int total = S.run_beg[n_runs];
 
-        // ---- A: deterministic rank of each kept candidate in its (run, column)
+        // ---- A: bin of every staged candidate + histogram ----
         for (int rs = warp; rs < n_runs; rs += kNW) {
             const int gs = S.run_g[rs], rb = S.run_beg[rs], len = S.run_beg[rs + 1] - rb;
-            for (int j0 = 0; j0 < len; j0 += 32) {
-                const int j = j0 + lane;
-                float mx = 0.f, my = 0.f;
-                bool keep = false;
-                int q = 0;
-                if (j < len) {
-                    mx = p.sx[base + gs + j];
-                    my = p.sy[base + gs + j];
-                    keep = mx >= fxlo && mx <= fxhi && my >= fylo && my <= fyhi;
-                    q = fine_col(mx, g.qx0, g.qscale) - q_lo;
-                    keep = keep && q >= 0 && q < nq;
+            for (int j = lane; j < len; j += 32) {
+                const int slot = gs + j;
+                const float mx = p.sx[base + slot], my = p.sy[base + slot];
+                const bool flag = (static_cast<uint32_t>(p.sidx[base + slot]) & kUnsafeBit) != 0;
+                int key = -1;
+                const double dx = static_cast<double>(mx) - cxo;
+                const double dy = static_cast<double>(my) - cyo;
+                if (!flag) {
+                    if (dx >= 0.0 && dy >= 0.0) {
+                        const double qf = floor(dx), yf = floor(dy * 0.5);
+                        if (qf < ncol && yf < nyb)
+                            key = static_cast<int>(qf) * nyb + static_cast<int>(yf);
+                    }
+                } else if (static_cast<double>(mx) >= xlo - 1.0 && static_cast<double>(mx) <= xhi + 1.0 &&
+                           static_cast<double>(my) >= ylo - 1.0 && static_cast<double>(my) <= yhi + 1.0) {
+                    key = nbins;  // the flag bin
                 }
-                const int key = keep ? q : (0x10000 + lane);
-                const unsigned peers = __match_any_sync(0xffffffffu, key);
-                const int leader = __ffs(peers) - 1;
-                int bcnt = 0;
-                if (keep && lane == leader) {
-                    bcnt = S.cnt[rs][q];
-                    S.cnt[rs][q] = static_cast<uint16_t>(bcnt + __popc(peers));
-                }
-                bcnt = __shfl_sync(0xffffffffu, bcnt, leader);
-                if (j < len)
-                    S.srank[rb + j] = keep ? static_cast<uint16_t>(bcnt + __popc(peers & lt)) : 0xFFFFu;
-                __syncwarp();
+                if (key >= 0) atomicAdd(&S.bin[key], 1);
+                S.u.st.key[rb + j] = key;
+                S.u.st.slot[rb + j] = slot;
             }
         }
         __syncthreads();
 
-        // ---- B: column starts and per-column run offsets ----
+        // ---- B: inclusive scan of the nbins + 1 counts (ends) ----
         {
-            int colsum = 0;
-            if (tid < nq) {
-                for (int rs = 0; rs < n_runs; ++rs) {
-                    const int v = S.cnt[rs][tid];
-                    S.cnt[rs][tid] = static_cast<uint16_t>(colsum);
-                    colsum += v;
-                }
+            constexpr int kPer = (kBinMax + 1 + kNT - 1) / kNT;
+            const int nb = nbins + 1;
+            const int k0 = tid * kPer;
+            int v[kPer];
+            int s = 0;
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                v[j] = (k0 + j < nb) ? S.bin[k0 + j] : 0;
+                s += v[j];
             }
-            int incl = colsum;
+            int incl = s;
             for (int o = 1; o < 32; o <<= 1) {
                 const int t = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += t;
             }
             if (lane == 31) S.scan_w[warp] = incl;
             __syncthreads();
-            int wbase = 0;
-            for (int w = 0; w < warp; ++w) wbase += S.scan_w[w];
-            if (tid < nq) S.colstart[tid] = wbase + incl - colsum;
-            if (tid == kNT - 1) S.colstart[nq] = wbase + incl;
-        }
-        __syncthreads();
-
-        // ---- C: scatter the records column-major ----
-        for (int rs = warp; rs < n_runs; rs += kNW) {
-            const int gs = S.run_g[rs], rb = S.run_beg[rs], len = S.run_beg[rs + 1] - rb;
-            for (int j = lane; j < len; j += 32) {
-                const int r = S.srank[rb + j];
-                if (r == 0xFFFF) continue;
-                const size_t slot = base + gs + j;
-                const float mx = p.sx[slot], my = p.sy[slot];
-                const int q = fine_col(mx, g.qx0, g.qscale) - q_lo;
-                const int dst = S.colstart[q] + S.cnt[rs][q] + r;
-                float c[4] = {0.f, 0.f, 0.f, 0.f};
+            int run = incl - s;
+            for (int w = 0; w < warp; ++w) run += S.scan_w[w];
 #pragma unroll
-                for (int ch = 0; ch < CC; ++ch)
-                    if (ch < nch)
-                        c[ch] = p.scol[(static_cast<size_t>(b) * p.C + ch0 + ch) * p.N + gs + j];
-                S.A[dst] = make_float4(mx, my, c[0], c[1]);
-                if (CC > 2) S.Bc[dst] = f2(c[2], c[3]);
-                const uint8_t fl = static_cast<uint8_t>(static_cast<uint32_t>(p.sidx[slot]) >> 31);
-                S.flag[dst] = fl;
-                if (fl) S.any_flag = 1;
+            for (int j = 0; j < kPer; ++j) {
+                run += v[j];
+                if (k0 + j < nb) S.bin[k0 + j] = run;
+            }
+            if (tid == kNT - 1) S.bin[nb] = run;  // total kept
+        }
+        __syncthreads();
+
+        // ---- C: scatter (ends -> starts by atomic decrement) ----
+        for (int k = tid; k < total; k += kNT) {
+            const int key = S.u.st.key[k];
+            if (key < 0) continue;
+            const int pos = atomicSub(&S.bin[key], 1) - 1;
+            const int slot = S.u.st.slot[k];
+            float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int ch = 0; ch < CC; ++ch)
+                if (ch < nch)
+                    c[ch] = p.scol[(static_cast<size_t>(b) * p.C + ch0 + ch) * p.N + slot];
+            S.A[pos] = make_float4(p.sx[base + slot], p.sy[base + slot], c[0], c[1]);
+            if (CC > 2) S.Bc[pos] = f2(c[2], c[3]);
+            S.idx[pos] = p.sidx[base + slot] & 0x7fffffff;
+        }
+        __syncthreads();
+
+        // ---- D: canonical order inside each bin (ascending original index) ----
+        for (int k = tid; k <= nbins; k += kNT) {
+            const int s = S.bin[k], e = S.bin[k + 1];
+            for (int i = s + 1; i < e; ++i) {
+                const int vi = S.idx[i];
+                if (S.idx[i - 1] <= vi) continue;
+                const float4 va = S.A[i];
+                const float2 vb = CC > 2 ? S.Bc[i] : f2(0.f, 0.f);
+                int j = i;
+                while (j > s && S.idx[j - 1] > vi) {
+                    S.idx[j] = S.idx[j - 1];
+                    S.A[j] = S.A[j - 1];
+                    if (CC > 2) S.Bc[j] = S.Bc[j - 1];
+                    --j;
+                }
+                S.idx[j] = vi;
+                S.A[j] = va;
+                if (CC > 2) S.Bc[j] = vb;
             }
         }
         __syncthreads();
-        const bool any_flag = S.any_flag != 0;
 
-        // ---- D: per-warp band list and per-lane windows ----
-        const int T = S.colstart[nq];
-        int nf = 0;
-        for (int k0 = 0; k0 < T; k0 += 32) {
-            const int k = k0 + lane;
-            bool fast = false;
-            if (k < T) {
-                const float my = S.A[k].y;
-                fast = my >= band_lo && my <= band_hi && !S.flag[k];
+        // ---- E: this warp's column-major list (row-pair bins [w, w+dyb]) ----
+        {
+            const int yb0 = warp, yb1 = min(warp + p.dyb, nyb - 1);
+            constexpr int kCpl = kColMax / 32;
+            const int c0 = lane * kCpl;
+            int ps[kCpl], pl[kCpl];
+            int s = 0;
+#pragma unroll
+            for (int j = 0; j < kCpl; ++j) {
+                const int q = c0 + j;
+                ps[j] = 0;
+                pl[j] = 0;
+                if (q < ncol) {
+                    ps[j] = S.bin[q * nyb + yb0];
+                    pl[j] = S.bin[q * nyb + yb1 + 1] - ps[j];
+                }
+                s += pl[j];
             }
-            const unsigned bf = __ballot_sync(0xffffffffu, fast);
-            if (fast) S.list[warp][nf + __popc(bf & lt)] = static_cast<uint16_t>(k);
-            if (lane == 0) {
-                S.bal[warp][k0 >> 5] = bf;
-                S.balpre[warp][k0 >> 5] = static_cast<uint16_t>(nf);
+            int incl = s;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
             }
-            nf += __popc(bf);
-        }
-        if (lane == 0) {
-            S.bal[warp][(T + 31) >> 5] = 0u;
-            S.balpre[warp][(T + 31) >> 5] = static_cast<uint16_t>(nf);
+            int at = incl - s;
+            uint16_t* wl = S.u.wl[warp];
+#pragma unroll
+            for (int j = 0; j < kCpl; ++j) {
+                const int q = c0 + j;
+                if (q <= ncol) S.wcs[warp][q] = static_cast<uint16_t>(at);
+                for (int e = 0; e < pl[j]; ++e) wl[at + e] = static_cast<uint16_t>(ps[j] + e);
+                at += pl[j];
+            }
         }
         __syncwarp();
-        auto prefix_kept = [&](int pos) -> int {
-            const int c = pos >> 5, bit = pos & 31;
-            return S.balpre[warp][c] + __popc(S.bal[warp][c] & ((1u << bit) - 1u));
-        };
-        int ts = 0, te = 0;
-        if (wq0 <= wq1) {
-            ts = prefix_kept(S.colstart[wq0]);
-            te = prefix_kept(S.colstart[wq1 + 1]);
-        }
 
         // ---- gather: 4 pixels per candidate, f32x2 ----
-        const uint16_t* lst = S.list[warp];
+        {
+            const int ts = S.wcs[warp][q_lo], te = S.wcs[warp][q_hi + 1];
+            const uint16_t* lst = S.u.wl[warp];
 #pragma unroll 2
-        for (int t = ts; t < te; ++t) {
-            const int kc = lst[t];
-            const float4 a = S.A[kc];
-            const float2 bcur = CC > 2 ? S.Bc[kc] : f2(0.f, 0.f);
-            const float2 dx = __fadd2_rn(X, f2(-a.x, -a.x));
-            const float2 dy = __fadd2_rn(Y, f2(-a.y, -a.y));
-            const float2 sxx = __fmul2_rn(dx, dx);
-            const float2 syy = __fmul2_rn(dy, dy);
-            const float2 da = __fadd2_rn(sxx, f2(syy.x, syy.x));
-            const float2 db = __fadd2_rn(sxx, f2(syy.y, syy.y));
-            const float2 aa = __fmul2_rn(da, nk2);
-            const float2 ab = __fmul2_rn(db, nk2);
-            const bool i00 = da.x <= p.r2f, i01 = da.y <= p.r2f;
-            const bool i10 = db.x <= p.r2f, i11 = db.y <= p.r2f;
-            const float2 wa = f2(i00 ? ex2(aa.x) : 0.f, i01 ? ex2(aa.y) : 0.f);
-            const float2 wb = f2(i10 ? ex2(ab.x) : 0.f, i11 ? ex2(ab.y) : 0.f);
-            Wa = __fadd2_rn(Wa, wa);
-            Wb = __fadd2_rn(Wb, wb);
-            Na[0] = __ffma2_rn(wa, f2(a.z, a.z), Na[0]);
-            Nb[0] = __ffma2_rn(wb, f2(a.z, a.z), Nb[0]);
-            if (CC > 1) {
-                Na[1] = __ffma2_rn(wa, f2(a.w, a.w), Na[1]);
-                Nb[1] = __ffma2_rn(wb, f2(a.w, a.w), Nb[1]);
-            }
-            if (CC > 2) {
-                const float2 bc = bcur;
-                Na[2] = __ffma2_rn(wa, f2(bc.x, bc.x), Na[2]);
-                Nb[2] = __ffma2_rn(wb, f2(bc.x, bc.x), Nb[2]);
-                if (CC > 3) {
-                    Na[3] = __ffma2_rn(wa, f2(bc.y, bc.y), Na[3]);
-                    Nb[3] = __ffma2_rn(wb, f2(bc.y, bc.y), Nb[3]);
+            for (int t = ts; t < te; ++t) {
+                const int kc = lst[t];
+                const float4 a = S.A[kc];
+                const float2 bcur = CC > 2 ? S.Bc[kc] : f2(0.f, 0.f);
+                const float2 dx = __fadd2_rn(X, f2(-a.x, -a.x));
+                const float2 dy = __fadd2_rn(Y, f2(-a.y, -a.y));
+                const float2 kx = __fmul2_rn(dx, nk2);
+                const float2 ey = __fmul2_rn(__fmul2_rn(dy, nk2), dy);
+                const float2 ea = __ffma2_rn(kx, dx, f2(ey.x, ey.x));
+                const float2 eb = __ffma2_rn(kx, dx, f2(ey.y, ey.y));
+                const bool i00 = ea.x >= thr, i01 = ea.y >= thr;
+                const bool i10 = eb.x >= thr, i11 = eb.y >= thr;
+                const float2 wa = f2(i00 ? ex2(ea.x) : 0.f, i01 ? ex2(ea.y) : 0.f);
+                const float2 wb = f2(i10 ? ex2(eb.x) : 0.f, i11 ? ex2(eb.y) : 0.f);
+                Wa = __fadd2_rn(Wa, wa);
+                Wb = __fadd2_rn(Wb, wb);
+                Na[0] = __ffma2_rn(wa, f2(a.z, a.z), Na[0]);
+                Nb[0] = __ffma2_rn(wb, f2(a.z, a.z), Nb[0]);
+                if (CC > 1) {
+                    Na[1] = __ffma2_rn(wa, f2(a.w, a.w), Na[1]);
+                    Nb[1] = __ffma2_rn(wb, f2(a.w, a.w), Nb[1]);
                 }
-            }
-            if (kCount) {
-                cnt00 += i00;
-                cnt01 += i01;
-                cnt10 += i10;
-                cnt11 += i11;
+                if (CC > 2) {
+                    Na[2] = __ffma2_rn(wa, f2(bcur.x, bcur.x), Na[2]);
+                    Nb[2] = __ffma2_rn(wb, f2(bcur.x, bcur.x), Nb[2]);
+                    if (CC > 3) {
+                        Na[3] = __ffma2_rn(wa, f2(bcur.y, bcur.y), Na[3]);
+                        Nb[3] = __ffma2_rn(wb, f2(bcur.y, bcur.y), Nb[3]);
+                    }
+                }
+                if (kCount) {
+                    cnt00 += i00;
+                    cnt01 += i01;
+                    cnt10 += i10;
+                    cnt11 += i11;
+                }
             }
         }
 
-        // ---- boundary-ambiguous points: f64 predicate (rare) ----
-        for (int k0 = 0; any_flag && k0 < T; k0 += 32) {
-            const int k = k0 + lane;
-            bool ex = false;
-            if (k < T) {
-                const float my = S.A[k].y;
-                ex = S.flag[k] && my >= band_lo && my <= band_hi;
-            }
-            unsigned bx = __ballot_sync(0xffffffffu, ex);
-            while (bx) {
-                const int kk = k0 + __ffs(bx) - 1;
-                bx &= bx - 1u;
+        // ---- boundary-ambiguous points: f64 predicate (rare), index order ----
+        {
+            const int fs = S.bin[nbins], fe = S.bin[nbins + 1];
+            for (int kk = fs; kk < fe; ++kk) {
                 const float4 a = S.A[kk];
+                if (!(a.y >= fb_lo && a.y <= fb_hi)) continue;  // warp-uniform
                 float cc[4] = {a.z, a.w, 0.f, 0.f};
                 if (CC > 2) {
                     const float2 bc = S.Bc[kk];
@@ -401,7 +417,7 @@ k_gather(GatherParams p) {
                         if (d2_ref(qx, qy, a.x, a.y) > p.r2_64) continue;
                         const float ddx = static_cast<float>(qx) - a.x;
                         const float ddy = static_cast<float>(qy) - a.y;
-                        const float w = ex2(fmaf(ddx, ddx, ddy * ddy) * p.nk);
+                        const float w = ex2(fmaf(ddx * p.nk, ddx, (ddy * p.nk) * ddy));
                         float2& Wr = py ? Wb : Wa;
                         float2* Nr = py ? Nb : Na;
                         if (px) Wr.y += w; else Wr.x += w;
@@ -472,13 +488,19 @@ void launch_cc(gmi_ctx* ctx, const GatherParams& p, dim3 grid) {
 namespace gmi_host {
 
 // Returns false when the configuration needs the generic gather
-// (f64 weight mode, C > 4, or a radius whose fine-column window exceeds the
-// staging tables).
+// (f64 weight mode, or a radius whose bin table exceeds the staging tables).
 bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts) {
     if (c->wsum64 != nullptr) return false;
-    const double need_cols = 2.0 * (kTW - 1 + 2.0 * c->cutoff + 0.05) + 4.0;
-    if (need_cols > kNqMax) return false;
+    const double r = c->cutoff;
     GatherParams p{};
+    // columns: floor(mu_x - (x0 - rc)), rc = ceil(r); lane windows are the
+    // columns of (xa - r, xa + 1 + r), so ncol covers the last lane's
+    p.rc = static_cast<int>(std::ceil(r));
+    p.ncol = static_cast<int>(std::ceil(static_cast<double>(kTW - 2 + p.rc + 1) + r));
+    // row pairs: floor((mu_y - (y0 - r)) / 2); warp w reads [w, w + dyb]
+    p.dyb = static_cast<int>(std::ceil(0.5 + r)) - 1;
+    p.nyb = kNW + p.dyb;
+    if (p.ncol >= kColMax || p.ncol * p.nyb + 1 > kBinMax) return false;
     p.geom = c->geom_d;
     p.bins = c->bins;
     p.sx = c->sx;
@@ -489,11 +511,13 @@ bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* count
     p.C = c->C;
     p.W = c->W;
     p.H = c->H;
-    p.r64 = c->cutoff;
-    p.r2_64 = c->cutoff * c->cutoff;
-    p.rf = static_cast<float>(c->cutoff);
+    p.r64 = r;
+    p.r2_64 = r * r;
     p.r2f = static_cast<float>(p.r2_64);
     p.nk = static_cast<float>(-1.4426950408889634 / (2.0 * c->sigma * c->sigma));
+    // in-ball test on e = nk d^2: e >= nk r^2 (fp32 rounding of both sides is
+    // ~3 ulp, far inside the 8e-6 r^2 safety band of unflagged points)
+    p.thr = p.r2f * p.nk;
     p.image = image;
     p.wsum = c->wsum;
     p.counts = counts;
