@@ -97,7 +97,7 @@ template <int CG>
 __global__ void __launch_bounds__(kThreads, 4)
 k_backward_points(BwdParams p) {
     using L = PairLayout<CG>;
-    extern __shared__ float4 s_pair[];   // [rows][pairs][L::kF4]
+    extern __shared__ float4 s_pair[];   // [L::kF4][rows][pairs]
     __shared__ int s_run[kRunMax + 1];   // prefix of the block's cell-row runs
     __shared__ int s_rung[kRunMax];      // first slot of each run
     __shared__ float s_red[4][kThreads / 32];
@@ -227,10 +227,10 @@ k_backward_points(BwdParams p) {
     }
     const bool staged = mode == 1;
     const int npairs = (rx1 - rx0 + 1) / 2;
+    const int area = npairs * (ry1 - ry0 + 1);
     const size_t img_base = static_cast<size_t>(b) * p.H * p.W;
 
     if (staged) {
-        const int area = npairs * (ry1 - ry0 + 1);
         // 8-byte alignment of a pixel pair in W / upstream / image rows
         const bool vec = (p.W % 2 == 0) && (CG == p.C);
         for (int k = tid; k < area; k += kThreads) {
@@ -272,10 +272,10 @@ k_backward_points(BwdParams p) {
             e[CG] = f2(-va, -vb);
 #pragma unroll
             for (int c = CG + 1; c < 2 * L::kF4; ++c) e[c] = f2(0.f, 0.f);
-            float4* dst = s_pair + static_cast<size_t>(k) * L::kF4;
+            // slot-major planes (16-byte stride: conflict-light LDS.128)
 #pragma unroll
             for (int j = 0; j < L::kF4; ++j)
-                dst[j] = make_float4(e[2 * j].x, e[2 * j].y, e[2 * j + 1].x, e[2 * j + 1].y);
+                s_pair[j * area + k] = make_float4(e[2 * j].x, e[2 * j].y, e[2 * j + 1].x, e[2 * j + 1].y);
         }
         __syncthreads();
     }
@@ -383,11 +383,12 @@ k_backward_points(BwdParams p) {
             float2 X = f2(static_cast<float>(xs), static_cast<float>(xs + 1));
             const float2 ey2 = f2(ey, ey), mmx = f2(-mx, -mx);
             float2 gyr2 = f2(0.f, 0.f);
-            const float4* pr = s_pair + (static_cast<size_t>(y - ry0) * npairs + ((xs - rx0) >> 1)) * L::kF4;
+            const float4* pr = s_pair + (y - ry0) * npairs + ((xs - rx0) >> 1);
+#pragma unroll 2
             for (int j = 0; j < np; ++j) {
                 float4 q4[L::kF4];
 #pragma unroll
-                for (int c = 0; c < L::kF4; ++c) q4[c] = pr[c];
+                for (int c = 0; c < L::kF4; ++c) q4[c] = pr[c * area];
                 const float2* q = reinterpret_cast<const float2*>(q4);
                 const float2 dx = __fadd2_rn(X, mmx);
                 const float2 arg = __ffma2_rn(__fmul2_rn(dx, nk2), dx, ey2);
@@ -404,7 +405,7 @@ k_backward_points(BwdParams p) {
                 gx2 = __ffma2_rn(a, dx, gx2);
                 gyr2 = __fadd2_rn(gyr2, a);
                 X = __fadd2_rn(X, two);
-                pr += L::kF4;
+                ++pr;
             }
             gy = fmaf(gyr2.x + gyr2.y, dy, gy);
         }

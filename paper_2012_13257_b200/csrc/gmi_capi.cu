@@ -102,13 +102,57 @@ int collect_issue(gmi_ctx* ctx, int B) {
 }
 
 void free_cache_buffers(gmi_cache* c) {
+    for (gmi_cache* part : c->parts) {
+        free_cache_buffers(part);
+        delete part;
+    }
+    c->parts.clear();
+    c->part_b0.clear();
     for (auto& b : c->owned) cudaFreeAsync(b.p, c->ctx->stream);
     c->owned.clear();
 }
 
+// Image chunks of the pipelined host API: enough chunks that the copy of
+// chunk k+1 in, chunk k-1 out and the kernels of chunk k overlap, few enough
+// that each chunk still fills the GPU (>= 1 image, <= 8 chunks).
+int host_chunks(int B) { return std::max(1, std::min(B, 8)); }
+
+void ensure_copy_streams(gmi_ctx* ctx) {
+    if (ctx->s_in == nullptr)
+        GMI_CUDA(cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking));
+    if (ctx->s_out == nullptr)
+        GMI_CUDA(cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking));
+}
+
+struct EventSet {
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t get() {
+        cudaEvent_t e;
+        GMI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ev.push_back(e);
+        return e;
+    }
+    ~EventSet() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
+// the backward of one (part) cache on device buffers at image offset 0
+void backward_part(gmi_ctx* ctx, const gmi_cache* c, const float* upstream, float* d_colors,
+                   float* d_positions) {
+    {
+        PhaseScope ph(ctx, 3);
+        gmi_host::launch_backward(ctx, c, upstream, d_colors, d_positions);
+    }
+    {
+        PhaseScope ph(ctx, 4);
+        gmi_host::launch_special_backward(ctx, c, upstream, d_colors, d_positions);
+    }
+}
+
 int do_forward(gmi_ctx* ctx, const float* pos, const float* col, int B, int N,
                int C, const gmi_config* cfg, float* image, gmi_cache* c,
-               int32_t* counts) {
+               int32_t* counts, unsigned long long* d_issue = nullptr) {
     c->ctx = ctx;
     c->B = B;
     c->N = N;
@@ -135,11 +179,14 @@ int do_forward(gmi_ctx* ctx, const float* pos, const float* col, int B, int N,
     c->special_cap = static_cast<int>(std::min<size_t>(BHW, size_t(1) << 22));
     c->special = static_cast<Special*>(gmi_host::cache_alloc(c, sizeof(Special) * c->special_cap));
     c->special_count_d = static_cast<int32_t*>(gmi_host::cache_alloc(c, sizeof(int32_t)));
-    ensure_issue(ctx, B);
+    if (d_issue == nullptr) {
+        ensure_issue(ctx, B);
+        d_issue = ctx->d_issue;
+    }
     host_trace("fwd: allocs");
     {
         PhaseScope ph(ctx, 0);
-        gmi_host::bin_points(ctx, c, pos, col, hot_cap(cfg), true, nullptr, ctx->d_issue);
+        gmi_host::bin_points(ctx, c, pos, col, hot_cap(cfg), true, nullptr, d_issue);
     }
     {
         PhaseScope ph(ctx, 1);
@@ -176,13 +223,15 @@ int backward_checks(const gmi_cache* c, int B, int N, int C, const gmi_config* c
 
 int do_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
                 float* d_colors, float* d_positions) {
-    {
-        PhaseScope ph(ctx, 3);
-        gmi_host::launch_backward(ctx, c, upstream, d_colors, d_positions);
-    }
-    {
-        PhaseScope ph(ctx, 4);
-        gmi_host::launch_special_backward(ctx, c, upstream, d_colors, d_positions);
+    if (c->parts.empty()) {
+        backward_part(ctx, c, upstream, d_colors, d_positions);
+    } else {
+        const size_t hwc = static_cast<size_t>(c->H) * c->W * c->C;
+        for (size_t k = 0; k < c->parts.size(); ++k) {
+            const size_t b0 = c->part_b0[k];
+            backward_part(ctx, c->parts[k], upstream + b0 * hwc,
+                          d_colors + b0 * c->N * c->C, d_positions + b0 * c->N * 2);
+        }
     }
     if (!(ctx->flags & GMI_CTX_ASYNC_ERRORS)) GMI_CUDA(cudaStreamSynchronize(ctx->stream));
     return GMI_OK;
@@ -295,6 +344,8 @@ int gmi_ctx_destroy(gmi_ctx* ctx) {
         if (ctx->d_issue) cudaFree(ctx->d_issue);
         if (ctx->h_issue) cudaFreeHost(ctx->h_issue);
         if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+        if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
+        if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
         delete ctx;
         return GMI_OK;
     });
@@ -422,6 +473,9 @@ int gmi_backward(gmi_ctx* ctx, const float* positions, const float* colors, int3
 int gmi_forward_host(gmi_ctx* ctx, const float* positions, const float* colors, int32_t batch,
                      int32_t num_points, int32_t channels, const gmi_config* cfg, float* image,
                      gmi_cache** cache_out) {
+    // Pipelined over image chunks: H2D of chunk k+1 (s_in), the forward of
+    // chunk k (ctx stream) and the D2H of chunk k-1 (s_out) overlap.  The
+    // returned cache is composite (one part cache per chunk).
     return guarded([&]() -> int {
         if (ctx == nullptr || cache_out == nullptr || image == nullptr)
             return fail(GMI_ERR_INVALID_ARGUMENT, "null argument");
@@ -430,28 +484,84 @@ int gmi_forward_host(gmi_ctx* ctx, const float* positions, const float* colors, 
         rc = check_config(cfg);
         if (rc) return rc;
         GMI_CUDA(cudaSetDevice(ctx->device));
+        ensure_copy_streams(ctx);
+        ensure_issue(ctx, batch);
         auto* c = new gmi_cache();
         c->ctx = ctx;
-        const size_t BN = static_cast<size_t>(batch) * num_points;
-        const size_t img = static_cast<size_t>(batch) * cfg->height * cfg->width * channels;
+        c->B = batch;
+        c->N = num_points;
+        c->C = channels;
+        c->W = cfg->width;
+        c->H = cfg->height;
+        c->sigma = cfg->sigma;
+        c->cutoff = cfg->cutoff_radius;
+        c->fallback = cfg->fallback;
+        const size_t N = num_points, C = channels;
+        const size_t hwc = static_cast<size_t>(cfg->height) * cfg->width * C;
+        const uint32_t saved = ctx->flags;
         try {
-            float* dpos = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN * 2));
-            float* dcol = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN * channels));
-            float* dimg = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * img));
-            GMI_CUDA(cudaMemcpyAsync(dpos, positions, sizeof(float) * BN * 2,
-                                     cudaMemcpyHostToDevice, ctx->stream));
-            GMI_CUDA(cudaMemcpyAsync(dcol, colors, sizeof(float) * BN * channels,
-                                     cudaMemcpyHostToDevice, ctx->stream));
-            const uint32_t saved = ctx->flags;
-            ctx->flags &= ~GMI_CTX_ASYNC_ERRORS;
-            rc = do_forward(ctx, dpos, dcol, batch, num_points, channels, cfg, dimg, c, nullptr);
+            EventSet E;
+            float* dpos = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * batch * N * 2));
+            float* dcol = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * batch * N * C));
+            float* dimg = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * batch * hwc));
+            c->pos = dpos;
+            c->col = dcol;
+            c->image = dimg;
+            cudaEvent_t alloc = E.get();
+            GMI_CUDA(cudaEventRecord(alloc, ctx->stream));
+            GMI_CUDA(cudaStreamWaitEvent(ctx->s_in, alloc, 0));
+            const int nk = host_chunks(batch);
+            std::vector<int> b0(nk + 1);
+            for (int k = 0; k <= nk; ++k) b0[k] = static_cast<int>((static_cast<int64_t>(batch) * k) / nk);
+            std::vector<cudaEvent_t> in(nk);
+            for (int k = 0; k < nk; ++k) {
+                const size_t o = b0[k], n = b0[k + 1] - b0[k];
+                GMI_CUDA(cudaMemcpyAsync(dpos + o * N * 2, positions + o * N * 2, sizeof(float) * n * N * 2,
+                                         cudaMemcpyHostToDevice, ctx->s_in));
+                GMI_CUDA(cudaMemcpyAsync(dcol + o * N * C, colors + o * N * C, sizeof(float) * n * N * C,
+                                         cudaMemcpyHostToDevice, ctx->s_in));
+                in[k] = E.get();
+                GMI_CUDA(cudaEventRecord(in[k], ctx->s_in));
+            }
+            ctx->flags |= GMI_CTX_ASYNC_ERRORS;
+            for (int k = 0; k < nk; ++k) {
+                const size_t o = b0[k];
+                const int n = b0[k + 1] - b0[k];
+                GMI_CUDA(cudaStreamWaitEvent(ctx->stream, in[k], 0));
+                auto* part = new gmi_cache();
+                part->ctx = ctx;
+                c->parts.push_back(part);
+                c->part_b0.push_back(static_cast<int>(o));
+                rc = do_forward(ctx, dpos + o * N * 2, dcol + o * N * C, n, num_points, channels, cfg,
+                                dimg + o * hwc, part, nullptr, ctx->d_issue + o);
+                if (rc != GMI_OK) break;
+                cudaEvent_t done = E.get();
+                GMI_CUDA(cudaEventRecord(done, ctx->stream));
+                GMI_CUDA(cudaStreamWaitEvent(ctx->s_out, done, 0));
+                GMI_CUDA(cudaMemcpyAsync(image + o * hwc, dimg + o * hwc, sizeof(float) * n * hwc,
+                                         cudaMemcpyDeviceToHost, ctx->s_out));
+            }
             ctx->flags = saved;
+            GMI_CUDA(cudaStreamSynchronize(ctx->s_out));
+            GMI_CUDA(cudaStreamSynchronize(ctx->s_in));
+            if (rc == GMI_OK) rc = collect_issue(ctx, batch);
             if (rc == GMI_OK) {
-                GMI_CUDA(cudaMemcpyAsync(image, dimg, sizeof(float) * img, cudaMemcpyDeviceToHost,
-                                         ctx->stream));
-                GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+                for (gmi_cache* part : c->parts) {
+                    int32_t nspec = 0;
+                    GMI_CUDA(cudaMemcpy(&nspec, part->special_count_d, sizeof(int32_t),
+                                        cudaMemcpyDeviceToHost));
+                    if (nspec > part->special_cap) {
+                        rc = fail(GMI_ERR_OUT_OF_MEMORY, "more than " + std::to_string(part->special_cap) +
+                                                             " fallback pixels");
+                        break;
+                    }
+                    part->special_count = nspec;
+                }
             }
         } catch (...) {
+            ctx->flags = saved;
+            cudaStreamSynchronize(ctx->s_in);
+            cudaStreamSynchronize(ctx->s_out);
             free_cache_buffers(c);
             delete c;
             throw;
@@ -470,6 +580,8 @@ int gmi_backward_host(gmi_ctx* ctx, const float* positions, const float* colors,
                       int32_t num_points, int32_t channels, const gmi_config* cfg,
                       const gmi_cache* cache, const float* upstream, float* d_colors,
                       float* d_positions) {
+    // Pipelined over the forward cache's image chunks: H2D of upstream chunk
+    // k+1, the backward of chunk k and the D2H of chunk k-1's gradients overlap.
     return guarded([&]() -> int {
         if (ctx == nullptr || upstream == nullptr || d_colors == nullptr || d_positions == nullptr)
             return fail(GMI_ERR_INVALID_ARGUMENT, "null argument");
@@ -480,25 +592,50 @@ int gmi_backward_host(gmi_ctx* ctx, const float* positions, const float* colors,
         rc = backward_checks(cache, batch, num_points, channels, cfg);
         if (rc) return rc;
         GMI_CUDA(cudaSetDevice(ctx->device));
-        const size_t BN = static_cast<size_t>(batch) * num_points;
-        const size_t img = static_cast<size_t>(batch) * cfg->height * cfg->width * channels;
-        float* dup = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * img));
-        float* dc = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * BN * channels));
-        float* dp = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * BN * 2));
-        GMI_CUDA(cudaMemcpyAsync(dup, upstream, sizeof(float) * img, cudaMemcpyHostToDevice,
-                                 ctx->stream));
-        {
-            PhaseScope ph(ctx, 3);
-            gmi_host::launch_backward(ctx, cache, dup, dc, dp);
+        ensure_copy_streams(ctx);
+        const size_t N = num_points, C = channels;
+        const size_t hwc = static_cast<size_t>(cfg->height) * cfg->width * C;
+        std::vector<const gmi_cache*> parts;
+        std::vector<int> b0;
+        if (cache->parts.empty()) {
+            parts.push_back(cache);
+            b0.push_back(0);
+        } else {
+            for (size_t k = 0; k < cache->parts.size(); ++k) {
+                parts.push_back(cache->parts[k]);
+                b0.push_back(cache->part_b0[k]);
+            }
         }
-        {
-            PhaseScope ph(ctx, 4);
-            gmi_host::launch_special_backward(ctx, cache, dup, dc, dp);
+        EventSet E;
+        float* dup = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * batch * hwc));
+        float* dc = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * batch * N * C));
+        float* dp = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * batch * N * 2));
+        cudaEvent_t alloc = E.get();
+        GMI_CUDA(cudaEventRecord(alloc, ctx->stream));
+        GMI_CUDA(cudaStreamWaitEvent(ctx->s_in, alloc, 0));
+        std::vector<cudaEvent_t> in(parts.size());
+        for (size_t k = 0; k < parts.size(); ++k) {
+            const size_t o = b0[k], n = parts[k]->B;
+            GMI_CUDA(cudaMemcpyAsync(dup + o * hwc, upstream + o * hwc, sizeof(float) * n * hwc,
+                                     cudaMemcpyHostToDevice, ctx->s_in));
+            in[k] = E.get();
+            GMI_CUDA(cudaEventRecord(in[k], ctx->s_in));
         }
-        GMI_CUDA(cudaMemcpyAsync(d_colors, dc, sizeof(float) * BN * channels,
-                                 cudaMemcpyDeviceToHost, ctx->stream));
-        GMI_CUDA(cudaMemcpyAsync(d_positions, dp, sizeof(float) * BN * 2, cudaMemcpyDeviceToHost,
-                                 ctx->stream));
+        for (size_t k = 0; k < parts.size(); ++k) {
+            const size_t o = b0[k], n = parts[k]->B;
+            GMI_CUDA(cudaStreamWaitEvent(ctx->stream, in[k], 0));
+            backward_part(ctx, parts[k], dup + o * hwc, dc + o * N * C, dp + o * N * 2);
+            cudaEvent_t done = E.get();
+            GMI_CUDA(cudaEventRecord(done, ctx->stream));
+            GMI_CUDA(cudaStreamWaitEvent(ctx->s_out, done, 0));
+            GMI_CUDA(cudaMemcpyAsync(d_colors + o * N * C, dc + o * N * C, sizeof(float) * n * N * C,
+                                     cudaMemcpyDeviceToHost, ctx->s_out));
+            GMI_CUDA(cudaMemcpyAsync(d_positions + o * N * 2, dp + o * N * 2, sizeof(float) * n * N * 2,
+                                     cudaMemcpyDeviceToHost, ctx->s_out));
+        }
+        cudaEvent_t out_done = E.get();
+        GMI_CUDA(cudaEventRecord(out_done, ctx->s_out));
+        GMI_CUDA(cudaStreamWaitEvent(ctx->stream, out_done, 0));
         gmi_host::dfree(ctx, dup);
         gmi_host::dfree(ctx, dc);
         gmi_host::dfree(ctx, dp);
@@ -542,6 +679,13 @@ static int read_special(const gmi_cache* c, std::vector<Special>& sp) {
 }
 
 int gmi_cache_fallback_count(const gmi_cache* c, int64_t* out) {
+    if (c != nullptr && out != nullptr && !c->parts.empty()) {
+        for (size_t k = 0; k < c->parts.size(); ++k) {
+            const int rc = gmi_cache_fallback_count(c->parts[k], out + c->part_b0[k]);
+            if (rc != GMI_OK) return rc;
+        }
+        return GMI_OK;
+    }
     return guarded([&]() -> int {
         if (c == nullptr || out == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "null argument");
         std::vector<Special> sp;
@@ -555,6 +699,17 @@ int gmi_cache_fallback_count(const gmi_cache* c, int64_t* out) {
 
 int gmi_cache_copy_pixels(const gmi_cache* c, float* normalizer, uint8_t* fallback_flag,
                           int32_t* nearest_index) {
+    if (c != nullptr && !c->parts.empty()) {
+        const size_t hw = static_cast<size_t>(c->H) * c->W;
+        for (size_t k = 0; k < c->parts.size(); ++k) {
+            const size_t o = static_cast<size_t>(c->part_b0[k]) * hw;
+            const int rc = gmi_cache_copy_pixels(c->parts[k], normalizer ? normalizer + o : nullptr,
+                                                 fallback_flag ? fallback_flag + o : nullptr,
+                                                 nearest_index ? nearest_index + o : nullptr);
+            if (rc != GMI_OK) return rc;
+        }
+        return GMI_OK;
+    }
     return guarded([&]() -> int {
         if (c == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "cache is null");
         const size_t BHW = static_cast<size_t>(c->B) * c->H * c->W;

@@ -61,6 +61,9 @@ struct gmi_ctx {
     // grow-only per-call scratch (stream-ordered reuse on the ctx stream)
     void* ws_ptr[16] = {nullptr};
     size_t ws_cap[16] = {0};
+    // copy streams of the pipelined host-buffer API (created on first use)
+    cudaStream_t s_in = nullptr;
+    cudaStream_t s_out = nullptr;
 };
 
 // scratch slots
@@ -137,6 +140,10 @@ struct gmi_cache {
     int special_count = -1;   // host copy (-1 = not read yet)
     bool special_overflow = false;
     bool force_generic = false;  // use the generic gather (tests / GMI_GENERIC)
+    // composite cache of the pipelined host API: image chunks [part_b0[k],
+    // part_b0[k] + parts[k]->B), each a complete cache of its own
+    std::vector<gmi_cache*> parts;
+    std::vector<int> part_b0;
 };
 
 namespace gmi_host {
