@@ -42,6 +42,7 @@ struct BwdParams {
     const float* sy;
     const int32_t* sidx;
     const float* scol;      // [B][C][N]
+    const float4* rec;      // fast layout [B][N][2] (replaces sx/sy/sidx/scol)
     const float* wsum;      // [B][H][W]
     const float* image;     // [B][H][W][C]
     const float* upstream;  // [B][H][W][C]
@@ -119,6 +120,7 @@ k_backward_points(BwdParams p) {
     const int local = blockIdx.x - p.blk_off[b];
     const int nbx = (g.n_cols + p.bs - 1) / p.bs;
     const int cx0 = (local % nbx) * p.bs, cy0 = (local / nbx) * p.bs;
+    if (cy0 >= g.n_rows) return;  // past this image's grid (device geometry)
     const int cx1 = min(cx0 + p.bs, g.n_cols), cy1 = min(cy0 + p.bs, g.n_rows);
     const int cg = blockIdx.y, ch0 = cg * CG, nch = min(CG, p.C - ch0);
     const int tid = threadIdx.x, lane = tid & 31;
@@ -167,7 +169,15 @@ k_backward_points(BwdParams p) {
     float mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
     for (int k = tid; k < total; k += kThreads) {
         const int s = slot_of(k);
-        const float x = p.sx[base + s], y = p.sy[base + s];
+        float x, y;
+        if (p.rec) {
+            const float4 ra = p.rec[(base + s) * 2];
+            x = ra.x;
+            y = ra.y;
+        } else {
+            x = p.sx[base + s];
+            y = p.sy[base + s];
+        }
         mnx = fminf(mnx, x);
         mny = fminf(mny, y);
         mxx = fmaxf(mxx, x);
@@ -217,7 +227,9 @@ k_backward_points(BwdParams p) {
     if (mode < 0) {
         // no frame pixel is reachable: gradients are zero
         for (int k = tid; k < total; k += kThreads) {
-            const int i = p.sidx[base + slot_of(k)] & 0x7fffffff;
+            const int sk = slot_of(k);
+            const int i = (p.rec ? static_cast<int>(__float_as_uint(p.rec[(base + sk) * 2 + 1].z))
+                                 : p.sidx[base + sk]) & 0x7fffffff;
             for (int c = 0; c < nch; ++c) p.d_col[(base + i) * p.C + ch0 + c] = 0.f;
             float* dp = p.d_pos + (static_cast<size_t>(cg) * p.B * p.N + base + i) * 2;
             dp[0] = 0.f;
@@ -298,14 +310,29 @@ k_backward_points(BwdParams p) {
         const int k = kb + lane;
         if (k >= total) continue;
         const int s = slot_of(k);
-        const float mx = p.sx[base + s], my = p.sy[base + s];
-        const uint32_t raw = static_cast<uint32_t>(p.sidx[base + s]);
+        float mx, my;
+        uint32_t raw;
+        float cc[CG];
+        if (p.rec) {
+            // fast layout: C <= 4, one channel group
+            const float4 ra = p.rec[(base + s) * 2];
+            const float4 rb = p.rec[(base + s) * 2 + 1];
+            mx = ra.x;
+            my = ra.y;
+            raw = __float_as_uint(rb.z);
+            const float cv[4] = {ra.z, ra.w, rb.x, rb.y};
+#pragma unroll
+            for (int c = 0; c < CG; ++c) cc[c] = cv[c];
+        } else {
+            mx = p.sx[base + s];
+            my = p.sy[base + s];
+            raw = static_cast<uint32_t>(p.sidx[base + s]);
+#pragma unroll
+            for (int c = 0; c < CG; ++c)
+                cc[c] = c < nch ? p.scol[(static_cast<size_t>(b) * p.C + ch0 + c) * p.N + s] : 0.f;
+        }
         const int i = static_cast<int>(raw & 0x7fffffffu);
         const bool unsafe = (raw & kUnsafeBit) != 0;
-        float cc[CG];
-#pragma unroll
-        for (int c = 0; c < CG; ++c)
-            cc[c] = c < nch ? p.scol[(static_cast<size_t>(b) * p.C + ch0 + c) * p.N + s] : 0.f;
         float2 dcol[CG];
 #pragma unroll
         for (int c = 0; c < CG; ++c) dcol[c] = f2(0.f, 0.f);
@@ -536,8 +563,16 @@ void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
     bs = std::max(1, std::min(bs, kRunMax));
     std::vector<int32_t> off(c->B + 1, 0);
     for (int b = 0; b < c->B; ++b) {
-        const auto& g = c->geom_h[b];
-        const int nb = ((g.n_cols + bs - 1) / bs) * ((g.n_rows + bs - 1) / bs);
+        int nb;
+        if (c->geom_h.empty()) {
+            // device geometry: a grid of at most grid_cap^2 cells per image;
+            // CTAs past the image's actual grid exit at once
+            const int side = (c->grid_cap + bs - 1) / bs;
+            nb = side * side;
+        } else {
+            const auto& g = c->geom_h[b];
+            nb = ((g.n_cols + bs - 1) / bs) * ((g.n_rows + bs - 1) / bs);
+        }
         off[b + 1] = off[b] + nb;
     }
     int32_t* d_off = static_cast<int32_t*>(scratch(ctx, WS_BLKOFF, sizeof(int32_t) * (c->B + 1)));
@@ -551,6 +586,7 @@ void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
     p.sy = c->sy;
     p.sidx = c->sidx;
     p.scol = c->scol;
+    p.rec = c->rec;
     p.wsum = c->wsum;
     p.image = c->image;
     p.upstream = upstream;

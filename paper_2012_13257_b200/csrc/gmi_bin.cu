@@ -78,22 +78,6 @@ __global__ void k_bbox_init(uint32_t* bbox, unsigned long long* issue, int B) {
 }
 
 // ---------------------------------------------------------------------------
-__global__ void k_count(const float2* __restrict__ pos, int N,
-                        const Geom* __restrict__ geom, int32_t* __restrict__ bins,
-                        int32_t* __restrict__ cellid, int32_t* __restrict__ rank) {
-    const int b = blockIdx.y;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= N) return;
-    const Geom g = geom[b];
-    const float2 v = pos[static_cast<size_t>(b) * N + i];
-    const int cx = cell_of(static_cast<double>(v.x), g.ox, g.cell, g.n_cols);
-    const int cy = cell_of(static_cast<double>(v.y), g.oy, g.cell, g.n_rows);
-    const int bin = cy * g.n_cols + cx;  // bin_grid.cpp:67
-    const int r = atomicAdd(bins + g.bin_off + bin, 1);
-    cellid[static_cast<size_t>(b) * N + i] = bin;
-    rank[static_cast<size_t>(b) * N + i] = r;
-}
-
 __global__ void k_scatter(int N, const Geom* __restrict__ geom,
                           const int32_t* __restrict__ bins,
                           const int32_t* __restrict__ cellid,
@@ -370,6 +354,173 @@ __global__ void k_emit(EmitParams p) {
     if (code) atomicMin(p.issue + b, (static_cast<unsigned long long>(i) << 8) | code);
 }
 
+// Device-side geometry (bin_grid.cpp:45-60 with axis_cells 18-24), the same
+// IEEE f64 operations as host_axis_cells: lets the hot path enqueue the whole
+// binning without a host round trip.  Images whose bbox is not finite (a
+// validation error is pending) get a 1x1 grid so the pipeline stays in
+// bounds until gmi_ctx_synchronize / the sync point reports the error.
+__device__ int dev_axis_cells(double span, double cell, int cap) {
+    const double ideal = ceil(__ddiv_rn(span, cell)) + 2.0;
+    if (!(ideal < static_cast<double>(cap))) return cap;
+    const int v = x86_d2i(ideal);
+    return v > 1 ? v : 1;
+}
+
+__global__ void k_geom(const uint32_t* __restrict__ bbox, int B, double cell, int cap,
+                       int64_t stride, Geom* __restrict__ geom) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const double mnx = ord2f(bbox[4 * b + 0]), mny = ord2f(bbox[4 * b + 1]);
+    const double mxx = ord2f(bbox[4 * b + 2]), mxy = ord2f(bbox[4 * b + 3]);
+    Geom g{};
+    g.cell = cell;
+    const bool ok = mnx <= mxx && mny <= mxy && fabs(mnx) < 1e300 && fabs(mxx) < 1e300 &&
+                    fabs(mny) < 1e300 && fabs(mxy) < 1e300;
+    if (ok) {
+        g.ox = __dsub_rn(mnx, cell);
+        g.oy = __dsub_rn(mny, cell);
+        g.n_cols = dev_axis_cells(__dsub_rn(mxx, mnx), cell, cap);
+        g.n_rows = dev_axis_cells(__dsub_rn(mxy, mny), cell, cap);
+    } else {
+        g.ox = 0.0;
+        g.oy = 0.0;
+        g.n_cols = 1;
+        g.n_rows = 1;
+    }
+    g.capped = (g.n_cols >= cap || g.n_rows >= cap) ? 1 : 0;
+    g.bin_off = static_cast<int64_t>(b) * stride;
+    g.qx0 = static_cast<float>(g.ox);
+    g.qscale = 2.0f;
+    geom[b] = g;
+}
+
+// Boundary ambiguity with fp32 row geometry and a ~2 ulp reciprocal square
+// root: the row crossing's nearest integers are found from s = sqrt(h^2),
+// whose error only matters when mu -+ s is within ~1e-6 of a half-integer,
+// i.e. when both neighbouring integers are ~1/2 away and far outside the
+// 8e-6 r^2 band (same decision as point_ambiguous_f32).
+__device__ __forceinline__ bool point_ambiguous_fast(float mx, float my, float rf, float r2f) {
+    if (!(fabsf(mx) < 1048576.f && fabsf(my) < 1048576.f)) return true;
+    const float tau = kAmbRel * r2f;
+    const float tx = truncf(mx), ty = truncf(my);
+    const float fmu = mx - tx, fmy = my - ty;  // exact
+    const int by = static_cast<int>(ty);
+    const int y0 = static_cast<int>(floorf(my - rf - 0.02f));
+    const int y1 = static_cast<int>(ceilf(my + rf + 0.02f));
+    bool amb = false;
+    for (int y = y0; y <= y1; ++y) {
+        const float dy = static_cast<float>(y - by) - fmy;
+        const float h2f = fmaf(-dy, dy, r2f);
+        const float hc = fmaxf(h2f, 0.f);
+        const float s = hc * rsqrtf(fmaxf(hc, 1e-30f));
+        const float nl = rintf(fmu - s), nr = rintf(fmu + s);
+        const float el = fmaf(nl - fmu, nl - fmu, -h2f);
+        const float er = fmaf(nr - fmu, nr - fmu, -h2f);
+        amb |= (h2f >= -tau) && (fabsf(el) <= tau || fabsf(er) <= tau);
+    }
+    return amb;
+}
+
+// Hot layout straight from the atomic cell ranks (no within-cell ordering:
+// the fast gather canonicalises its own bins and the backward is
+// order-independent): thread per point (4 per thread for memory-level
+// parallelism), coalesced reads of the point, ONE 32-byte record written at
+// bin_start[cell] + rank — (x, y, c0, c1) (c2, c3, idx | ambiguity flag, 0) —
+// plus colour validation (core.cpp:80-92).
+struct ScatterEmitParams {
+    const float2* pos;
+    const float* col;
+    const Geom* geom;
+    const int32_t* bins;
+    const int32_t* cellid;
+    const int32_t* rank;
+    float4* rec;
+    unsigned long long* issue;
+    int N, C;
+    int classify;
+    float rf, r2f;
+};
+
+constexpr int kEmitPer = 4;
+
+__global__ void __launch_bounds__(256) k_scatter_emit(ScatterEmitParams p) {
+    const int b = blockIdx.y;
+    const size_t base = static_cast<size_t>(b) * p.N;
+    const int64_t boff = p.geom[b].bin_off;
+    const int i0 = blockIdx.x * (blockDim.x * kEmitPer) + threadIdx.x;
+    int dst[kEmitPer];
+    float2 v[kEmitPer];
+    float c[kEmitPer][4];
+#pragma unroll
+    for (int u = 0; u < kEmitPer; ++u) {
+        const int i = i0 + u * blockDim.x;
+        dst[u] = -1;
+        if (i < p.N) {
+            dst[u] = p.bins[boff + p.cellid[base + i]] + p.rank[base + i];
+            v[u] = p.pos[base + i];
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) c[u][ch] = ch < p.C ? p.col[(base + i) * p.C + ch] : 0.f;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kEmitPer; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (dst[u] < 0) continue;
+        unsigned code = 0;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+            if (ch < p.C && code == 0) {
+                if (!is_finite_f(c[u][ch])) code = 1;                   // NonFiniteValue
+                else if (c[u][ch] < 0.0f || c[u][ch] > 1.0f) code = 2;  // ColorOutOfRange
+            }
+        }
+        if (code) atomicMin(p.issue + b, (static_cast<unsigned long long>(i) << 8) | code);
+        const bool amb = p.classify && point_ambiguous_fast(v[u].x, v[u].y, p.rf, p.r2f);
+        const uint32_t id = static_cast<uint32_t>(i) | (amb ? kUnsafeBit : 0u);
+        float4* r = p.rec + (base + dst[u]) * 2;
+        r[0] = make_float4(v[u].x, v[u].y, c[u][0], c[u][1]);
+        r[1] = make_float4(c[u][2], c[u][3], __uint_as_float(id), 0.f);
+    }
+}
+
+// k_count with 4 points per thread: 4 independent position loads and cell
+// atomics in flight per thread (the single-point kernel is latency bound).
+__global__ void __launch_bounds__(256) k_count4(const float2* __restrict__ pos, int N,
+                                                const Geom* __restrict__ geom,
+                                                int32_t* __restrict__ bins,
+                                                int32_t* __restrict__ cellid,
+                                                int32_t* __restrict__ rank) {
+    const int b = blockIdx.y;
+    const Geom g = geom[b];
+    const size_t base = static_cast<size_t>(b) * N;
+    const int i0 = blockIdx.x * (blockDim.x * kEmitPer) + threadIdx.x;
+    float2 v[kEmitPer];
+#pragma unroll
+    for (int u = 0; u < kEmitPer; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < N) v[u] = pos[base + i];
+    }
+    int bin[kEmitPer], r[kEmitPer];
+#pragma unroll
+    for (int u = 0; u < kEmitPer; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < N) {
+            const int cx = cell_of(static_cast<double>(v[u].x), g.ox, g.cell, g.n_cols);
+            const int cy = cell_of(static_cast<double>(v[u].y), g.oy, g.cell, g.n_rows);
+            bin[u] = cy * g.n_cols + cx;  // bin_grid.cpp:67
+            r[u] = atomicAdd(bins + g.bin_off + bin[u], 1);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kEmitPer; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < N) {
+            cellid[base + i] = bin[u];
+            rank[base + i] = r[u];
+        }
+    }
+}
+
 }  // namespace
 
 namespace gmi_host {
@@ -382,91 +533,17 @@ int host_axis_cells(double span, double cell, int cap) {
     return std::max(1, v);
 }
 
-void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
-                int cap, bool hot, int32_t* point_index_out,
-                unsigned long long* d_issue) {
-    const int B = c->B, N = c->N;
-    const double cell = c->cutoff;
+// Scan tiles over segments [seg_start[b], seg_start[b] + seg_len[b]).
+static void scan_segments(gmi_ctx* ctx, int32_t* data, const std::vector<int64_t>& seg_start,
+                          const std::vector<int64_t>& seg_len) {
     cudaStream_t st = ctx->stream;
-    const float2* p2 = reinterpret_cast<const float2*>(pos);
-
-    // ---- bbox + position validation -> host (one sync: sizes are data
-    // dependent exactly as in the reference) ----
-    uint32_t* d_bbox = static_cast<uint32_t*>(scratch(ctx, WS_BBOX, sizeof(uint32_t) * 4 * B));
-    k_bbox_init<<<(B + 127) / 128, 128, 0, st>>>(d_bbox, d_issue, B);
-    GMI_LAUNCHED(ctx);
-    {
-        const int per_img = std::max(1, std::min((N + 1023) / 1024,
-                                                 (4 * ctx->num_sms + B - 1) / B));
-        k_bbox_validate<<<dim3(per_img, B), 256, 0, st>>>(p2, N, d_bbox, d_issue);
-        GMI_LAUNCHED(ctx);
-    }
-    std::vector<uint32_t> bbox(4 * B);
-    std::vector<unsigned long long> issue(B);
-    GMI_CUDA(cudaMemcpyAsync(bbox.data(), d_bbox, sizeof(uint32_t) * 4 * B,
-                             cudaMemcpyDeviceToHost, st));
-    GMI_CUDA(cudaMemcpyAsync(issue.data(), d_issue, sizeof(unsigned long long) * B,
-                             cudaMemcpyDeviceToHost, st));
-    host_trace("bin: launched bbox");
-    GMI_CUDA(cudaStreamSynchronize(st));
-    host_trace("bin: bbox sync");
-    for (int b = 0; b < B; ++b) {
-        if (issue[b] != kNoIssue) {
-            const long idx = static_cast<long>(issue[b] >> 8);
-            throw GmiFail{GMI_ERR_NON_FINITE_VALUE,
-                          "non-finite position at index " + std::to_string(idx) +
-                              (B > 1 ? " (image " + std::to_string(b) + ")" : "")};
-        }
-    }
-
-    // ---- geometry (bin_grid.cpp:45-60), f64 on the host (IEEE, same ops) ----
-    c->geom_h.resize(B);
-    int64_t off = 0;
-    int max_bins = 0;
-    for (int b = 0; b < B; ++b) {
-        const double mnx = ord2f(bbox[4 * b + 0]), mny = ord2f(bbox[4 * b + 1]);
-        const double mxx = ord2f(bbox[4 * b + 2]), mxy = ord2f(bbox[4 * b + 3]);
-        gmi_dev::Geom g{};
-        g.cell = cell;
-        g.ox = mnx - cell;
-        g.oy = mny - cell;
-        g.n_cols = host_axis_cells(mxx - mnx, cell, cap);
-        g.n_rows = host_axis_cells(mxy - mny, cell, cap);
-        g.capped = (g.n_cols >= cap || g.n_rows >= cap) ? 1 : 0;
-        g.bin_off = off;
-        g.qx0 = static_cast<float>(g.ox);
-        // fine x-columns: 2 per pixel unless the frame is so wide that the
-        // forward's column tables would overflow (see gmi_forward.cu)
-        g.qscale = 2.0f;
-        off += static_cast<int64_t>(g.n_cols) * g.n_rows + 1;
-        max_bins = std::max(max_bins, g.n_cols * g.n_rows);
-        c->geom_h[b] = g;
-    }
-    c->total_bins = off;
-    c->geom_d = static_cast<gmi_dev::Geom*>(cache_alloc(c, sizeof(gmi_dev::Geom) * B));
-    GMI_CUDA(cudaMemcpyAsync(c->geom_d, c->geom_h.data(), sizeof(gmi_dev::Geom) * B,
-                             cudaMemcpyHostToDevice, st));
-    c->bins = static_cast<int32_t*>(cache_alloc(c, sizeof(int32_t) * off));
-    GMI_CUDA(cudaMemsetAsync(c->bins, 0, sizeof(int32_t) * off, st));
-
-    // ---- count ----
-    const size_t BN = static_cast<size_t>(B) * N;
-    int32_t* cellid = static_cast<int32_t*>(scratch(ctx, WS_CELLID, sizeof(int32_t) * BN));
-    int32_t* rank = static_cast<int32_t*>(scratch(ctx, WS_RANK, sizeof(int32_t) * BN));
-    const dim3 pgrid((N + 255) / 256, B);
-    host_trace("bin: geometry+allocs");
-    k_count<<<pgrid, 256, 0, st>>>(p2, N, c->geom_d, c->bins, cellid, rank);
-    GMI_LAUNCHED(ctx);
-    host_trace("bin: count launched");
-
-    // ---- segmented scan ----
+    const int B = static_cast<int>(seg_start.size());
     std::vector<ScanTile> tiles;
     std::vector<int32_t> seg_off(B + 1, 0);
     for (int b = 0; b < B; ++b) {
-        const int64_t len = static_cast<int64_t>(c->geom_h[b].n_cols) * c->geom_h[b].n_rows + 1;
-        for (int64_t s = 0; s < len; s += kScanTile)
-            tiles.push_back({c->geom_h[b].bin_off + s,
-                             static_cast<int32_t>(std::min<int64_t>(kScanTile, len - s)), b});
+        for (int64_t s = 0; s < seg_len[b]; s += kScanTile)
+            tiles.push_back({seg_start[b] + s,
+                             static_cast<int32_t>(std::min<int64_t>(kScanTile, seg_len[b] - s)), b});
         seg_off[b + 1] = static_cast<int32_t>(tiles.size());
     }
     const int nt = static_cast<int>(tiles.size());
@@ -477,18 +554,136 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
                              cudaMemcpyHostToDevice, st));
     GMI_CUDA(cudaMemcpyAsync(d_segoff, seg_off.data(), sizeof(int32_t) * (B + 1),
                              cudaMemcpyHostToDevice, st));
-    k_scan_reduce<<<nt, kScanThreads, 0, st>>>(c->bins, d_tiles, d_tsum);
+    k_scan_reduce<<<nt, kScanThreads, 0, st>>>(data, d_tiles, d_tsum);
     GMI_LAUNCHED(ctx);
     k_scan_segments<<<B, 1024, 0, st>>>(d_tsum, d_segoff);
     GMI_LAUNCHED(ctx);
-    k_scan_apply<<<nt, kScanThreads, 0, st>>>(c->bins, d_tiles, d_tsum);
+    k_scan_apply<<<nt, kScanThreads, 0, st>>>(data, d_tiles, d_tsum);
     GMI_LAUNCHED(ctx);
+}
 
-    // ---- scatter + per-cell ordering ----
+void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
+                int cap, bool hot, int32_t* point_index_out,
+                unsigned long long* d_issue) {
+    const int B = c->B, N = c->N;
+    const double cell = c->cutoff;
+    cudaStream_t st = ctx->stream;
+    const float2* p2 = reinterpret_cast<const float2*>(pos);
+
+    // ---- bbox + position validation ----
+    uint32_t* d_bbox = static_cast<uint32_t*>(scratch(ctx, WS_BBOX, sizeof(uint32_t) * 4 * B));
+    k_bbox_init<<<(B + 127) / 128, 128, 0, st>>>(d_bbox, d_issue, B);
+    GMI_LAUNCHED(ctx);
+    {
+        const int per_img = std::max(1, std::min((N + 1023) / 1024,
+                                                 (4 * ctx->num_sms + B - 1) / B));
+        k_bbox_validate<<<dim3(per_img, B), 256, 0, st>>>(p2, N, d_bbox, d_issue);
+        GMI_LAUNCHED(ctx);
+    }
+    c->geom_d = static_cast<gmi_dev::Geom*>(cache_alloc(c, sizeof(gmi_dev::Geom) * B));
+    std::vector<int64_t> seg_start(B), seg_len(B);
+    int max_bins = 0;
+    // device geometry (no host round trip) when the frame-derived bin array
+    // stays small; otherwise the exact host geometry with the reference cap
+    const int64_t cells = static_cast<int64_t>(cap) * cap;
+    if (hot && cells <= (int64_t(1) << 22) && cells * B <= (int64_t(1) << 26)) {
+        const int64_t stride = cells + 1;
+        c->geom_h.clear();
+        c->grid_cap = cap;
+        c->grid_stride = stride;
+        k_geom<<<(B + 127) / 128, 128, 0, st>>>(d_bbox, B, cell, cap, stride, c->geom_d);
+        GMI_LAUNCHED(ctx);
+        c->total_bins = stride * B;
+        for (int b = 0; b < B; ++b) {
+            seg_start[b] = b * stride;
+            seg_len[b] = stride;
+        }
+        max_bins = static_cast<int>(cells);
+    } else {
+        if (hot) cap = std::max(cap, 2048);
+        // one sync: sizes are data dependent exactly as in the reference
+        std::vector<uint32_t> bbox(4 * B);
+        std::vector<unsigned long long> issue(B);
+        GMI_CUDA(cudaMemcpyAsync(bbox.data(), d_bbox, sizeof(uint32_t) * 4 * B,
+                                 cudaMemcpyDeviceToHost, st));
+        GMI_CUDA(cudaMemcpyAsync(issue.data(), d_issue, sizeof(unsigned long long) * B,
+                                 cudaMemcpyDeviceToHost, st));
+        GMI_CUDA(cudaStreamSynchronize(st));
+        for (int b = 0; b < B; ++b) {
+            if (issue[b] != kNoIssue) {
+                const long idx = static_cast<long>(issue[b] >> 8);
+                throw GmiFail{GMI_ERR_NON_FINITE_VALUE,
+                              "non-finite position at index " + std::to_string(idx) +
+                                  (B > 1 ? " (image " + std::to_string(b) + ")" : "")};
+            }
+        }
+        // geometry (bin_grid.cpp:45-60), f64 on the host (IEEE, same ops)
+        c->geom_h.resize(B);
+        int64_t off = 0;
+        for (int b = 0; b < B; ++b) {
+            const double mnx = ord2f(bbox[4 * b + 0]), mny = ord2f(bbox[4 * b + 1]);
+            const double mxx = ord2f(bbox[4 * b + 2]), mxy = ord2f(bbox[4 * b + 3]);
+            gmi_dev::Geom g{};
+            g.cell = cell;
+            g.ox = mnx - cell;
+            g.oy = mny - cell;
+            g.n_cols = host_axis_cells(mxx - mnx, cell, cap);
+            g.n_rows = host_axis_cells(mxy - mny, cell, cap);
+            g.capped = (g.n_cols >= cap || g.n_rows >= cap) ? 1 : 0;
+            g.bin_off = off;
+            g.qx0 = static_cast<float>(g.ox);
+            g.qscale = 2.0f;
+            seg_start[b] = off;
+            seg_len[b] = static_cast<int64_t>(g.n_cols) * g.n_rows + 1;
+            off += seg_len[b];
+            max_bins = std::max(max_bins, g.n_cols * g.n_rows);
+            c->geom_h[b] = g;
+        }
+        c->total_bins = off;
+        GMI_CUDA(cudaMemcpyAsync(c->geom_d, c->geom_h.data(), sizeof(gmi_dev::Geom) * B,
+                                 cudaMemcpyHostToDevice, st));
+    }
+    c->bins = static_cast<int32_t*>(cache_alloc(c, sizeof(int32_t) * c->total_bins));
+    GMI_CUDA(cudaMemsetAsync(c->bins, 0, sizeof(int32_t) * c->total_bins, st));
+
+    // ---- count (atomic arrival rank in the cell) + segmented scan ----
+    const size_t BN = static_cast<size_t>(B) * N;
+    int32_t* cellid = static_cast<int32_t*>(scratch(ctx, WS_CELLID, sizeof(int32_t) * BN));
+    int32_t* rank = static_cast<int32_t*>(scratch(ctx, WS_RANK, sizeof(int32_t) * BN));
+    const dim3 pgrid((N + 255) / 256, B);
+    const dim3 pgrid4((N + 256 * kEmitPer - 1) / (256 * kEmitPer), B);
+    k_count4<<<pgrid4, 256, 0, st>>>(p2, N, c->geom_d, c->bins, cellid, rank);
+    GMI_LAUNCHED(ctx);
+    host_trace("bin: count launched");
+    scan_segments(ctx, c->bins, seg_start, seg_len);
+
+    const bool classify = c->wsum64 == nullptr;
+    if (hot && !c->sort_cells) {
+        // fast path: 32-byte records at bin_start + arrival rank
+        ScatterEmitParams e{};
+        e.pos = p2;
+        e.col = col;
+        e.geom = c->geom_d;
+        e.bins = c->bins;
+        e.cellid = cellid;
+        e.rank = rank;
+        e.rec = c->rec;
+        e.issue = d_issue;
+        e.N = N;
+        e.C = c->C;
+        e.classify = classify ? 1 : 0;
+        e.rf = static_cast<float>(c->cutoff);
+        e.r2f = static_cast<float>(c->cutoff * c->cutoff);
+        k_scatter_emit<<<pgrid4, 256, 0, st>>>(e);
+        GMI_LAUNCHED(ctx);
+        host_trace("bin: scatter_emit launched");
+        return;
+    }
+
+    // ---- scatter + per-cell index order (the reference's point_index) ----
     int32_t* tmp = static_cast<int32_t*>(scratch(ctx, WS_TMP, sizeof(int32_t) * BN));
     k_scatter<<<pgrid, 256, 0, st>>>(N, c->geom_d, c->bins, cellid, rank, tmp);
     GMI_LAUNCHED(ctx);
-
     int2* d_big = static_cast<int2*>(scratch(ctx, WS_BIG, sizeof(int2) * std::max<size_t>(1, BN / (kSmallCell + 1) + 1)));
     int32_t* d_bigcount = static_cast<int32_t*>(scratch(ctx, WS_BIGCOUNT, sizeof(int32_t)));
     GMI_CUDA(cudaMemsetAsync(d_bigcount, 0, sizeof(int32_t), st));
@@ -514,7 +709,7 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
         e.N = N;
         e.C = c->C;
         // f64 weight mode decides every pair in f64: no classification needed
-        e.classify = c->wsum64 == nullptr ? 1 : 0;
+        e.classify = classify ? 1 : 0;
         e.rf = static_cast<float>(c->cutoff);
         e.r2f = static_cast<float>(c->cutoff * c->cutoff);
         k_emit<<<pgrid, 256, 0, st>>>(e);

@@ -65,11 +65,15 @@ int check_points(const float* pos, const float* col, int B, int N, int C) {
 // is covered without clamping (the 2048 cap puts >1M
 // points in one bin at 8192^2 / r=3).  When the reference grid is not capped
 // the two are identical.
-int hot_cap(const gmi_config* cfg) {
+//
+// The device-geometry path (no host round trip) caps at the frame's own need:
+// points inside the frame never reach it, so the grid is still the
+// reference's; only point sets reaching far outside the frame get clamped
+// edge cells (exact, see gmi_bin.cu / nearest_exact).
+int frame_cells(const gmi_config* cfg) {
     const double span = std::max(cfg->width, cfg->height) + 2.0 * cfg->cutoff_radius;
     const double need = std::ceil(span / cfg->cutoff_radius) + 8.0;
-    const double cap = std::min(8192.0, std::max(2048.0, need));
-    return static_cast<int>(cap);
+    return static_cast<int>(std::min(8192.0, need));
 }
 
 void ensure_issue(gmi_ctx* ctx, int B) {
@@ -168,10 +172,6 @@ int do_forward(gmi_ctx* ctx, const float* pos, const float* col, int B, int N,
     c->force_generic = std::getenv("GMI_GENERIC") != nullptr;
     const size_t BN = static_cast<size_t>(B) * N;
     const size_t BHW = static_cast<size_t>(B) * c->H * c->W;
-    c->sx = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN));
-    c->sy = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN));
-    c->sidx = static_cast<int32_t*>(gmi_host::cache_alloc(c, sizeof(int32_t) * BN));
-    c->scol = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN * C));
     c->wsum = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BHW));
     // f64 weight mode beyond 6 sigma (see gmi_forward.cu)
     if (cfg->cutoff_radius > 6.0 * cfg->sigma)
@@ -186,7 +186,19 @@ int do_forward(gmi_ctx* ctx, const float* pos, const float* col, int B, int N,
     host_trace("fwd: allocs");
     {
         PhaseScope ph(ctx, 0);
-        gmi_host::bin_points(ctx, c, pos, col, hot_cap(cfg), true, nullptr, d_issue);
+        // fast gather: unordered cells and the 32-byte record layout;
+        // otherwise index-ordered cells in SoA (the generic gather's order)
+        const bool fast = gmi_host::gather_fast_ok(c);
+        c->sort_cells = !fast;
+        if (fast) {
+            c->rec = static_cast<float4*>(gmi_host::cache_alloc(c, sizeof(float4) * 2 * BN));
+        } else {
+            c->sx = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN));
+            c->sy = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN));
+            c->sidx = static_cast<int32_t*>(gmi_host::cache_alloc(c, sizeof(int32_t) * BN));
+            c->scol = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN * C));
+        }
+        gmi_host::bin_points(ctx, c, pos, col, frame_cells(cfg), true, nullptr, d_issue);
     }
     {
         PhaseScope ph(ctx, 1);

@@ -235,6 +235,7 @@ struct SpecParams {
     const float* sy;
     const int32_t* sidx;
     const float* scol;   // [B][C][N]
+    const float4* rec;   // fast layout [B][N][2] (sx/sy/sidx null)
     const float* col;    // original colours [B][N][C]
     const float* wsum;
     int N, C, W, H;
@@ -247,6 +248,20 @@ struct SpecParams {
     int special_cap;
     int overflow_scan;   // 1: list overflowed — scan wsum for specials
 };
+
+// position and original index of hot-layout slot k (either layout)
+__device__ __forceinline__ void point_at(const SpecParams& p, size_t k, float& x, float& y, int& i) {
+    if (p.rec) {
+        const float4 ra = p.rec[k * 2];
+        x = ra.x;
+        y = ra.y;
+        i = static_cast<int>(__float_as_uint(p.rec[k * 2 + 1].z) & 0x7fffffffu);
+    } else {
+        x = p.sx[k];
+        y = p.sy[k];
+        i = p.sidx[k] & 0x7fffffff;
+    }
+}
 
 __device__ __forceinline__ void warp_argmin(double& d2, int& idx) {
     for (int o = 16; o > 0; o >>= 1) {
@@ -272,9 +287,10 @@ __device__ int nearest_exact(const SpecParams& p, const Geom& g, int b,
         const int64_t bin = g.bin_off + static_cast<int64_t>(gy) * g.n_cols + gx;
         const int s = p.bins[bin], e = p.bins[bin + 1];
         for (int k = s + lane; k < e; k += 32) {
-            const double d2 = d2_ref(qx, qy, static_cast<double>(p.sx[base + k]),
-                                     static_cast<double>(p.sy[base + k]));
-            const int i = p.sidx[base + k] & 0x7fffffff;
+            float px, py;
+            int i;
+            point_at(p, base + k, px, py, i);
+            const double d2 = d2_ref(qx, qy, static_cast<double>(px), static_cast<double>(py));
             if (d2 < best || (d2 == best && i < bi)) {
                 best = d2;
                 bi = i;
@@ -284,9 +300,10 @@ __device__ int nearest_exact(const SpecParams& p, const Geom& g, int b,
     if (g.capped) {
         // clamped edge cells break ring pruning: brute force
         for (int k = lane; k < p.N; k += 32) {
-            const double d2 = d2_ref(qx, qy, static_cast<double>(p.sx[base + k]),
-                                     static_cast<double>(p.sy[base + k]));
-            const int i = p.sidx[base + k] & 0x7fffffff;
+            float px, py;
+            int i;
+            point_at(p, base + k, px, py, i);
+            const double d2 = d2_ref(qx, qy, static_cast<double>(px), static_cast<double>(py));
             if (d2 < best || (d2 == best && i < bi)) {
                 best = d2;
                 bi = i;
@@ -337,6 +354,7 @@ __device__ void special_pixel(const SpecParams& p, int b, int pix, int slot) {
     float* out = p.image + (static_cast<size_t>(b) * p.H * p.W + pix) * p.C;
     int nearest = -1;
     if (p.fallback == GMI_FALLBACK_NEAREST) nearest = nearest_exact(p, g, b, qx, qy);
+    if (nearest == INT32_MAX) nearest = -1;  // no finite point (a validation error is pending)
     if (lane == 0) {
         for (int c = 0; c < p.C; ++c)
             out[c] = nearest >= 0 ? p.col[(base + nearest) * p.C + c] : 0.0f;
@@ -387,7 +405,7 @@ static FwdParams fwd_params(const gmi_cache* c, float* image, int32_t* counts) {
 
 void launch_forward(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts) {
     // fast path (gmi_gather.cu) unless f64 weights / C > 4 / very wide radius
-    if (!c->force_generic && launch_gather_fast(ctx, c, image, counts)) return;
+    if (launch_gather_fast(ctx, c, image, counts)) return;
     const FwdParams p = fwd_params(c, image, counts);
     const int tiles_x = (c->W + kTW - 1) / kTW;
     const int tiles_y = (c->H + kTH - 1) / kTH;
@@ -412,6 +430,7 @@ void launch_special_forward(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* c
     p.sy = c->sy;
     p.sidx = c->sidx;
     p.scol = c->scol;
+    p.rec = c->rec;
     p.col = c->col;
     p.wsum = c->wsum;
     p.N = c->N;

@@ -67,10 +67,7 @@ struct SmemGather {
 struct GatherParams {
     const Geom* geom;
     const int32_t* bins;
-    const float* sx;
-    const float* sy;
-    const int32_t* sidx;
-    const float* scol;  // [B][C][N]
+    const float4* rec;  // [B][N][2]: (x, y, c0, c1) (c2, c3, idx|flag, 0)
     int N, C, W, H;
     int ncol, nyb, dyb, rc;   // bin geometry (see launch_gather_fast)
     double r64, r2_64;
@@ -227,8 +224,9 @@ k_gather(GatherParams p) {
             const int gs = S.run_g[rs], rb = S.run_beg[rs], len = S.run_beg[rs + 1] - rb;
             for (int j = lane; j < len; j += 32) {
                 const int slot = gs + j;
-                const float mx = p.sx[base + slot], my = p.sy[base + slot];
-                const bool flag = (static_cast<uint32_t>(p.sidx[base + slot]) & kUnsafeBit) != 0;
+                const float4 ra = p.rec[(base + slot) * 2];
+                const float mx = ra.x, my = ra.y;
+                const bool flag = (__float_as_uint(p.rec[(base + slot) * 2 + 1].z) & kUnsafeBit) != 0;
                 int key = -1;
                 const double dx = static_cast<double>(mx) - cxo;
                 const double dy = static_cast<double>(my) - cyo;
@@ -285,14 +283,11 @@ k_gather(GatherParams p) {
             if (key < 0) continue;
             const int pos = atomicSub(&S.bin[key], 1) - 1;
             const int slot = S.u.st.slot[k];
-            float c[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int ch = 0; ch < CC; ++ch)
-                if (ch < nch)
-                    c[ch] = p.scol[(static_cast<size_t>(b) * p.C + ch0 + ch) * p.N + slot];
-            S.A[pos] = make_float4(p.sx[base + slot], p.sy[base + slot], c[0], c[1]);
-            if (CC > 2) S.Bc[pos] = f2(c[2], c[3]);
-            S.idx[pos] = p.sidx[base + slot] & 0x7fffffff;
+            const float4 ra = p.rec[(base + slot) * 2];
+            const float4 rb = p.rec[(base + slot) * 2 + 1];
+            S.A[pos] = ra;
+            if (CC > 2) S.Bc[pos] = f2(rb.x, rb.y);
+            S.idx[pos] = static_cast<int>(__float_as_uint(rb.z) & 0x7fffffffu);
         }
         __syncthreads();
 
@@ -487,26 +482,34 @@ void launch_cc(gmi_ctx* ctx, const GatherParams& p, dim3 grid) {
 
 namespace gmi_host {
 
+static void gather_geometry(double r, int& rc, int& ncol, int& dyb, int& nyb) {
+    // columns: floor(mu_x - (x0 - rc)), rc = ceil(r); lane windows are the
+    // columns of (xa - r, xa + 1 + r), so ncol covers the last lane's
+    rc = static_cast<int>(std::ceil(r));
+    ncol = static_cast<int>(std::ceil(static_cast<double>(kTW - 2 + rc + 1) + r));
+    // row pairs: floor((mu_y - (y0 - r)) / 2); warp w reads [w, w + dyb]
+    dyb = static_cast<int>(std::ceil(0.5 + r)) - 1;
+    nyb = kNW + dyb;
+}
+
+// The fast gather applies: fp32 weight mode and a bin table that fits.
+bool gather_fast_ok(const gmi_cache* c) {
+    if (c->wsum64 != nullptr || c->force_generic || c->C > 4) return false;
+    int rc, ncol, dyb, nyb;
+    gather_geometry(c->cutoff, rc, ncol, dyb, nyb);
+    return ncol < kColMax && ncol * nyb + 1 <= kBinMax;
+}
+
 // Returns false when the configuration needs the generic gather
 // (f64 weight mode, or a radius whose bin table exceeds the staging tables).
 bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts) {
-    if (c->wsum64 != nullptr) return false;
+    if (!gather_fast_ok(c)) return false;
     const double r = c->cutoff;
     GatherParams p{};
-    // columns: floor(mu_x - (x0 - rc)), rc = ceil(r); lane windows are the
-    // columns of (xa - r, xa + 1 + r), so ncol covers the last lane's
-    p.rc = static_cast<int>(std::ceil(r));
-    p.ncol = static_cast<int>(std::ceil(static_cast<double>(kTW - 2 + p.rc + 1) + r));
-    // row pairs: floor((mu_y - (y0 - r)) / 2); warp w reads [w, w + dyb]
-    p.dyb = static_cast<int>(std::ceil(0.5 + r)) - 1;
-    p.nyb = kNW + p.dyb;
-    if (p.ncol >= kColMax || p.ncol * p.nyb + 1 > kBinMax) return false;
+    gather_geometry(r, p.rc, p.ncol, p.dyb, p.nyb);
     p.geom = c->geom_d;
     p.bins = c->bins;
-    p.sx = c->sx;
-    p.sy = c->sy;
-    p.sidx = c->sidx;
-    p.scol = c->scol;
+    p.rec = c->rec;
     p.N = c->N;
     p.C = c->C;
     p.W = c->W;

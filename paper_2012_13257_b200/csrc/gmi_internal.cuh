@@ -125,11 +125,20 @@ struct gmi_cache {
     gmi_dev::Geom* geom_d = nullptr;
     int32_t* bins = nullptr;  // concatenated bin_start per image
     int64_t total_bins = 0;
+    // device-geometry binning: image b's bin_start at b * grid_stride, grid
+    // dims <= grid_cap (geom_h is empty; the geometry lives only in geom_d)
+    int grid_cap = 0;
+    int64_t grid_stride = 0;
+    bool sort_cells = true;   // within-cell index order (generic gather)
     // hot layout (sorted by cell, then fine x-column, then index)
     float* sx = nullptr;      // [B][N]
     float* sy = nullptr;      // [B][N]
     int32_t* sidx = nullptr;  // [B][N] original point index
     float* scol = nullptr;    // [B][C][N] channel-planar
+    // fast-path hot layout (C <= 4, fp32 weights): one 32-byte record per
+    // point in bin order, (x, y, c0, c1) (c2, c3, idx|flag bits, 0); replaces
+    // sx/sy/sidx/scol, which stay null
+    float4* rec = nullptr;    // [B][N][2]
     // per pixel
     float* wsum = nullptr;    // [B][H][W]; 0 => special pixel
     double* wsum64 = nullptr; // [B][H][W] f64 normaliser (precise mode only)
@@ -167,6 +176,7 @@ int host_axis_cells(double span, double cell, int cap);
 // ---- forward (gmi_forward.cu) ----
 void launch_forward(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts);
 bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts);
+bool gather_fast_ok(const gmi_cache* c);
 void launch_special_forward(gmi_ctx* ctx, gmi_cache* c, float* image,
                             int32_t* counts);
 
