@@ -83,7 +83,7 @@ struct GatherParams {
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
 template <int CC, bool kCount>
-__global__ void __launch_bounds__(kNT, 3)
+__global__ void __launch_bounds__(kNT, 4)
 k_gather(GatherParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SmemGather<CC>& S = *reinterpret_cast<SmemGather<CC>*>(smem_raw);
@@ -132,11 +132,10 @@ k_gather(GatherParams p) {
 
     if (warp == 0) {
         // the f64 cell rectangle (four lanes in parallel)
-        int cv = 0;
-        if (lane == 0) cv = cell_of(xlo, g.ox, g.cell, g.n_cols);
-        if (lane == 1) cv = cell_of(xhi, g.ox, g.cell, g.n_cols);
-        if (lane == 2) cv = cell_of(ylo, g.oy, g.cell, g.n_rows);
-        if (lane == 3) cv = cell_of(yhi, g.oy, g.cell, g.n_rows);
+        // one convergent call: lane 0/1 -> x bounds, lane 2/3 -> y bounds
+        const bool ax = lane < 2;
+        const int cv = cell_of(ax ? ((lane & 1) ? xhi : xlo) : ((lane & 1) ? yhi : ylo),
+                               ax ? g.ox : g.oy, g.cell, ax ? g.n_cols : g.n_rows);
         const int cx0 = __shfl_sync(0xffffffffu, cv, 0), cx1 = __shfl_sync(0xffffffffu, cv, 1);
         const int cy0 = __shfl_sync(0xffffffffu, cv, 2), cy1 = __shfl_sync(0xffffffffu, cv, 3);
         // common case: <= 32 cell rows and <= kCap candidates -> one chunk,
