@@ -42,6 +42,7 @@ constexpr int kCap = 1024;         // staged candidates per chunk
 constexpr int kRsMax = 32;         // cell-row runs per chunk
 constexpr int kColMax = 128;       // 1-px columns across the tile's reach
 constexpr int kBinMax = 2048;      // (column, row-pair) bins (+1 flag bin)
+constexpr int kMultiCap = kNW * (kColMax + 1);  // multi-bin list, shares wcs
 
 template <int CC>
 struct SmemGather {
@@ -56,10 +57,14 @@ struct SmemGather {
         uint16_t wl[kNW][kCap];            // per-warp column-major lists
     } u;
     int bin[kBinMax + 2];                  // counts -> inclusive ends -> starts
-    uint16_t wcs[kNW][kColMax + 1];        // per-warp column starts in wl
+    union {
+        uint16_t wcs[kNW][kColMax + 1];    // per-warp column starts in wl
+        uint16_t multi[kMultiCap];         // bins with >= 2 candidates (B..D)
+    } v;
     int run_beg[kRsMax + 1];
     int run_g[kRsMax];
     int scan_w[kNW];
+    int n_multi;
     int n_runs, cur_cy, cur_off, done, pre;
     int cx0, cx1, cy1;
 };
@@ -213,6 +218,7 @@ k_gather(GatherParams p) {
             S.done = cy > cy1;
         }
         for (int k = tid; k <= nbins + 1; k += kNT) S.bin[k] = 0;
+        if (tid == 0) S.n_multi = 0;
         __syncthreads();
         const int n_runs = S.n_runs;
         if (n_runs == 0) break;
@@ -271,6 +277,11 @@ k_gather(GatherParams p) {
             for (int j = 0; j < kPer; ++j) {
                 run += v[j];
                 if (k0 + j < nb) S.bin[k0 + j] = run;
+                // bins holding 2+ candidates need the canonical-order pass
+                if (v[j] > 1) {
+                    const int m = atomicAdd(&S.n_multi, 1);
+                    if (m < kMultiCap) S.v.multi[m] = static_cast<uint16_t>(k0 + j);
+                }
             }
             if (tid == kNT - 1) S.bin[nb] = run;  // total kept
         }
@@ -291,7 +302,10 @@ k_gather(GatherParams p) {
         __syncthreads();
 
         // ---- D: canonical order inside each bin (ascending original index) ----
-        for (int k = tid; k <= nbins; k += kNT) {
+        const int n_multi = S.n_multi;
+        const int n_sort = n_multi <= kMultiCap ? n_multi : nbins + 1;  // overflow: every bin
+        for (int m = tid; m < n_sort; m += kNT) {
+            const int k = n_multi <= kMultiCap ? S.v.multi[m] : m;
             const int s = S.bin[k], e = S.bin[k + 1];
             for (int i = s + 1; i < e; ++i) {
                 const int vi = S.idx[i];
@@ -315,8 +329,9 @@ k_gather(GatherParams p) {
         // ---- E: this warp's column-major list (row-pair bins [w, w+dyb]) ----
         {
             const int yb0 = warp, yb1 = min(warp + p.dyb, nyb - 1);
+            // columns [c0, c1) of this lane: ncol spread evenly over the warp
             constexpr int kCpl = kColMax / 32;
-            const int c0 = lane * kCpl;
+            const int c0 = (lane * ncol) >> 5, c1 = ((lane + 1) * ncol) >> 5;
             int ps[kCpl], pl[kCpl];
             int s = 0;
 #pragma unroll
@@ -324,7 +339,7 @@ k_gather(GatherParams p) {
                 const int q = c0 + j;
                 ps[j] = 0;
                 pl[j] = 0;
-                if (q < ncol) {
+                if (q < c1) {
                     ps[j] = S.bin[q * nyb + yb0];
                     pl[j] = S.bin[q * nyb + yb1 + 1] - ps[j];
                 }
@@ -340,16 +355,17 @@ k_gather(GatherParams p) {
 #pragma unroll
             for (int j = 0; j < kCpl; ++j) {
                 const int q = c0 + j;
-                if (q <= ncol) S.wcs[warp][q] = static_cast<uint16_t>(at);
+                if (q < c1) S.v.wcs[warp][q] = static_cast<uint16_t>(at);
                 for (int e = 0; e < pl[j]; ++e) wl[at + e] = static_cast<uint16_t>(ps[j] + e);
                 at += pl[j];
             }
+            if (lane == 31) S.v.wcs[warp][ncol] = static_cast<uint16_t>(at);
         }
         __syncwarp();
 
         // ---- gather: 4 pixels per candidate, f32x2 ----
         {
-            const int ts = S.wcs[warp][q_lo], te = S.wcs[warp][q_hi + 1];
+            const int ts = S.v.wcs[warp][q_lo], te = S.v.wcs[warp][q_hi + 1];
             const uint16_t* lst = S.u.wl[warp];
 #pragma unroll 2
             for (int t = ts; t < te; ++t) {
@@ -434,11 +450,39 @@ k_gather(GatherParams p) {
     }
 
     // ---- fused normalisation + store (engine.cpp:74-100) ----
+    // out = num / W with one Newton step; W kept for the backward
+    auto norm = [](float num, float w, float inv) {
+        const float q0 = num * inv;
+        return fmaf(fmaf(-q0, w, num), inv, q0);
+    };
 #pragma unroll
     for (int py = 0; py < 2; ++py) {
+        const int qy = ya + py;
+        const float2 wr = py ? Wb : Wa;
+        // both pixels inside and non-fallback, C == CC, 8-byte aligned: 64-bit
+        // stores of the pixel pair
+        const size_t bpr = (static_cast<size_t>(b) * p.H + qy) * p.W + xa;
+        const bool al = ((reinterpret_cast<uintptr_t>(p.image + bpr * CC) |
+                          reinterpret_cast<uintptr_t>(p.wsum + bpr)) & 7) == 0;
+        if (qy < p.H && xa + 1 < p.W && wr.x > 0.f && wr.y > 0.f && nch == p.C && !kCount && al) {
+            const size_t bp = bpr;
+            const float ia = 1.0f / wr.x, ib = 1.0f / wr.y;
+            float o[2 * CC];
+#pragma unroll
+            for (int c = 0; c < CC; ++c) {
+                const float2 nm = py ? Nb[c] : Na[c];
+                o[c] = norm(nm.x, wr.x, ia);
+                o[CC + c] = norm(nm.y, wr.y, ib);
+            }
+            float2* out2 = reinterpret_cast<float2*>(p.image + bp * CC);
+#pragma unroll
+            for (int j = 0; j < CC; ++j) out2[j] = f2(o[2 * j], o[2 * j + 1]);
+            *reinterpret_cast<float2*>(p.wsum + bp) = wr;
+            continue;
+        }
 #pragma unroll
         for (int px = 0; px < 2; ++px) {
-            const int qx = xa + px, qy = ya + py;
+            const int qx = xa + px;
             if (qx >= p.W || qy >= p.H) continue;
             const float w = py ? (px ? Wb.y : Wb.x) : (px ? Wa.y : Wa.x);
             const size_t bp = (static_cast<size_t>(b) * p.H + qy) * p.W + qx;
