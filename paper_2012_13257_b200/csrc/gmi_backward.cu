@@ -103,7 +103,6 @@ k_backward_points(BwdParams p) {
     __shared__ int s_rung[kRunMax];      // first slot of each run
     __shared__ float s_red[4][kThreads / 32];
     __shared__ int s_region[5];
-    __shared__ int s_next;
 
     // ---- image / cell block of this CTA ----
     int b = 0;
@@ -165,7 +164,35 @@ k_backward_points(BwdParams p) {
         return s_rung[lo] + (k - s_run[lo]);
     };
 
-    // ---- pixel region reached by the block's points (bbox + r) ----
+    // ---- pixel region reached by the block's points ----
+    // Uncapped grids: the block's cells bound its points' positions exactly
+    // (cell_of = floor((v - origin) / cell), no clamping in use), so the
+    // region is the cell rectangle grown by r — no pass over the points.
+    // Capped grids (clamped edge cells) or an oversized rectangle: the
+    // points' bbox grown by r.
+    if (tid == 0) {
+        s_region[4] = -2;
+        if (!g.capped) {
+            const double pad = p.r64 + 1.0;
+            const int x0 = max(0, static_cast<int>(floor(g.ox + cx0 * g.cell - pad))) & ~1;
+            const int y0 = max(0, static_cast<int>(floor(g.oy + cy0 * g.cell - pad)));
+            const int x1 = min(p.W - 1, static_cast<int>(ceil(g.ox + cx1 * g.cell + pad))) | 1;
+            const int y1 = min(p.H - 1, static_cast<int>(ceil(g.oy + cy1 * g.cell + pad)));
+            const long npairs = (x1 >= x0) ? (x1 - x0 + 1) / 2 : 0;
+            const long area = (y1 >= y0) ? npairs * (y1 - y0 + 1) : 0;
+            if (area <= 0) {
+                s_region[4] = -1;
+            } else if (area * L::kF4 * static_cast<long>(sizeof(float4)) <= kSmemBudget) {
+                s_region[0] = x0;
+                s_region[1] = y0;
+                s_region[2] = x1;
+                s_region[3] = y1;
+                s_region[4] = 1;
+            }
+        }
+    }
+    __syncthreads();
+    if (s_region[4] == -2) {
     float mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
     for (int k = tid; k < total; k += kThreads) {
         const int s = slot_of(k);
@@ -222,6 +249,7 @@ k_backward_points(BwdParams p) {
                           : (area > 0 ? 0 : -1);
     }
     __syncthreads();
+    }
     const int rx0 = s_region[0], ry0 = s_region[1], rx1 = s_region[2], ry1 = s_region[3];
     const int mode = s_region[4];
     if (mode < 0) {
@@ -245,6 +273,7 @@ k_backward_points(BwdParams p) {
     if (staged) {
         // 8-byte alignment of a pixel pair in W / upstream / image rows
         const bool vec = (p.W % 2 == 0) && (CG == p.C);
+#pragma unroll 2
         for (int k = tid; k < area; k += kThreads) {
             const int row = k / npairs;
             const int pp = k - row * npairs, yy = ry0 + row;
@@ -298,25 +327,34 @@ k_backward_points(BwdParams p) {
     const double r2_64 = p.r2_64;
     const int xmin = max(rx0, 0), xmax = min(rx1, p.W - 1);
     const float2 nk2 = f2(nk, nk), two = f2(2.f, 2.f);
-    // dynamic warp tasks of 32 consecutive points (bin order keeps a warp's
-    // points adjacent): balances the CTA's warps without idle tails
-    if (tid == 0) s_next = 0;
-    __syncthreads();
-    while (true) {
-        int kb = 0;
-        if (lane == 0) kb = atomicAdd(&s_next, 32);
-        kb = __shfl_sync(0xffffffffu, kb, 0);
-        if (kb >= total) break;
+    // warp tasks of 32 consecutive points (bin order keeps a warp's points
+    // adjacent), dealt round-robin; the next task's record is prefetched
+    const int warp = tid >> 5;
+    float4 nra = make_float4(0.f, 0.f, 0.f, 0.f), nrb = nra;
+    int ns = 0;
+    if (p.rec && warp * 32 + lane < total) {
+        ns = slot_of(warp * 32 + lane);
+        nra = p.rec[(base + ns) * 2];
+        nrb = p.rec[(base + ns) * 2 + 1];
+    }
+    for (int kb = warp * 32; kb < total; kb += kThreads) {
         const int k = kb + lane;
+        const float4 cra = nra, crb = nrb;
+        const int cs = ns;
+        if (p.rec && k + kThreads < total) {
+            ns = slot_of(k + kThreads);
+            nra = p.rec[(base + ns) * 2];
+            nrb = p.rec[(base + ns) * 2 + 1];
+        }
         if (k >= total) continue;
-        const int s = slot_of(k);
+        const int s = p.rec ? cs : slot_of(k);
         float mx, my;
         uint32_t raw;
         float cc[CG];
         if (p.rec) {
             // fast layout: C <= 4, one channel group
-            const float4 ra = p.rec[(base + s) * 2];
-            const float4 rb = p.rec[(base + s) * 2 + 1];
+            const float4 ra = cra;
+            const float4 rb = crb;
             mx = ra.x;
             my = ra.y;
             raw = __float_as_uint(rb.z);
