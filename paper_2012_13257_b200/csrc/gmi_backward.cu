@@ -449,7 +449,7 @@ k_backward_points(BwdParams p) {
             const float2 ey2 = f2(ey, ey), mmx = f2(-mx, -mx);
             float2 gyr2 = f2(0.f, 0.f);
             const float4* pr = s_pair + (y - ry0) * npairs + ((xs - rx0) >> 1);
-#pragma unroll 2
+#pragma unroll 1
             for (int j = 0; j < np; ++j) {
                 float4 q4[L::kF4];
 #pragma unroll
