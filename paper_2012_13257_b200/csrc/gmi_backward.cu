@@ -273,10 +273,12 @@ k_backward_points(BwdParams p) {
     if (staged) {
         // 8-byte alignment of a pixel pair in W / upstream / image rows
         const bool vec = (p.W % 2 == 0) && (CG == p.C);
+        // rows by warps, pixel pairs by lanes (coalesced, no index division)
+        const int nrows = ry1 - ry0 + 1;
+        for (int row = tid >> 5; row < nrows; row += kThreads / 32)
 #pragma unroll 2
-        for (int k = tid; k < area; k += kThreads) {
-            const int row = k / npairs;
-            const int pp = k - row * npairs, yy = ry0 + row;
+        for (int pp = lane; pp < npairs; pp += 32) {
+            const int k = row * npairs + pp, yy = ry0 + row;
             const int xa = rx0 + 2 * pp;
             float ua[CG], ub[CG], va = 0.f, vb = 0.f;
             if (vec && xa >= 0 && xa + 1 < p.W && yy < p.H) {
@@ -387,18 +389,24 @@ k_backward_points(BwdParams p) {
         const int ya = max(ry0, static_cast<int>(ceilf(my - rf - pad)));
         const int yb = min(ry1, static_cast<int>(floorf(my + rf + pad)));
 
-        for (int y = ya; y <= yb; ++y) {
+        float yf = static_cast<float>(ya);  // exact row coordinate
+        for (int y = ya; y <= yb; ++y, yf += 1.0f) {
             float dy;
             int xl, xr;
             if (!unsafe) {
-                // safe point: fp32 row geometry decides the reference's ball
-                dy = static_cast<float>(y - by) - fmy;
+                // safe point: fp32 row geometry decides the reference's ball;
+                // dy = y - my is the forward's own operation (bit-identical)
+                dy = yf - my;
                 const float h2f = fmaf(-dy, dy, r2f);
                 if (h2f < 0.f) continue;
                 // ~2 ulp: a safe point's row ends are >= 8e-6 r^2 from the ball
                 const float sq = h2f * rsqrtf(fmaxf(h2f, 1e-30f));
-                xl = bx + static_cast<int>(ceilf(fmu - sq));
-                xr = bx + static_cast<int>(floorf(fmu + sq));
+                // ceil / floor of small values by directed-rounding adds of
+                // 1.5 * 2^23 (FMA pipe, no conversion on the XU pipe)
+                constexpr float kMagic = 12582912.0f;
+                constexpr int kMagicBits = 0x4B400000;
+                xl = bx + (__float_as_int(__fadd_ru(fmu - sq, kMagic)) - kMagicBits);
+                xr = bx + (__float_as_int(__fadd_rd(fmu + sq, kMagic)) - kMagicBits);
             } else {
                 const double dy64 = __dsub_rn(static_cast<double>(y), static_cast<double>(my));
                 const double h2 = __dsub_rn(r2_64, __dmul_rn(dy64, dy64));
