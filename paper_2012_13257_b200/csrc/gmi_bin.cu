@@ -407,16 +407,29 @@ __device__ __forceinline__ bool point_ambiguous_fast(float mx, float my, float r
     const int by = static_cast<int>(ty);
     const int y0 = static_cast<int>(floorf(my - rf - 0.02f));
     const int y1 = static_cast<int>(ceilf(my + rf + 0.02f));
+    // two rows per step in f32x2; nearest integers by round-to-nearest adds
+    // of 1.5 * 2^23 (|values| < 2^22), no conversions on the XU pipe
+    constexpr float kM = 12582912.0f;
+    const float2 fm2 = make_float2(fmu, fmu), mf2 = make_float2(-fmu, -fmu);
+    const float2 M2 = make_float2(kM, kM), nM2 = make_float2(-kM, -kM);
+    float2 dy = make_float2(static_cast<float>(y0 - by) - fmy, static_cast<float>(y0 + 1 - by) - fmy);
+    const float2 two = make_float2(2.f, 2.f), r2 = make_float2(r2f, r2f);
     bool amb = false;
-    for (int y = y0; y <= y1; ++y) {
-        const float dy = static_cast<float>(y - by) - fmy;
-        const float h2f = fmaf(-dy, dy, r2f);
-        const float hc = fmaxf(h2f, 0.f);
-        const float s = hc * rsqrtf(fmaxf(hc, 1e-30f));
-        const float nl = rintf(fmu - s), nr = rintf(fmu + s);
-        const float el = fmaf(nl - fmu, nl - fmu, -h2f);
-        const float er = fmaf(nr - fmu, nr - fmu, -h2f);
-        amb |= (h2f >= -tau) && (fabsf(el) <= tau || fabsf(er) <= tau);
+    for (int y = y0; y <= y1; y += 2) {
+        const float2 h2 = __ffma2_rn(make_float2(-dy.x, -dy.y), dy, r2);
+        const float hx = fmaxf(h2.x, 0.f), hy = fmaxf(h2.y, 0.f);
+        const float2 sq = __fmul2_rn(make_float2(hx, hy),
+                                     make_float2(rsqrtf(fmaxf(hx, 1e-30f)), rsqrtf(fmaxf(hy, 1e-30f))));
+        const float2 lo = __fadd2_rn(fm2, make_float2(-sq.x, -sq.y));
+        const float2 hi = __fadd2_rn(fm2, sq);
+        const float2 nl = __fadd2_rn(__fadd2_rn(lo, M2), nM2);  // rint
+        const float2 nr = __fadd2_rn(__fadd2_rn(hi, M2), nM2);
+        const float2 dl = __fadd2_rn(nl, mf2), dr = __fadd2_rn(nr, mf2);
+        const float2 el = __ffma2_rn(dl, dl, make_float2(-h2.x, -h2.y));
+        const float2 er = __ffma2_rn(dr, dr, make_float2(-h2.x, -h2.y));
+        amb |= (h2.x >= -tau) && (fabsf(el.x) <= tau || fabsf(er.x) <= tau);
+        amb |= (y + 1 <= y1) && (h2.y >= -tau) && (fabsf(el.y) <= tau || fabsf(er.y) <= tau);
+        dy = __fadd2_rn(dy, two);
     }
     return amb;
 }
@@ -492,6 +505,7 @@ __global__ void __launch_bounds__(256) k_count4(const float2* __restrict__ pos, 
                                                 int32_t* __restrict__ rank) {
     const int b = blockIdx.y;
     const Geom g = geom[b];
+    const double inv = 1.0 / g.cell;
     const size_t base = static_cast<size_t>(b) * N;
     const int i0 = blockIdx.x * (blockDim.x * kEmitPer) + threadIdx.x;
     float2 v[kEmitPer];
@@ -505,8 +519,8 @@ __global__ void __launch_bounds__(256) k_count4(const float2* __restrict__ pos, 
     for (int u = 0; u < kEmitPer; ++u) {
         const int i = i0 + u * blockDim.x;
         if (i < N) {
-            const int cx = cell_of(static_cast<double>(v[u].x), g.ox, g.cell, g.n_cols);
-            const int cy = cell_of(static_cast<double>(v[u].y), g.oy, g.cell, g.n_rows);
+            const int cx = cell_of_fast(static_cast<double>(v[u].x), g.ox, g.cell, inv, g.n_cols);
+            const int cy = cell_of_fast(static_cast<double>(v[u].y), g.oy, g.cell, inv, g.n_rows);
             bin[u] = cy * g.n_cols + cx;  // bin_grid.cpp:67
             r[u] = atomicAdd(bins + g.bin_off + bin[u], 1);
         }

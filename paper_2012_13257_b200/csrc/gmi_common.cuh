@@ -37,6 +37,20 @@ __device__ __forceinline__ int cell_of(double v, double origin, double cell,
     return clamp_int(x86_d2i(floor(t)), 0, n - 1);
 }
 
+// cell_of with the division replaced by a multiply by the rounded
+// reciprocal: q = d * (1/cell) is within ~2 ulp of fl(d / cell), so its floor
+// is the reference's unless q lies within 1e-9 of an integer (|q| < 2^20
+// here), in which case the exact division decides.  Bit-identical to cell_of.
+__device__ __forceinline__ int cell_of_fast(double v, double origin, double cell,
+                                            double inv_cell, int n) {
+    const double d = __dsub_rn(v, origin);
+    const double q = __dmul_rn(d, inv_cell);
+    double f = floor(q);
+    if (!(q - f > 1e-9 && f + 1.0 - q > 1e-9 && fabs(q) < 1048576.0))
+        f = floor(__ddiv_rn(d, cell));
+    return clamp_int(x86_d2i(f), 0, n - 1);
+}
+
 // Unclamped cell index (nearest_point's ring centre, bin_grid.cpp:131-132).
 __device__ __forceinline__ int cell_of_unclamped(double v, double origin,
                                                  double cell) {
