@@ -75,6 +75,7 @@ struct GatherParams {
     const float4* rec;  // [B][N][2]: (x, y, c0, c1) (c2, c3, idx|flag, 0)
     int N, C, W, H;
     int ncol, nyb, dyb, rc;   // bin geometry (see launch_gather_fast)
+    uint8_t qlo[32], qhi[32]; // per-lane column window [qlo, qhi]
     double r64, r2_64;
     float r2f, nk, thr;
     float* image;
@@ -94,12 +95,11 @@ k_gather(GatherParams p) {
     SmemGather<CC>& S = *reinterpret_cast<SmemGather<CC>*>(smem_raw);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // channel group of this CTA (C > 4: grid.z groups, weights recomputed per
-    // group; group 0 owns W, counts and the fallback list)
-    const int ch0 = blockIdx.z * CC, nch = min(CC, p.C - ch0);
-    const int tiles_y = (p.H + kTH - 1) / kTH;
-    const int b = blockIdx.y / tiles_y;
-    const int y0 = (blockIdx.y % tiles_y) * kTH;
+    // grid (tiles_x, tiles_y, B); C <= 4 channels in one group
+    constexpr int ch0 = 0;
+    const int nch = p.C;
+    const int b = blockIdx.z;
+    const int y0 = blockIdx.y * kTH;
     const int x0 = blockIdx.x * kTW;
     const Geom g = p.geom[b];
     const size_t base = static_cast<size_t>(b) * p.N;
@@ -128,9 +128,10 @@ k_gather(GatherParams p) {
         Nb[c] = f2(0.f, 0.f);
     }
     int cnt00 = 0, cnt01 = 0, cnt10 = 0, cnt11 = 0;
-    // lane window: columns of mu_x in (xa - r, xa + 1 + r) (exact in f64)
-    const int q_lo = max(0, static_cast<int>(floor(static_cast<double>(2 * lane + p.rc) - p.r64)));
-    const int q_hi = min(ncol - 1, static_cast<int>(ceil(static_cast<double>(2 * lane + p.rc + 1) + p.r64)) - 1);
+    // lane window: columns of mu_x in (xa - r, xa + 1 + r) (exact in f64,
+    // tabulated per lane on the host)
+    const int q_lo = p.qlo[lane];
+    const int q_hi = p.qhi[lane];
     // flagged points: generous band test (decided exactly by the f64 predicate)
     const float fb_lo = static_cast<float>(ya) - static_cast<float>(p.r64) - 1.0f;
     const float fb_hi = static_cast<float>(ya + 1) + static_cast<float>(p.r64) + 1.0f;
@@ -496,11 +497,11 @@ k_gather(GatherParams p) {
                     const float q0 = num * inv;
                     out[c] = fmaf(fmaf(-q0, w, num), inv, q0);
                 }
-                if (blockIdx.z == 0) {
+                {
                     p.wsum[bp] = w;
                     if (kCount) p.counts[bp] = py ? (px ? cnt11 : cnt10) : (px ? cnt01 : cnt00);
                 }
-            } else if (blockIdx.z == 0) {
+            } else {
                 // empty neighbourhood: fallback pixel (K3)
                 p.wsum[bp] = 0.f;
                 if (kCount) p.counts[bp] = 0;
@@ -550,6 +551,11 @@ bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* count
     const double r = c->cutoff;
     GatherParams p{};
     gather_geometry(r, p.rc, p.ncol, p.dyb, p.nyb);
+    for (int l = 0; l < 32; ++l) {
+        p.qlo[l] = static_cast<uint8_t>(std::max(0, static_cast<int>(std::floor(2.0 * l + p.rc - r))));
+        p.qhi[l] = static_cast<uint8_t>(std::min(p.ncol - 1,
+                                                 static_cast<int>(std::ceil(2.0 * l + p.rc + 1 + r)) - 1));
+    }
     p.geom = c->geom_d;
     p.bins = c->bins;
     p.rec = c->rec;
@@ -571,7 +577,7 @@ bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* count
     p.special_count = c->special_count_d;
     p.special_cap = c->special_cap;
     const int cc = c->C <= 4 ? c->C : 4;
-    const dim3 grid((c->W + kTW - 1) / kTW, ((c->H + kTH - 1) / kTH) * c->B, (c->C + cc - 1) / cc);
+    const dim3 grid((c->W + kTW - 1) / kTW, (c->H + kTH - 1) / kTH, c->B);
     GMI_CUDA(cudaMemsetAsync(c->special_count_d, 0, sizeof(int32_t), ctx->stream));
     const bool cnt = counts != nullptr;
     switch (cc) {
