@@ -105,6 +105,21 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def traffic_of(kernel: str, config: int, batch: int):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
+    --set full capture of this workload (profiles/traffic_cfg3.json, made by
+    tools/capture_traffic.sh + tools/traffic_json.py), else None."""
+    if config != 3 or batch != CFG["B"]:
+        return None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic_cfg3.json")) as f:
+            d = json.load(f)
+        v = d.get(kernel, {}).get("traffic_bytes")
+        return int(v) if v else None
+    except Exception:
+        return None
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -392,7 +407,7 @@ def main():
         "phases_ms_per_step": {k: round(v, 4) for k, v in per_call.items()},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                      "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
-                     "traffic": None, "peak_kind": peak_kind,
+                     "traffic": traffic_of(dom, args.config, B), "peak_kind": peak_kind,
                      "note": "algorithmic bytes per launch / CUDA-event time; the path is FP32-pipe bound, see roofline_fp32"},
         "roofline_fp32": {"bound": "fp32_pipe", "kernel": dom, "achieved": round(fp32_ach, 3),
                           "peak": round(fp32_peak, 2), "unit": "T FP32-instr/s",

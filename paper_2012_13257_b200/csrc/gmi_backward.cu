@@ -583,6 +583,36 @@ __global__ void k_special_backward(SpecBwdParams p) {
 // float4 slots of one staged pixel pair (PairLayout<CG>::kF4)
 inline int pair_f4(int cg) { return (cg + 2) / 2; }
 
+// Precise fallback routing (special count known on the host, i.e. the
+// synchronous API): the upstream of every fallback pixel is summed per
+// (point, channel) in f64 and added to the point's fp32 d_col with ONE
+// rounding.  Sparse inputs route hundreds of O(1) upstream values into a
+// single point; fp32 atomics would carry their rounding (and their
+// nondeterministic order) into a cancellation to ~1e-2.
+__global__ void k_special_backward64(SpecBwdParams p, double* __restrict__ acc) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int n = min(*p.special_count, p.special_cap);
+    for (int si = warp; si < n; si += nwarps) {
+        const Special sp = p.special[si];
+        if (sp.kind != 1 || sp.nearest < 0) continue;
+        const size_t pixb = static_cast<size_t>(sp.b) * p.H * p.W + sp.pix;
+        const size_t base = static_cast<size_t>(sp.b) * p.N;
+        for (int c = lane; c < p.C; c += 32)
+            atomicAdd(acc + (base + sp.nearest) * p.C + c,
+                      static_cast<double>(p.upstream[pixb * p.C + c]));
+    }
+}
+
+__global__ void k_merge_special(const double* __restrict__ acc, float* __restrict__ d_col,
+                                size_t n) {
+    const size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (k >= n) return;
+    const double a = acc[k];
+    if (a != 0.0) d_col[k] = static_cast<float>(static_cast<double>(d_col[k]) + a);
+}
+
 template <int CG>
 void launch_points(gmi_ctx* ctx, const BwdParams& p, int nblocks, int groups) {
     const int smem = kSmemBudget;
@@ -699,6 +729,18 @@ void launch_special_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upst
     p.H = c->H;
     p.fallback = c->fallback;
     p.d_col = d_colors;
+    if (c->special_count == 0 || c->fallback != GMI_FALLBACK_NEAREST) return;
+    if (c->special_count > 0) {
+        const size_t n = static_cast<size_t>(c->B) * c->N * c->C;
+        double* acc = static_cast<double*>(scratch(ctx, WS_PART, sizeof(double) * n));
+        GMI_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * n, ctx->stream));
+        k_special_backward64<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(p, acc);
+        GMI_LAUNCHED(ctx);
+        k_merge_special<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(acc, d_colors, n);
+        GMI_LAUNCHED(ctx);
+        return;
+    }
+    // count unknown (asynchronous API): fp32 atomics
     k_special_backward<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(p);
     GMI_LAUNCHED(ctx);
 }

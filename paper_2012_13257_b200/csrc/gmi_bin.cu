@@ -548,10 +548,25 @@ int host_axis_cells(double span, double cell, int cap) {
 }
 
 // Scan tiles over segments [seg_start[b], seg_start[b] + seg_len[b]).
+// `equal`: all segments have the same length (device geometry); the tile
+// table then depends only on (B, stride) and is cached in the context.
 static void scan_segments(gmi_ctx* ctx, int32_t* data, const std::vector<int64_t>& seg_start,
-                          const std::vector<int64_t>& seg_len) {
+                          const std::vector<int64_t>& seg_len, bool equal = false) {
     cudaStream_t st = ctx->stream;
     const int B = static_cast<int>(seg_start.size());
+    if (equal && ctx->eq_B == B && ctx->eq_stride == seg_len[0]) {
+        const int nt = ctx->eq_nt;
+        ScanTile* d_tiles = static_cast<ScanTile*>(ctx->ws_ptr[WS_TILES_EQ]);
+        int32_t* d_segoff = static_cast<int32_t*>(ctx->ws_ptr[WS_SEGOFF_EQ]);
+        int32_t* d_tsum = static_cast<int32_t*>(scratch(ctx, WS_TSUM, sizeof(int32_t) * nt));
+        k_scan_reduce<<<nt, kScanThreads, 0, st>>>(data, d_tiles, d_tsum);
+        GMI_LAUNCHED(ctx);
+        k_scan_segments<<<B, 1024, 0, st>>>(d_tsum, d_segoff);
+        GMI_LAUNCHED(ctx);
+        k_scan_apply<<<nt, kScanThreads, 0, st>>>(data, d_tiles, d_tsum);
+        GMI_LAUNCHED(ctx);
+        return;
+    }
     std::vector<ScanTile> tiles;
     std::vector<int32_t> seg_off(B + 1, 0);
     for (int b = 0; b < B; ++b) {
@@ -561,9 +576,16 @@ static void scan_segments(gmi_ctx* ctx, int32_t* data, const std::vector<int64_t
         seg_off[b + 1] = static_cast<int32_t>(tiles.size());
     }
     const int nt = static_cast<int>(tiles.size());
-    ScanTile* d_tiles = static_cast<ScanTile*>(scratch(ctx, WS_TILES, sizeof(ScanTile) * nt));
+    ScanTile* d_tiles = static_cast<ScanTile*>(
+        scratch(ctx, equal ? WS_TILES_EQ : WS_TILES, sizeof(ScanTile) * nt));
     int32_t* d_tsum = static_cast<int32_t*>(scratch(ctx, WS_TSUM, sizeof(int32_t) * nt));
-    int32_t* d_segoff = static_cast<int32_t*>(scratch(ctx, WS_SEGOFF, sizeof(int32_t) * (B + 1)));
+    int32_t* d_segoff = static_cast<int32_t*>(
+        scratch(ctx, equal ? WS_SEGOFF_EQ : WS_SEGOFF, sizeof(int32_t) * (B + 1)));
+    if (equal) {
+        ctx->eq_B = B;
+        ctx->eq_stride = seg_len[0];
+        ctx->eq_nt = nt;
+    }
     GMI_CUDA(cudaMemcpyAsync(d_tiles, tiles.data(), sizeof(ScanTile) * nt,
                              cudaMemcpyHostToDevice, st));
     GMI_CUDA(cudaMemcpyAsync(d_segoff, seg_off.data(), sizeof(int32_t) * (B + 1),
@@ -669,7 +691,7 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
     k_count4<<<pgrid4, 256, 0, st>>>(p2, N, c->geom_d, c->bins, cellid, rank);
     GMI_LAUNCHED(ctx);
     host_trace("bin: count launched");
-    scan_segments(ctx, c->bins, seg_start, seg_len);
+    scan_segments(ctx, c->bins, seg_start, seg_len, c->geom_h.empty());
 
     const bool classify = c->wsum64 == nullptr;
     if (hot && !c->sort_cells) {

@@ -61,6 +61,11 @@ struct gmi_ctx {
     // grow-only per-call scratch (stream-ordered reuse on the ctx stream)
     void* ws_ptr[16] = {nullptr};
     size_t ws_cap[16] = {0};
+    // scan tiles of the equal-segment (device geometry) binning, cached per
+    // (batch, stride) so the hot path issues no host->device copy
+    int eq_B = -1;
+    int64_t eq_stride = -1;
+    int eq_nt = 0;
     // copy streams of the pipelined host-buffer API (created on first use)
     cudaStream_t s_in = nullptr;
     cudaStream_t s_out = nullptr;
@@ -69,7 +74,8 @@ struct gmi_ctx {
 // scratch slots
 enum WsSlot {
     WS_BBOX = 0, WS_CELLID, WS_RANK, WS_TMP, WS_BIG, WS_BIGCOUNT, WS_TILES, WS_TSUM,
-    WS_SEGOFF, WS_BLKOFF, WS_PART, WS_HOST_IN0, WS_HOST_IN1, WS_HOST_IN2, WS_COUNT
+    WS_SEGOFF, WS_BLKOFF, WS_PART, WS_HOST_IN0, WS_HOST_IN1, WS_HOST_IN2,
+    WS_TILES_EQ, WS_SEGOFF_EQ, WS_COUNT
 };
 
 // RAII phase marker: records an event pair on the ctx stream when profiling.
