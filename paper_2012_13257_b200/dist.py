@@ -48,6 +48,71 @@ def halo_points(pos_y: np.ndarray, height: int, world: int, cutoff: float) -> np
     return n
 
 
+def band_points(pos_y: np.ndarray, r0: int, r1: int, cutoff: float) -> np.ndarray:
+    """Ascending indices of the points a rank needs for rows [r0, r1).  The
+    ascending order keeps the reference's per-pixel summation order
+    (engine.cpp:59-72 sums in ascending point index)."""
+    return np.nonzero(band_point_mask(pos_y, r0, r1, cutoff))[0]
+
+
+def shared_points(pos_y: np.ndarray, height: int, world: int, cutoff: float) -> np.ndarray:
+    """Ascending indices of the points whose balls reach two or more bands:
+    the only gradients that need a cross-rank reduction."""
+    return np.nonzero(halo_points(pos_y, height, world, cutoff) > 1)[0]
+
+
+class BandPlan:
+    """One rank's share of a single huge image (BASELINE configs[3]): its row
+    band, the points it renders (with their band-local positions: y shifted
+    by -r0, exact in fp32 for integer r0 within the frame) and where the
+    globally shared points sit in its local arrays."""
+
+    def __init__(self, pos: np.ndarray, height: int, world: int, rank: int, cutoff: float):
+        self.r0, self.r1 = band_rows(height, world, rank)
+        self.idx = band_points(pos[:, 1], self.r0, self.r1, cutoff)
+        self.shared = shared_points(pos[:, 1], height, world, cutoff)
+        # local slot of each shared point on this rank (-1: not in this band)
+        where = np.full(pos.shape[0], -1, np.int64)
+        where[self.idx] = np.arange(self.idx.size)
+        self.shared_local = where[self.shared]
+        # points this rank owns outright (in no other band)
+        owned = np.ones(self.idx.size, bool)
+        owned[self.shared_local[self.shared_local >= 0]] = False
+        self.owned_local = np.nonzero(owned)[0]
+
+    @property
+    def rows(self) -> int:
+        return self.r1 - self.r0
+
+    def local_positions(self, pos: np.ndarray) -> np.ndarray:
+        p = np.array(pos[self.idx], dtype=pos.dtype, copy=True)
+        p[:, 1] -= p.dtype.type(self.r0)
+        return p
+
+    def shared_partials(self, d_col: np.ndarray, d_pos: np.ndarray) -> np.ndarray:
+        """[len(shared), C + 2] partial gradients of the shared points (zeros
+        for the ones outside this band), the buffer the ranks SUM-reduce."""
+        C = d_col.shape[1]
+        buf = np.zeros((self.shared.size, C + 2), d_col.dtype)
+        have = self.shared_local >= 0
+        buf[have, :C] = d_col[self.shared_local[have]]
+        buf[have, C:] = d_pos[self.shared_local[have]]
+        return buf
+
+    def assemble(self, d_col: np.ndarray, d_pos: np.ndarray, reduced: np.ndarray, n: int):
+        """Full-size gradients as this rank holds them: its owned points and
+        every shared point (reduced); other ranks' owned points stay zero."""
+        C = d_col.shape[1]
+        g_col = np.zeros((n, C), d_col.dtype)
+        g_pos = np.zeros((n, 2), d_pos.dtype)
+        own = self.idx[self.owned_local]
+        g_col[own] = d_col[self.owned_local]
+        g_pos[own] = d_pos[self.owned_local]
+        g_col[self.shared] = reduced[:, :C]
+        g_pos[self.shared] = reduced[:, C:]
+        return g_col, g_pos
+
+
 def max_over_ranks(value: float, device=None) -> float:
     """Max of a scalar across ranks (the timing rule of the bench)."""
     import torch

@@ -46,6 +46,57 @@ def _worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
+def _band_worker(rank, world, port, out):
+    """configs[3] decomposition on CPU: every rank renders its row band from
+    its halo points with the oracle (the reference restated), the shared
+    points' partial gradients are SUM-reduced over gloo, and the result must
+    equal the full-frame reference."""
+    import oracle
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        orc = oracle.Oracle()
+        rng = np.random.default_rng(5)
+        W, H, N, C, sigma, cutoff = 48, 40, 900, 3, 1.0, 3.0
+        pos = np.stack([rng.uniform(-0.5, W - 0.5, N), rng.uniform(-0.5, H - 0.5, N)], 1).astype(np.float32)
+        col = rng.uniform(0, 1, (N, C)).astype(np.float32)
+        up = rng.uniform(-1, 1, (H, W, C))
+        full = orc.forward(pos, col, W, H, sigma, cutoff)
+        rdc, rdp = orc.backward(pos, col, full, up, sigma, cutoff)
+        plan = gdist.BandPlan(pos, H, world, rank, cutoff)
+        bpos = plan.local_positions(pos)
+        f = orc.forward(bpos, col[plan.idx], W, plan.rows, sigma, cutoff)
+        dc, dp = orc.backward(bpos, col[plan.idx], f, up[plan.r0:plan.r1], sigma, cutoff)
+        buf = torch.from_numpy(plan.shared_partials(dc, dp))
+        gdist.sum_over_ranks(buf)
+        g_col, g_pos = plan.assemble(dc, dp, buf.numpy(), N)
+        rows_ok = bool(np.array_equal(f["image"], full["image"][plan.r0:plan.r1]))
+        nofb = int(full["fallback_flag"].sum()) == 0
+        mine = np.zeros(N, bool)
+        mine[plan.idx[plan.owned_local]] = True
+        mine[plan.shared] = True
+        err_c = float(np.abs(g_col[mine] - rdc[mine]).max())
+        err_p = float(np.abs(g_pos[mine] - rdp[mine]).max())
+        out[rank] = (rows_ok, nofb, err_c, err_p, int(plan.shared.size))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_band_split_matches_full_frame():
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_band_worker, args=(world, port, out), nprocs=world, join=True)
+    for r in range(world):
+        rows_ok, nofb, err_c, err_p, n_shared = out[r]
+        assert rows_ok, "band image rows differ from the full-frame reference"
+        assert nofb
+        assert err_c < 1e-9 and err_p < 1e-9, (err_c, err_p)
+        assert n_shared > 0
+
+
 def test_two_rank_sharding_and_reductions():
     world = 2
     port = _free_port()
