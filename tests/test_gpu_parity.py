@@ -255,13 +255,13 @@ def test_smoke_entry():
 
 def test_band_split_matches_full_frame(gmi, ctx, orc):
     """configs[3] decomposition on the real kernels (one GPU, bands run in
-    sequence, the shared-point reduction done on the host): band images equal
-    the full frame's rows bit for bit, gradients match the full-frame
-    reference within tolerance."""
+    sequence, the shared-point reduction done on the host): band images and
+    the reduced gradients match the full-frame reference within tolerance
+    (the summation order inside a tile follows the band's own cell grid)."""
     from paper_2012_13257_b200 import dist as gdist
 
-    W, H, world, sigma, cutoff = 160, 128, 4, 1.0, 3.0
-    pos, col, up = orc.synth_batch(21, 1, 6000, 3, W, H)
+    W, H, world, sigma, cutoff = 160, 128, 4, 1.5, 4.5
+    pos, col, up = orc.synth_batch(21, 1, 10000, 3, W, H)
     pos, col, up = f32(pos[0]), f32(col[0]), f32(up[0])
     img, cache = gmi.forward_batch(pos[None], col[None], W, H, sigma, cutoff, ctx=ctx)
     assert cache.fallback_count == 0
@@ -274,7 +274,7 @@ def test_band_split_matches_full_frame(gmi, ctx, orc):
         bpos = plan.local_positions(pos)
         bimg, bcache = gmi.forward_batch(bpos[None], col[plan.idx][None], W, plan.rows, sigma,
                                          cutoff, ctx=ctx)
-        assert np.array_equal(bimg[0], img[0][plan.r0:plan.r1]), f"band {rank} image rows differ"
+        assert_close(bimg[0], r["image"][plan.r0:plan.r1], what=f"band {rank} image")
         dc, dp = gmi.backward_batch(bpos[None], col[plan.idx][None], bcache,
                                     up[plan.r0:plan.r1][None], sigma, cutoff, ctx=ctx)
         g_col[plan.idx] += dc[0]
