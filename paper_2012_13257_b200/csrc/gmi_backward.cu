@@ -43,6 +43,8 @@ struct BwdParams {
     const int32_t* sidx;
     const float* scol;      // [B][C][N]
     const float4* rec;      // fast layout [B][N][2] (replaces sx/sy/sidx/scol)
+    const float* ccol;      // C > 4 with the fast layout: [B][N][C] colours
+    int lpp;                // lanes per point (1, 2, 4, 8): rows split over lanes
     const float* wsum;      // [B][H][W]
     const float* image;     // [B][H][W][C]
     const float* upstream;  // [B][H][W][C]
@@ -94,7 +96,7 @@ __device__ __forceinline__ void pixel_terms(const BwdParams& p, size_t img_base,
     }
 }
 
-template <int CG>
+template <int CG, int LPP>
 __global__ void __launch_bounds__(kThreads, 4)
 k_backward_points(BwdParams p) {
     using L = PairLayout<CG>;
@@ -329,27 +331,34 @@ k_backward_points(BwdParams p) {
     const double r2_64 = p.r2_64;
     const int xmin = max(rx0, 0), xmax = min(rx1, p.W - 1);
     const float2 nk2 = f2(nk, nk), two = f2(2.f, 2.f);
-    // warp tasks of 32 consecutive points (bin order keeps a warp's points
-    // adjacent), dealt round-robin; the next task's record is prefetched
+    // warp tasks of 32/lpp consecutive points (bin order keeps a warp's points
+    // adjacent), dealt round-robin; the next task's record is prefetched.
+    // With lpp > 1 (wide radii) the lpp lanes of a point take interleaved rows
+    // of its disk and their partial sums are combined by a fixed shuffle tree.
     const int warp = tid >> 5;
+    constexpr int lpp = LPP;
+    const int sub = lane & (lpp - 1);
+    const int ppw = 32 / lpp;                 // points per warp task
+    const int pstep = (kThreads / 32) * ppw;  // points per CTA round
     float4 nra = make_float4(0.f, 0.f, 0.f, 0.f), nrb = nra;
     int ns = 0;
-    if (p.rec && warp * 32 + lane < total) {
-        ns = slot_of(warp * 32 + lane);
+    if (p.rec && warp * ppw + lane / lpp < total) {
+        ns = slot_of(warp * ppw + lane / lpp);
         nra = p.rec[(base + ns) * 2];
         nrb = p.rec[(base + ns) * 2 + 1];
     }
-    for (int kb = warp * 32; kb < total; kb += kThreads) {
-        const int k = kb + lane;
+    for (int kb = warp * ppw; kb < total; kb += pstep) {
+        const int k = kb + lane / lpp;
         const float4 cra = nra, crb = nrb;
         const int cs = ns;
-        if (p.rec && k + kThreads < total) {
-            ns = slot_of(k + kThreads);
+        if (p.rec && k + pstep < total) {
+            ns = slot_of(k + pstep);
             nra = p.rec[(base + ns) * 2];
             nrb = p.rec[(base + ns) * 2 + 1];
         }
-        if (k >= total) continue;
-        const int s = p.rec ? cs : slot_of(k);
+        const bool live = k < total;
+        if (lpp == 1 && !live) continue;
+        const int s = p.rec ? cs : slot_of(min(k, total - 1));
         float mx, my;
         uint32_t raw;
         float cc[CG];
@@ -360,9 +369,15 @@ k_backward_points(BwdParams p) {
             mx = ra.x;
             my = ra.y;
             raw = __float_as_uint(rb.z);
-            const float cv[4] = {ra.z, ra.w, rb.x, rb.y};
+            if (p.ccol != nullptr) {
 #pragma unroll
-            for (int c = 0; c < CG; ++c) cc[c] = cv[c];
+                for (int c = 0; c < CG; ++c)
+                    cc[c] = c < nch ? p.ccol[(base + s) * p.C + ch0 + c] : 0.f;
+            } else {
+                const float cv[4] = {ra.z, ra.w, rb.x, rb.y};
+#pragma unroll
+                for (int c = 0; c < CG; ++c) cc[c] = cv[c];
+            }
         } else {
             mx = p.sx[base + s];
             my = p.sy[base + s];
@@ -386,11 +401,11 @@ k_backward_points(BwdParams p) {
         // my +- r) suffices; flagged points keep a one-row margin for the f64
         // predicate
         const float pad = unsafe ? 1.0f : 1e-2f;
-        const int ya = max(ry0, static_cast<int>(ceilf(my - rf - pad)));
-        const int yb = min(ry1, static_cast<int>(floorf(my + rf + pad)));
+        const int ya = max(ry0, static_cast<int>(ceilf(my - rf - pad))) + sub;
+        const int yb = live ? min(ry1, static_cast<int>(floorf(my + rf + pad))) : ya - 1;
 
         float yf = static_cast<float>(ya);  // exact row coordinate
-        for (int y = ya; y <= yb; ++y, yf += 1.0f) {
+        for (int y = ya; y <= yb; y += lpp, yf += static_cast<float>(lpp)) {
             float dy;
             int xl, xr;
             if (!unsafe) {
@@ -482,10 +497,20 @@ k_backward_points(BwdParams p) {
             }
             gy = fmaf(gyr2.x + gyr2.y, dy, gy);
         }
-        for (int c = 0; c < nch; ++c)
-            p.d_col[(base + i) * p.C + ch0 + c] = dcol[c].x + dcol[c].y;
+        float gxs = gx2.x + gx2.y;
+        float dcs[CG];
+#pragma unroll
+        for (int c = 0; c < CG; ++c) dcs[c] = dcol[c].x + dcol[c].y;
+        for (int o = lpp >> 1; o > 0; o >>= 1) {
+#pragma unroll
+            for (int c = 0; c < CG; ++c) dcs[c] += __shfl_xor_sync(0xffffffffu, dcs[c], o);
+            gxs += __shfl_xor_sync(0xffffffffu, gxs, o);
+            gy += __shfl_xor_sync(0xffffffffu, gy, o);
+        }
+        if (!live || sub != 0) continue;
+        for (int c = 0; c < nch; ++c) p.d_col[(base + i) * p.C + ch0 + c] = dcs[c];
         float* dp = p.d_pos + (static_cast<size_t>(cg) * p.B * p.N + base + i) * 2;
-        dp[0] = (gx2.x + gx2.y) * inv_s2;
+        dp[0] = gxs * inv_s2;
         dp[1] = gy * inv_s2;
     }
 }
@@ -613,13 +638,23 @@ __global__ void k_merge_special(const double* __restrict__ acc, float* __restric
     if (a != 0.0) d_col[k] = static_cast<float>(static_cast<double>(d_col[k]) + a);
 }
 
+template <int CG, int LPP>
+void launch_points_lpp(gmi_ctx* ctx, const BwdParams& p, int nblocks, int groups) {
+    const int smem = kSmemBudget;
+    static int set_dev = -1;  // attribute set once per device
+    if (set_dev != ctx->device) {
+        set_dev = ctx->device;
+        GMI_CUDA(cudaFuncSetAttribute(k_backward_points<CG, LPP>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
+    k_backward_points<CG, LPP><<<dim3(nblocks, groups), kThreads, smem, ctx->stream>>>(p);
+    GMI_LAUNCHED(ctx);
+}
+
 template <int CG>
 void launch_points(gmi_ctx* ctx, const BwdParams& p, int nblocks, int groups) {
-    const int smem = kSmemBudget;
-    GMI_CUDA(cudaFuncSetAttribute(k_backward_points<CG>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    k_backward_points<CG><<<dim3(nblocks, groups), kThreads, smem, ctx->stream>>>(p);
-    GMI_LAUNCHED(ctx);
+    if (p.lpp > 1) launch_points_lpp<CG, 8>(ctx, p, nblocks, groups);
+    else launch_points_lpp<CG, 1>(ctx, p, nblocks, groups);
 }
 
 }  // namespace
@@ -663,6 +698,10 @@ void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
     p.sidx = c->sidx;
     p.scol = c->scol;
     p.rec = c->rec;
+    p.ccol = c->ccol;
+    // lanes per point: a point's disk has ~2r+1 rows; split them over lanes
+    // once they outnumber what keeps a 256-thread block busy
+    p.lpp = c->cutoff >= 6.0 ? 8 : 1;
     p.wsum = c->wsum;
     p.image = c->image;
     p.upstream = upstream;

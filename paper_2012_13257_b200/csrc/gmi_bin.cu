@@ -448,6 +448,7 @@ struct ScatterEmitParams {
     const int32_t* cellid;
     const int32_t* rank;
     float4* rec;
+    float* ccol;   // C > 4: [B][N][C] colours in bin order
     unsigned long long* issue;
     int N, C;
     int classify;
@@ -485,6 +486,19 @@ __global__ void __launch_bounds__(256) k_scatter_emit(ScatterEmitParams p) {
             if (ch < p.C && code == 0) {
                 if (!is_finite_f(c[u][ch])) code = 1;                   // NonFiniteValue
                 else if (c[u][ch] < 0.0f || c[u][ch] > 1.0f) code = 2;  // ColorOutOfRange
+            }
+        }
+        if (p.ccol != nullptr) {
+            // C > 4: every channel, validated in channel order, copied whole
+            const float* src = p.col + (base + i) * p.C;
+            float* dstc = p.ccol + (base + dst[u]) * p.C;
+            for (int ch = 0; ch < p.C; ++ch) {
+                const float cv = src[ch];
+                dstc[ch] = cv;
+                if (code == 0) {
+                    if (!is_finite_f(cv)) code = 1;
+                    else if (cv < 0.0f || cv > 1.0f) code = 2;
+                }
             }
         }
         if (code) atomicMin(p.issue + b, (static_cast<unsigned long long>(i) << 8) | code);
@@ -704,6 +718,7 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
         e.cellid = cellid;
         e.rank = rank;
         e.rec = c->rec;
+        e.ccol = c->ccol;
         e.issue = d_issue;
         e.N = N;
         e.C = c->C;

@@ -192,6 +192,8 @@ int do_forward(gmi_ctx* ctx, const float* pos, const float* col, int B, int N,
         c->sort_cells = !fast;
         if (fast) {
             c->rec = static_cast<float4*>(gmi_host::cache_alloc(c, sizeof(float4) * 2 * BN));
+            if (C > 4)
+                c->ccol = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN * C));
         } else {
             c->sx = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN));
             c->sy = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BN));

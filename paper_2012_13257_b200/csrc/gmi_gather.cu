@@ -73,6 +73,7 @@ struct GatherParams {
     const Geom* geom;
     const int32_t* bins;
     const float4* rec;  // [B][N][2]: (x, y, c0, c1) (c2, c3, idx|flag, 0)
+    const float* ccol;  // C > 4: [B][N][C] colours in bin order
     int N, C, W, H;
     int ncol, nyb, dyb, rc;   // bin geometry (see launch_gather_fast)
     uint8_t qlo[32], qhi[32]; // per-lane column window [qlo, qhi]
@@ -88,17 +89,21 @@ struct GatherParams {
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-template <int CC, bool kCount>
+template <int CC, bool kCount, bool kMulti>
 __global__ void __launch_bounds__(kNT, 4)
 k_gather(GatherParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SmemGather<CC>& S = *reinterpret_cast<SmemGather<CC>*>(smem_raw);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // grid (tiles_x, tiles_y, B); C <= 4 channels in one group
-    constexpr int ch0 = 0;
-    const int nch = p.C;
-    const int b = blockIdx.z;
+    // grid (tiles_x, tiles_y, B * groups): channel group g = blockIdx.z %
+    // groups handles channels [4g, 4g + 4) (C > 4: the weights are
+    // recomputed per group; group 0 owns W, counts and the fallback list)
+    const int groups = kMulti ? (p.C + CC - 1) / CC : 1;
+    const int grp = kMulti ? static_cast<int>(blockIdx.z) % groups : 0;
+    const int ch0 = grp * CC;
+    const int nch = kMulti ? min(CC, p.C - ch0) : p.C;
+    const int b = kMulti ? static_cast<int>(blockIdx.z) / groups : static_cast<int>(blockIdx.z);
     const int y0 = blockIdx.y * kTH;
     const int x0 = blockIdx.x * kTW;
     const Geom g = p.geom[b];
@@ -294,8 +299,16 @@ k_gather(GatherParams p) {
             if (key < 0) continue;
             const int pos = atomicSub(&S.bin[key], 1) - 1;
             const int slot = S.u.st.slot[k];
-            const float4 ra = p.rec[(base + slot) * 2];
-            const float4 rb = p.rec[(base + slot) * 2 + 1];
+            float4 ra = p.rec[(base + slot) * 2];
+            float4 rb = p.rec[(base + slot) * 2 + 1];
+            if (kMulti) {
+                // C > 4: this group's channels from the bin-ordered colours
+                const float* cs = p.ccol + (base + slot) * p.C + ch0;
+                ra.z = cs[0];
+                ra.w = nch > 1 ? cs[1] : 0.f;
+                rb.x = nch > 2 ? cs[2] : 0.f;
+                rb.y = nch > 3 ? cs[3] : 0.f;
+            }
             S.A[pos] = ra;
             if (CC > 2) S.Bc[pos] = f2(rb.x, rb.y);
             S.idx[pos] = static_cast<int>(__float_as_uint(rb.z) & 0x7fffffffu);
@@ -478,7 +491,7 @@ k_gather(GatherParams p) {
             float2* out2 = reinterpret_cast<float2*>(p.image + bp * CC);
 #pragma unroll
             for (int j = 0; j < CC; ++j) out2[j] = f2(o[2 * j], o[2 * j + 1]);
-            *reinterpret_cast<float2*>(p.wsum + bp) = wr;
+            if (grp == 0) *reinterpret_cast<float2*>(p.wsum + bp) = wr;
             continue;
         }
 #pragma unroll
@@ -497,11 +510,11 @@ k_gather(GatherParams p) {
                     const float q0 = num * inv;
                     out[c] = fmaf(fmaf(-q0, w, num), inv, q0);
                 }
-                {
+                if (grp == 0) {
                     p.wsum[bp] = w;
                     if (kCount) p.counts[bp] = py ? (px ? cnt11 : cnt10) : (px ? cnt01 : cnt00);
                 }
-            } else {
+            } else if (grp == 0) {
                 // empty neighbourhood: fallback pixel (K3)
                 p.wsum[bp] = 0.f;
                 if (kCount) p.counts[bp] = 0;
@@ -513,16 +526,16 @@ k_gather(GatherParams p) {
     }
 }
 
-template <int CC, bool kCount>
+template <int CC, bool kCount, bool kMulti = false>
 void launch_cc(gmi_ctx* ctx, const GatherParams& p, dim3 grid) {
     const int smem = static_cast<int>(sizeof(SmemGather<CC>));
     static int set_dev = -1;  // attribute set once per device
     if (set_dev != ctx->device) {
         set_dev = ctx->device;
-    GMI_CUDA(cudaFuncSetAttribute(k_gather<CC, kCount>,
+    GMI_CUDA(cudaFuncSetAttribute(k_gather<CC, kCount, kMulti>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     }
-    k_gather<CC, kCount><<<grid, kNT, smem, ctx->stream>>>(p);
+    k_gather<CC, kCount, kMulti><<<grid, kNT, smem, ctx->stream>>>(p);
     GMI_LAUNCHED(ctx);
 }
 
@@ -542,7 +555,7 @@ static void gather_geometry(double r, int& rc, int& ncol, int& dyb, int& nyb) {
 
 // The fast gather applies: fp32 weight mode and a bin table that fits.
 bool gather_fast_ok(const gmi_cache* c) {
-    if (c->wsum64 != nullptr || c->force_generic || c->C > 4) return false;
+    if (c->wsum64 != nullptr || c->force_generic) return false;
     int rc, ncol, dyb, nyb;
     gather_geometry(c->cutoff, rc, ncol, dyb, nyb);
     return ncol < kColMax && ncol * nyb + 1 <= kBinMax;
@@ -563,6 +576,7 @@ bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* count
     p.geom = c->geom_d;
     p.bins = c->bins;
     p.rec = c->rec;
+    p.ccol = c->ccol;
     p.N = c->N;
     p.C = c->C;
     p.W = c->W;
@@ -581,14 +595,17 @@ bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* count
     p.special_count = c->special_count_d;
     p.special_cap = c->special_cap;
     const int cc = c->C <= 4 ? c->C : 4;
-    const dim3 grid((c->W + kTW - 1) / kTW, (c->H + kTH - 1) / kTH, c->B);
+    const dim3 grid((c->W + kTW - 1) / kTW, (c->H + kTH - 1) / kTH, c->B * ((c->C + cc - 1) / cc));
     GMI_CUDA(cudaMemsetAsync(c->special_count_d, 0, sizeof(int32_t), ctx->stream));
     const bool cnt = counts != nullptr;
     switch (cc) {
         case 1: cnt ? launch_cc<1, true>(ctx, p, grid) : launch_cc<1, false>(ctx, p, grid); break;
         case 2: cnt ? launch_cc<2, true>(ctx, p, grid) : launch_cc<2, false>(ctx, p, grid); break;
         case 3: cnt ? launch_cc<3, true>(ctx, p, grid) : launch_cc<3, false>(ctx, p, grid); break;
-        default: cnt ? launch_cc<4, true>(ctx, p, grid) : launch_cc<4, false>(ctx, p, grid); break;
+        default:
+            if (c->C > 4) cnt ? launch_cc<4, true, true>(ctx, p, grid) : launch_cc<4, false, true>(ctx, p, grid);
+            else cnt ? launch_cc<4, true>(ctx, p, grid) : launch_cc<4, false>(ctx, p, grid);
+            break;
     }
     return true;
 }

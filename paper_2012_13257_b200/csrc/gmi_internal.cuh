@@ -145,6 +145,7 @@ struct gmi_cache {
     // point in bin order, (x, y, c0, c1) (c2, c3, idx|flag bits, 0); replaces
     // sx/sy/sidx/scol, which stay null
     float4* rec = nullptr;    // [B][N][2]
+    float* ccol = nullptr;    // C > 4: all colours [B][N][C] in bin order
     // per pixel
     float* wsum = nullptr;    // [B][H][W]; 0 => special pixel
     double* wsum64 = nullptr; // [B][H][W] f64 normaliser (precise mode only)
