@@ -381,9 +381,12 @@ k_gather(GatherParams p) {
         {
             const int ts = S.v.wcs[warp][q_lo], te = S.v.wcs[warp][q_hi + 1];
             const uint16_t* lst = S.u.wl[warp];
+            // list entry of the next candidate fetched one iteration ahead
+            int kn = ts < te ? lst[ts] : 0;
 #pragma unroll 2
             for (int t = ts; t < te; ++t) {
-                const int kc = lst[t];
+                const int kc = kn;
+                kn = lst[t + 1 < te ? t + 1 : t];
                 const float4 a = S.A[kc];
                 const float2 bcur = CC > 2 ? S.Bc[kc] : f2(0.f, 0.f);
                 const float2 dx = __fadd2_rn(X, f2(-a.x, -a.x));
@@ -458,9 +461,11 @@ k_gather(GatherParams p) {
                 }
             }
         }
-        const bool last = S.done;
+        // the last chunk needs no barrier: a warp that is done goes straight
+        // to its epilogue instead of waiting for the CTA's longest window
+        // (S.done was published before this chunk's first barrier)
+        if (S.done) break;
         __syncthreads();
-        if (last) break;
     }
 
     // ---- fused normalisation + store (engine.cpp:74-100) ----
