@@ -562,8 +562,9 @@ int gmi_forward_host(gmi_ctx* ctx, const float* positions, const float* colors, 
             if (rc == GMI_OK) {
                 for (gmi_cache* part : c->parts) {
                     int32_t nspec = 0;
-                    GMI_CUDA(cudaMemcpy(&nspec, part->special_count_d, sizeof(int32_t),
-                                        cudaMemcpyDeviceToHost));
+                    GMI_CUDA(cudaMemcpyAsync(&nspec, part->special_count_d, sizeof(int32_t),
+                                             cudaMemcpyDeviceToHost, ctx->stream));
+                    GMI_CUDA(cudaStreamSynchronize(ctx->stream));
                     if (nspec > part->special_cap) {
                         rc = fail(GMI_ERR_OUT_OF_MEMORY, "more than " + std::to_string(part->special_cap) +
                                                              " fallback pixels");
