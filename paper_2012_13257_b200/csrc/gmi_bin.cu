@@ -636,7 +636,7 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
     // device geometry (no host round trip) when the frame-derived bin array
     // stays small; otherwise the exact host geometry with the reference cap
     const int64_t cells = static_cast<int64_t>(cap) * cap;
-    if (hot && cells <= (int64_t(1) << 22) && cells * B <= (int64_t(1) << 26)) {
+    if (hot && cells <= (int64_t(1) << 24) && cells * B <= (int64_t(1) << 27)) {
         const int64_t stride = cells + 1;
         c->geom_h.clear();
         c->grid_cap = cap;

@@ -318,6 +318,24 @@ __device__ int nearest_exact(const SpecParams& p, const Geom& g, int b,
     const int cap_x = max(abs(qcx), abs(qcx - (g.n_cols - 1)));
     const int cap_y = max(abs(qcy), abs(qcy - (g.n_rows - 1)));
     const int ring_cap = max(cap_x, cap_y);
+    // lane-parallel over the cells of a ring (8 R cells), each lane scanning
+    // its cell's points in turn; the bound is checked between rings exactly
+    // as the reference does, so the set of rings visited is the same
+    auto scan_cell_serial = [&](int gx, int gy) {
+        if (gx < 0 || gx >= g.n_cols || gy < 0 || gy >= g.n_rows) return;
+        const int64_t bin = g.bin_off + static_cast<int64_t>(gy) * g.n_cols + gx;
+        const int s = p.bins[bin], e = p.bins[bin + 1];
+        for (int k = s; k < e; ++k) {
+            float px, py;
+            int i;
+            point_at(p, base + k, px, py, i);
+            const double d2 = d2_ref(qx, qy, static_cast<double>(px), static_cast<double>(py));
+            if (d2 < best || (d2 == best && i < bi)) {
+                best = d2;
+                bi = i;
+            }
+        }
+    };
     for (int ring = 0; ring <= ring_cap; ++ring) {
         double wb = best;
         int wi = bi;
@@ -330,13 +348,23 @@ __device__ int nearest_exact(const SpecParams& p, const Geom& g, int b,
             scan_cell(qcx, qcy);
             continue;
         }
-        for (int gx = qcx - ring; gx <= qcx + ring; ++gx) {
-            scan_cell(gx, qcy - ring);
-            scan_cell(gx, qcy + ring);
-        }
-        for (int gy = qcy - ring + 1; gy <= qcy + ring - 1; ++gy) {
-            scan_cell(qcx - ring, gy);
-            scan_cell(qcx + ring, gy);
+        const int side = 2 * ring + 1;
+        for (int c = lane; c < 8 * ring; c += 32) {
+            int gx, gy;
+            if (c < side) {
+                gx = qcx - ring + c;
+                gy = qcy - ring;
+            } else if (c < 2 * side) {
+                gx = qcx - ring + (c - side);
+                gy = qcy + ring;
+            } else if (c < 2 * side + side - 2) {
+                gx = qcx - ring;
+                gy = qcy - ring + 1 + (c - 2 * side);
+            } else {
+                gx = qcx + ring;
+                gy = qcy - ring + 1 + (c - 2 * side - (side - 2));
+            }
+            scan_cell_serial(gx, gy);
         }
     }
     warp_argmin(best, bi);
