@@ -275,6 +275,9 @@ k_backward_points(BwdParams p) {
     if (staged) {
         // 8-byte alignment of a pixel pair in W / upstream / image rows
         const bool vec = (p.W % 2 == 0) && (CG == p.C);
+        const bool vec4 = CG == 4 && (p.C % 4) == 0 && (p.W % 2) == 0 &&
+                          (reinterpret_cast<uintptr_t>(p.upstream) & 15) == 0 &&
+                          (reinterpret_cast<uintptr_t>(p.image) & 15) == 0;
         // rows by warps, pixel pairs by lanes (coalesced, no index division)
         const int nrows = ry1 - ry0 + 1;
         for (int row = tid >> 5; row < nrows; row += kThreads / 32)
@@ -306,6 +309,26 @@ k_backward_points(BwdParams p) {
                     ub[c] = upv[CG + c] * ib;
                     va = fmaf(ua[c], imv[c], va);
                     vb = fmaf(ub[c], imv[CG + c], vb);
+                }
+            } else if (vec4 && xa >= 0 && xa + 1 < p.W && yy < p.H) {
+                // channel group of 4 inside C % 4 == 0 channels: 128-bit
+                // loads of the group's slice of both pixels
+                const size_t pix = img_base + static_cast<size_t>(yy) * p.W + xa;
+                const float2 wv = *reinterpret_cast<const float2*>(p.wsum + pix);
+                const float4 ua4 = *reinterpret_cast<const float4*>(p.upstream + pix * p.C + ch0);
+                const float4 ub4 = *reinterpret_cast<const float4*>(p.upstream + (pix + 1) * p.C + ch0);
+                const float4 oa4 = *reinterpret_cast<const float4*>(p.image + pix * p.C + ch0);
+                const float4 ob4 = *reinterpret_cast<const float4*>(p.image + (pix + 1) * p.C + ch0);
+                const float ia = wv.x > 0.f ? 1.0f / wv.x : 0.f;
+                const float ib = wv.y > 0.f ? 1.0f / wv.y : 0.f;
+                const float uav[4] = {ua4.x, ua4.y, ua4.z, ua4.w}, ubv[4] = {ub4.x, ub4.y, ub4.z, ub4.w};
+                const float oav[4] = {oa4.x, oa4.y, oa4.z, oa4.w}, obv[4] = {ob4.x, ob4.y, ob4.z, ob4.w};
+#pragma unroll
+                for (int c = 0; c < CG; ++c) {
+                    ua[c] = uav[c] * ia;
+                    ub[c] = ubv[c] * ib;
+                    va = fmaf(ua[c], oav[c], va);
+                    vb = fmaf(ub[c], obv[c], vb);
                 }
             } else {
                 pixel_terms<CG>(p, img_base, ch0, nch, xa, yy, ua, va);
