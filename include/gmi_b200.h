@@ -183,6 +183,28 @@ int gmi_bin_grid_host(gmi_ctx* ctx, const float* positions, int32_t batch,
                       int32_t* n_cols, int32_t* n_rows, int32_t* bin_start,
                       int32_t* point_index);
 
+/* ---- point optimisation: optimize_points (optimize.hpp:43-46,
+ * optimize.cpp:47-98) -------------------------------------------------------
+ * `steps` rounds of: forward -> L1 loss against target (l1_loss_and_grad,
+ * optimize.cpp:12-28: loss = mean |pred - target|, upstream = sign/(H*W*C))
+ * -> backward -> descent (positions -= lr * d_positions; colours clamped to
+ * [0,1] after colours -= lr * d_colors), the bin grid rebuilt on the device in
+ * every forward.  positions[B][N][2] / colors[B][N][C] are updated in place
+ * (DEVICE buffers); target[B][H][W][C] on the device; loss_curve, if not NULL,
+ * receives B x (steps + 1) losses on the HOST (step 0 = the initial points).
+ * flags: GMI_OPT_POSITIONS | GMI_OPT_COLORS.  steps >= 1 and a finite
+ * learning_rate >= 0, else ConfigInvalid (optimize.cpp:32-44). */
+enum { GMI_OPT_POSITIONS = 1, GMI_OPT_COLORS = 2 };
+int gmi_optimize_points(gmi_ctx* ctx, float* positions, float* colors, int32_t batch,
+                        int32_t num_points, int32_t channels, const gmi_config* cfg,
+                        const float* target, int32_t steps, double learning_rate,
+                        uint32_t flags, double* loss_curve);
+/* Same with HOST buffers (copied in and back inside the call). */
+int gmi_optimize_points_host(gmi_ctx* ctx, float* positions, float* colors, int32_t batch,
+                             int32_t num_points, int32_t channels, const gmi_config* cfg,
+                             const float* target, int32_t steps, double learning_rate,
+                             uint32_t flags, double* loss_curve);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

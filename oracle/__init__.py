@@ -107,10 +107,29 @@ class Reference:
         L.ref_oracle_gradients_fd.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _dp, C.c_double, _dp, _dp]
         L.ref_random_instance.argtypes = [C.c_uint64, C.c_int, C.c_int, _ip, _ip, _ip, _ip, _dp, _dp, _dp]
         L.ref_rng_u64.argtypes = [C.c_uint64, C.c_int, _u64p]
+        L.ref_optimize_points.argtypes = [_dp, _dp, C.c_int, C.c_int, _dp, C.c_int, C.c_int,
+                                          C.c_double, C.c_double, C.c_int, C.c_int, C.c_double,
+                                          C.c_int, C.c_int, _dp, _dp, _dp]
 
     def _check(self, rc):
         if rc != 0:
             raise OracleError(rc, self.lib.ref_last_error().decode())
+
+    def optimize_points(self, pos, col, target, sigma, cutoff, steps, lr, opt_pos=True,
+                        opt_col=False, fallback=0):
+        """gmi::optimize_points (optimize.cpp:47-98) -> (positions, colors, loss_curve)."""
+        pos = np.ascontiguousarray(pos, np.float64)
+        col = np.ascontiguousarray(col, np.float64)
+        tgt = np.ascontiguousarray(target, np.float64)
+        n, ch = col.shape
+        h, w = tgt.shape[:2]
+        op = np.zeros_like(pos)
+        oc = np.zeros_like(col)
+        loss = np.zeros(steps + 1)
+        self._check(self.lib.ref_optimize_points(
+            _ptr(pos, _dp), _ptr(col, _dp), n, ch, _ptr(tgt, _dp), w, h, sigma, cutoff, fallback,
+            steps, lr, int(opt_pos), int(opt_col), _ptr(op, _dp), _ptr(oc, _dp), _ptr(loss, _dp)))
+        return op, oc, loss
 
     def gaussian_weight(self, qx, qy, mx, my, sigma):
         return self.lib.ref_gaussian_weight(qx, qy, mx, my, sigma)

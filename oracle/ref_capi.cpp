@@ -21,6 +21,7 @@
 
 #include "gmi/bin_grid.hpp"
 #include "gmi/engine.hpp"
+#include "gmi/optimize.hpp"
 #include "gmi/oracle.hpp"
 #include "gmi/rng.hpp"
 #include "gmi/validate.hpp"
@@ -272,6 +273,35 @@ void ref_rng_u64(std::uint64_t seed, int k, std::uint64_t* out) {
     for (int i = 0; i < k; ++i) {
         out[i] = rng.next_u64();
     }
+}
+
+// gmi::optimize_points (optimize.cpp:47-98): `steps` rounds of forward -> L1
+// loss (l1_loss_and_grad, optimize.cpp:12-28) -> backward -> descent, the bin
+// grid rebuilt inside every forward.  Final positions / colours and the loss
+// curve (steps + 1 entries) are copied out.
+int ref_optimize_points(const double* pos, const double* col, int n, int channels,
+                        const double* target, int width, int height, double sigma,
+                        double cutoff, int fallback, int steps, double lr, int opt_pos,
+                        int opt_col, double* out_pos, double* out_col, double* loss_curve) {
+    return guarded([&] {
+        const gmi::PointSet ps = make_points(pos, col, n, channels);
+        gmi::ImageBuffer tgt = gmi::ImageBuffer::zeros(height, width, channels);
+        tgt.data.assign(target, target + static_cast<std::size_t>(height) * width * channels);
+        gmi::OptimConfig oc;
+        oc.steps = steps;
+        oc.learning_rate = lr;
+        oc.optimize_positions = opt_pos != 0;
+        oc.optimize_colors = opt_col != 0;
+        oc.log_every = steps > 0 ? steps : 1;
+        const gmi::OptimResult r =
+            gmi::optimize_points(ps, tgt, make_cfg(sigma, cutoff, fallback, width, height), oc, 1);
+        for (int i = 0; i < n; ++i) {
+            out_pos[2 * i] = r.points.positions[i].x;
+            out_pos[2 * i + 1] = r.points.positions[i].y;
+        }
+        std::memcpy(out_col, r.points.colors.data(), sizeof(double) * r.points.colors.size());
+        std::memcpy(loss_curve, r.loss_curve.data(), sizeof(double) * r.loss_curve.size());
+    });
 }
 
 }  // extern "C"

@@ -38,7 +38,7 @@ from ._lib import GmiConfig, lib
 __all__ = [
     "ForwardCache", "GmiError", "PointSet", "backward", "forward", "gaussian_weight",
     "forward_batch", "backward_batch", "Context", "bin_grid", "forward_counts",
-    "default_context", "ERROR_NAMES", "__version__",
+    "default_context", "optimize_points", "ERROR_NAMES", "__version__",
 ]
 
 __version__ = "0.1.0"
@@ -377,6 +377,61 @@ def backward(points: PointSet, cache: ForwardCache, upstream, sigma: float, radi
     dc, dp = backward_batch(points._pos32[None], points._col32[None], cache, up[None], sigma,
                             radius, fallback)
     return dc[0].astype(np.float64), dp[0].astype(np.float64)
+
+
+def optimize_points(points: PointSet, target, sigma: float, radius: float = 0.0,
+                    steps: int = 100, learning_rate: float = 0.5,
+                    optimize_positions: bool = True, optimize_colors: bool = False,
+                    log_every: int = 10, workers: int = 1, ctx: Context | None = None) -> dict:
+    """gmi._core.optimize_points (bindings.cpp:282-322, optimize.cpp:47-98) on
+    the GPU: render -> L1 loss -> backward -> descent, `steps` times, the bin
+    grid rebuilt on the device in every render.  Returns the reference's dict:
+    points, loss_curve (steps + 1), trajectory [(step, i, x, y, loss)] at step
+    0, every log_every and the last step, mean/max displacement."""
+    if not isinstance(points, PointSet):
+        raise TypeError("points must be a PointSet")
+    if log_every < 1:
+        raise GmiError(6, "log_every must be >= 1")
+    ctx = ctx or default_context()
+    tgt = _upstream_array(target).astype(np.float32)
+    h, w = tgt.shape[:2]
+    if tgt.shape[2] != points.channels:
+        raise GmiError(4, "target channels do not match the point set")
+    cfg = _interp_config(sigma, radius, "nearest", w, h)
+    pos = points._pos32.copy()
+    col = points._col32.copy()
+    n, ch = col.shape
+    flags = (1 if optimize_positions else 0) | (2 if optimize_colors else 0)
+    fp = C.POINTER(C.c_float)
+    loss_curve, trajectory = [], []
+
+    def log(step, loss):
+        for i in range(n):
+            trajectory.append((step, i, float(pos[i, 0]), float(pos[i, 1]), float(loss)))
+
+    # segments of log_every steps: the trajectory needs the positions at the
+    # logged steps; each segment's first loss is the previous segment's last
+    pos0 = pos.copy()
+    done = 0
+    while done < steps:
+        seg = min(log_every - done % log_every, steps - done)
+        lc = np.zeros(seg + 1, np.float64)
+        _check(lib.gmi_optimize_points_host(ctx.handle, pos.ctypes.data_as(fp), col.ctypes.data_as(fp),
+                                            1, n, ch, C.byref(cfg), tgt.ctypes.data_as(fp), seg,
+                                            float(learning_rate), flags,
+                                            lc.ctypes.data_as(C.POINTER(C.c_double))))
+        if done == 0:
+            loss_curve.append(lc[0])
+            trajectory.extend((0, i, float(pos0[i, 0]), float(pos0[i, 1]), float(lc[0]))
+                              for i in range(n))
+        loss_curve.extend(lc[1:].tolist())
+        done += seg
+        log(done, lc[-1])
+    pts = PointSet(pos.astype(np.float64), col.astype(np.float64))
+    d = np.hypot(*(pos.astype(np.float64) - pos0.astype(np.float64)).T)
+    return {"points": pts, "loss_curve": np.asarray(loss_curve), "trajectory": trajectory,
+            "mean_displacement": float(d.mean()) if n else 0.0,
+            "max_displacement": float(d.max()) if n else 0.0}
 
 
 def forward_counts(cache: ForwardCache) -> np.ndarray:

@@ -64,6 +64,12 @@ SIGNATURES = {
                                _ip, _ip]),
     "gmi_bin_grid_host": (C.c_int, [_vp, _fp, C.c_int32, C.c_int32, C.c_double, _dp, _ip, _ip,
                                     _ip, _ip]),
+    "gmi_optimize_points": (C.c_int, [_vp, _vp, _vp, C.c_int32, C.c_int32, C.c_int32,
+                                      C.POINTER(GmiConfig), _vp, C.c_int32, C.c_double,
+                                      C.c_uint32, _dp]),
+    "gmi_optimize_points_host": (C.c_int, [_vp, _fp, _fp, C.c_int32, C.c_int32, C.c_int32,
+                                           C.POINTER(GmiConfig), _fp, C.c_int32, C.c_double,
+                                           C.c_uint32, _dp]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

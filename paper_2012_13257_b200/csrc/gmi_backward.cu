@@ -416,9 +416,9 @@ k_backward_points(BwdParams p) {
         for (int c = 0; c < CG; ++c) dcol[c] = f2(0.f, 0.f);
         float2 gx2 = f2(0.f, 0.f);
         float gy = 0.f;
-        const float tx = truncf(mx), ty = truncf(my);
-        const float fmu = mx - tx, fmy = my - ty;  // exact
-        const int bx = static_cast<int>(tx), by = static_cast<int>(ty);
+        const float tx = truncf(mx);
+        const float fmu = mx - tx;  // exact
+        const int bx = static_cast<int>(tx);
         // rows that can hold an in-ball pixel: a safe point's boundary rows are
         // decided by the fp32 test below, so a small pad (>> fp32 rounding of
         // my +- r) suffices; flagged points keep a one-row margin for the f64

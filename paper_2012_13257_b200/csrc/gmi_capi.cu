@@ -251,6 +251,117 @@ int do_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
     return GMI_OK;
 }
 
+// ---- optimize_points (optimize.cpp:12-98) ----
+constexpr int kLossThreads = 256;
+
+// l1_loss_and_grad (optimize.cpp:12-28) per image: upstream = sign(pred -
+// target) / (H W C) (sign(0) = 0) and per-block f64 partial sums of |d|,
+// reduced in block order by k_loss_finalize (deterministic).
+__global__ void k_l1_loss_grad(const float* __restrict__ pred, const float* __restrict__ target,
+                               float* __restrict__ up, size_t per_img, double inv,
+                               double* __restrict__ partial) {
+    __shared__ double red[kLossThreads / 32];
+    const int b = blockIdx.y;
+    const size_t base = static_cast<size_t>(b) * per_img;
+    double s = 0.0;
+    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < per_img;
+         k += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const double d = static_cast<double>(pred[base + k]) - static_cast<double>(target[base + k]);
+        s += fabs(d);
+        up[base + k] = static_cast<float>(d > 0.0 ? inv : (d < 0.0 ? -inv : 0.0));
+    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kLossThreads / 32; ++w) t += red[w];
+        partial[static_cast<size_t>(b) * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+__global__ void k_loss_finalize(const double* __restrict__ partial, int nblk, double inv,
+                                double* __restrict__ loss, int stride, int step, int B) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    double t = 0.0;
+    for (int k = 0; k < nblk; ++k) t += partial[static_cast<size_t>(b) * nblk + k];
+    loss[static_cast<size_t>(b) * stride + step] = t * inv;
+}
+
+// descent update (optimize.cpp:80-96), in f64 then rounded to the fp32 state
+__global__ void k_descent(float* __restrict__ pos, float* __restrict__ col,
+                          const float* __restrict__ d_pos, const float* __restrict__ d_col,
+                          size_t n_pts, int C, double lr, uint32_t flags) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= n_pts) return;
+    if (flags & GMI_OPT_POSITIONS) {
+        pos[2 * i] = static_cast<float>(static_cast<double>(pos[2 * i]) - lr * d_pos[2 * i]);
+        pos[2 * i + 1] =
+            static_cast<float>(static_cast<double>(pos[2 * i + 1]) - lr * d_pos[2 * i + 1]);
+    }
+    if (flags & GMI_OPT_COLORS) {
+        for (int c = 0; c < C; ++c) {
+            const double v = static_cast<double>(col[i * C + c]) - lr * d_col[i * C + c];
+            col[i * C + c] = static_cast<float>(fmin(fmax(v, 0.0), 1.0));
+        }
+    }
+}
+
+int do_optimize(gmi_ctx* ctx, float* pos, float* col, int B, int N, int C,
+                const gmi_config* cfg, const float* target, int steps, double lr,
+                uint32_t flags, double* loss_curve) {
+    const size_t hwc = static_cast<size_t>(cfg->height) * cfg->width * C;
+    const size_t BN = static_cast<size_t>(B) * N;
+    float* img = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * B * hwc));
+    float* up = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * B * hwc));
+    float* dcol = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * BN * C));
+    float* dpos = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * BN * 2));
+    const int nblk = static_cast<int>(std::min<size_t>((hwc + kLossThreads - 1) / kLossThreads,
+                                                       std::max(1, 2 * ctx->num_sms / B + 1)));
+    double* partial = static_cast<double*>(gmi_host::dalloc(ctx, sizeof(double) * B * nblk));
+    double* loss = static_cast<double*>(gmi_host::dalloc(ctx, sizeof(double) * B * (steps + 1)));
+    const double inv = 1.0 / static_cast<double>(hwc);
+    ensure_issue(ctx, B);
+    const uint32_t saved = ctx->flags;
+    ctx->flags |= GMI_CTX_ASYNC_ERRORS;
+    int rc = GMI_OK;
+    try {
+        for (int step = 0; step <= steps && rc == GMI_OK; ++step) {
+            gmi_cache c;
+            c.ctx = ctx;
+            rc = do_forward(ctx, pos, col, B, N, C, cfg, img, &c, nullptr);
+            if (rc == GMI_OK) {
+                k_l1_loss_grad<<<dim3(nblk, B), kLossThreads, 0, ctx->stream>>>(img, target, up, hwc, inv,
+                                                                                partial);
+                GMI_LAUNCHED(ctx);
+                k_loss_finalize<<<(B + 63) / 64, 64, 0, ctx->stream>>>(partial, nblk, inv, loss, steps + 1,
+                                                                       step, B);
+                GMI_LAUNCHED(ctx);
+                if (step < steps) {
+                    backward_part(ctx, &c, up, dcol, dpos);
+                    k_descent<<<static_cast<unsigned>((BN + 255) / 256), 256, 0, ctx->stream>>>(
+                        pos, col, dpos, dcol, BN, C, lr, flags);
+                    GMI_LAUNCHED(ctx);
+                }
+            }
+            free_cache_buffers(&c);
+        }
+    } catch (...) {
+        ctx->flags = saved;
+        throw;
+    }
+    ctx->flags = saved;
+    if (rc == GMI_OK && loss_curve != nullptr)
+        GMI_CUDA(cudaMemcpyAsync(loss_curve, loss, sizeof(double) * B * (steps + 1),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+    for (void* q : {static_cast<void*>(img), static_cast<void*>(up), static_cast<void*>(dcol),
+                    static_cast<void*>(dpos), static_cast<void*>(partial), static_cast<void*>(loss)})
+        gmi_host::dfree(ctx, q);
+    if (rc == GMI_OK) rc = collect_issue(ctx, B);  // synchronises
+    return rc;
+}
+
 }  // namespace
 
 void host_trace(const char* what) {
@@ -846,6 +957,61 @@ int gmi_bin_grid_host(gmi_ctx* ctx, const float* positions, int32_t batch, int32
         const int rc = gmi_bin_grid(ctx, d, batch, num_points, cell_size, origin, n_cols, n_rows,
                                     bin_start, point_index);
         gmi_host::dfree(ctx, d);
+        GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+        return rc;
+    });
+}
+
+int gmi_optimize_points(gmi_ctx* ctx, float* positions, float* colors, int32_t batch,
+                        int32_t num_points, int32_t channels, const gmi_config* cfg,
+                        const float* target, int32_t steps, double learning_rate,
+                        uint32_t flags, double* loss_curve) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr || target == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "null argument");
+        int rc = check_points(positions, colors, batch, num_points, channels);
+        if (rc) return rc;
+        rc = check_config(cfg);
+        if (rc) return rc;
+        // check_optim_config (optimize.cpp:32-44)
+        if (steps < 1) return fail(GMI_ERR_CONFIG_INVALID, "steps must be >= 1");
+        if (!std::isfinite(learning_rate) || learning_rate < 0.0)
+            return fail(GMI_ERR_CONFIG_INVALID, "learning_rate must be finite and >= 0");
+        GMI_CUDA(cudaSetDevice(ctx->device));
+        return do_optimize(ctx, positions, colors, batch, num_points, channels, cfg, target, steps,
+                           learning_rate, flags, loss_curve);
+    });
+}
+
+int gmi_optimize_points_host(gmi_ctx* ctx, float* positions, float* colors, int32_t batch,
+                             int32_t num_points, int32_t channels, const gmi_config* cfg,
+                             const float* target, int32_t steps, double learning_rate,
+                             uint32_t flags, double* loss_curve) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr || positions == nullptr || colors == nullptr || target == nullptr || cfg == nullptr)
+            return fail(GMI_ERR_INVALID_ARGUMENT, "null argument");
+        if (batch < 1 || num_points < 1 || channels < 1)
+            return check_points(positions, colors, batch, num_points, channels);
+        GMI_CUDA(cudaSetDevice(ctx->device));
+        const size_t BN = static_cast<size_t>(batch) * num_points;
+        const size_t img = static_cast<size_t>(batch) * cfg->height * cfg->width * channels;
+        float* dp = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * BN * 2));
+        float* dc = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * BN * channels));
+        float* dt = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * img));
+        GMI_CUDA(cudaMemcpyAsync(dp, positions, sizeof(float) * BN * 2, cudaMemcpyHostToDevice, ctx->stream));
+        GMI_CUDA(cudaMemcpyAsync(dc, colors, sizeof(float) * BN * channels, cudaMemcpyHostToDevice,
+                                 ctx->stream));
+        GMI_CUDA(cudaMemcpyAsync(dt, target, sizeof(float) * img, cudaMemcpyHostToDevice, ctx->stream));
+        const int rc = gmi_optimize_points(ctx, dp, dc, batch, num_points, channels, cfg, dt, steps,
+                                           learning_rate, flags, loss_curve);
+        if (rc == GMI_OK) {
+            GMI_CUDA(cudaMemcpyAsync(positions, dp, sizeof(float) * BN * 2, cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+            GMI_CUDA(cudaMemcpyAsync(colors, dc, sizeof(float) * BN * channels, cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+        }
+        gmi_host::dfree(ctx, dp);
+        gmi_host::dfree(ctx, dc);
+        gmi_host::dfree(ctx, dt);
         GMI_CUDA(cudaStreamSynchronize(ctx->stream));
         return rc;
     });

@@ -281,3 +281,28 @@ def test_band_split_matches_full_frame(gmi, ctx, orc):
         g_pos[plan.idx] += dp[0]
     assert_close(g_col, rdc, what="band d_colors")
     assert_close(g_pos, rdp, what="band d_positions")
+
+
+@pytest.mark.parametrize("opt", [(True, False), (False, True), (True, True)])
+def test_optimize_points_matches_reference(gmi, ctx, opt):
+    """optimize_points (optimize.cpp:47-98) on the device against the
+    reference's own loop (oracle/_ref): loss curve and final points."""
+    import oracle
+
+    if not oracle.reference_available():
+        pytest.skip("oracle/_ref not built")
+    ref = oracle.Reference()
+    rng = np.random.default_rng(11)
+    W, H, N, steps, lr = 40, 32, 500, 6, 0.5
+    pos = f32(np.stack([rng.uniform(-0.5, W - 0.5, N), rng.uniform(-0.5, H - 0.5, N)], 1))
+    col = f32(rng.uniform(0, 1, (N, 3)))
+    tgt = f32(rng.uniform(0, 1, (H, W, 3)))
+    rp, rc, rl = ref.optimize_points(pos, col, tgt, 1.0, 3.0, steps, lr, *opt)
+    out = gmi.optimize_points(gmi.PointSet(pos, col), tgt, 1.0, steps=steps, learning_rate=lr,
+                              optimize_positions=opt[0], optimize_colors=opt[1], log_every=4,
+                              ctx=ctx)
+    assert_close(out["loss_curve"], rl, what="loss curve")
+    assert_close(out["points"].positions, rp, what="positions")
+    assert_close(out["points"].colors, rc, what="colors")
+    steps_logged = sorted({e[0] for e in out["trajectory"]})
+    assert steps_logged == [0, 4, 6]
