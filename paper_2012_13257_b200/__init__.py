@@ -382,7 +382,8 @@ def backward(points: PointSet, cache: ForwardCache, upstream, sigma: float, radi
 def optimize_points(points: PointSet, target, sigma: float, radius: float = 0.0,
                     steps: int = 100, learning_rate: float = 0.5,
                     optimize_positions: bool = True, optimize_colors: bool = False,
-                    log_every: int = 10, workers: int = 1, ctx: Context | None = None) -> dict:
+                    log_every: int = 10, workers: int = 1, ctx: Context | None = None,
+                    log_trajectory: bool = True) -> dict:
     """gmi._core.optimize_points (bindings.cpp:282-322, optimize.cpp:47-98) on
     the GPU: render -> L1 loss -> backward -> descent, `steps` times, the bin
     grid rebuilt on the device in every render.  Returns the reference's dict:
@@ -406,6 +407,8 @@ def optimize_points(points: PointSet, target, sigma: float, radius: float = 0.0,
     loss_curve, trajectory = [], []
 
     def log(step, loss):
+        if not log_trajectory:
+            return
         for i in range(n):
             trajectory.append((step, i, float(pos[i, 0]), float(pos[i, 1]), float(loss)))
 
@@ -422,8 +425,9 @@ def optimize_points(points: PointSet, target, sigma: float, radius: float = 0.0,
                                             lc.ctypes.data_as(C.POINTER(C.c_double))))
         if done == 0:
             loss_curve.append(lc[0])
-            trajectory.extend((0, i, float(pos0[i, 0]), float(pos0[i, 1]), float(lc[0]))
-                              for i in range(n))
+            if log_trajectory:
+                trajectory.extend((0, i, float(pos0[i, 0]), float(pos0[i, 1]), float(lc[0]))
+                                  for i in range(n))
         loss_curve.extend(lc[1:].tolist())
         done += seg
         log(done, lc[-1])

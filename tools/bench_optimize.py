@@ -27,16 +27,16 @@ def main():
     col = rng.uniform(0, 1, (a.points, 3)).astype(np.float32)
     tgt = rng.uniform(0, 1, (H, W, 3)).astype(np.float32)
     ps = gmi.PointSet(pos, col)
-    gmi.optimize_points(ps, tgt, 1.0, steps=2, log_every=100)  # warm-up
+    gmi.optimize_points(ps, tgt, 1.0, steps=2, log_every=100, log_trajectory=False)  # warm-up
     t0 = time.perf_counter()
-    out = gmi.optimize_points(ps, tgt, 1.0, steps=a.steps, log_every=a.steps)
+    out = gmi.optimize_points(ps, tgt, 1.0, steps=a.steps, log_every=a.steps, log_trajectory=False)
     t_gpu = time.perf_counter() - t0
     line = {"metric": "optimize_points steps/s (render + L1 + backward + descent, rebinning)",
             "config": {"frame": [H, W], "points": a.points, "channels": 3, "sigma": 1.0,
                        "steps": a.steps},
             "gpu_steps_per_s": round(a.steps / t_gpu, 2),
             "loss_first_last": [float(out["loss_curve"][0]), float(out["loss_curve"][-1])]}
-    if oracle.reference_available():
+    if oracle.reference_available() and a.ref_steps > 0:
         ref = oracle.Reference()
         t0 = time.perf_counter()
         _, _, rl = ref.optimize_points(pos.astype(np.float64), col.astype(np.float64),
