@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib")
 INCLUDE = os.path.join(ROOT, "include")
 
-CU_SOURCES = ["gmi_bin.cu", "gmi_gather.cu", "gmi_forward.cu", "gmi_backward.cu", "gmi_capi.cu"]
+CU_SOURCES = ["gmi_bin.cu", "gmi_gather.cu", "gmi_forward.cu", "gmi_backward.cu", "gmi_wide.cu", "gmi_capi.cu"]
 HEADERS = ["gmi_common.cuh", "gmi_internal.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",

@@ -686,6 +686,8 @@ namespace gmi_host {
 
 void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
                      float* d_colors, float* d_positions) {
+    // C > 4 with the record layout: the wide-channel backward (gmi_wide.cu)
+    if (launch_backward_wide(ctx, c, upstream, d_colors, d_positions)) return;
     cudaStream_t st = ctx->stream;
     const int CG = c->C <= 4 ? c->C : 4;
     const int groups = (c->C + CG - 1) / CG;

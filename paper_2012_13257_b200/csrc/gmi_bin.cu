@@ -510,6 +510,148 @@ __global__ void __launch_bounds__(256) k_scatter_emit(ScatterEmitParams p) {
     }
 }
 
+// Record layout in index-ordered cells (wide-channel path, C > 4): thread
+// per slot, point i = tmp[slot]; the 32-byte record, all C colours and the
+// colour validation, as k_scatter_emit but in the reference's bin order.
+__global__ void __launch_bounds__(256) k_emit_rec(ScatterEmitParams p, const int32_t* __restrict__ tmp) {
+    const int b = blockIdx.y;
+    const size_t base = static_cast<size_t>(b) * p.N;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= p.N) return;
+    const int i = tmp[base + k];
+    const float2 v = p.pos[base + i];
+    const float* src = p.col + (base + i) * p.C;
+    float* dstc = p.ccol + (base + k) * p.C;
+    unsigned code = 0;
+    const bool vec = (p.C % 4) == 0 && (reinterpret_cast<uintptr_t>(p.col) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(p.ccol) & 15) == 0;
+    float c4[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int ch = 0; ch < p.C; ch += 4) {
+        float cv[4];
+        if (vec) {
+            const float4 t = *reinterpret_cast<const float4*>(src + ch);
+            cv[0] = t.x; cv[1] = t.y; cv[2] = t.z; cv[3] = t.w;
+            *reinterpret_cast<float4*>(dstc + ch) = t;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                cv[j] = ch + j < p.C ? src[ch + j] : 0.f;
+                if (ch + j < p.C) dstc[ch + j] = cv[j];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (ch + j < p.C && code == 0) {
+                if (!is_finite_f(cv[j])) code = 1;                // NonFiniteValue
+                else if (cv[j] < 0.0f || cv[j] > 1.0f) code = 2;  // ColorOutOfRange
+            }
+        }
+        if (ch == 0) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) c4[j] = cv[j];
+        }
+    }
+    if (code) atomicMin(p.issue + b, (static_cast<unsigned long long>(i) << 8) | code);
+    const bool amb = p.classify && point_ambiguous_fast(v.x, v.y, p.rf, p.r2f);
+    const uint32_t id = static_cast<uint32_t>(i) | (amb ? kUnsafeBit : 0u);
+    float4* r = p.rec + (base + k) * 2;
+    r[0] = make_float4(v.x, v.y, c4[0], c4[1]);
+    r[1] = make_float4(c4[2], c4[3], __uint_as_float(id), 0.f);
+}
+
+// Cells the fast gather may split across chunks (> its 1024-candidate
+// capacity) get their records in ascending original index, so chunk
+// membership — and the summation order — is independent of the atomic
+// arrival order (bit-deterministic results for clustered inputs).
+constexpr int kBigRecCell = 1024;   // = the fast gather's chunk capacity (kCap)
+constexpr int kBigRecSmem = 4096;   // cells up to this size sort in shared memory
+
+__global__ void k_find_big_cells(const Geom* __restrict__ geom, const int32_t* __restrict__ bins,
+                                 int2* __restrict__ big, int32_t* big_count) {
+    const int b = blockIdx.y;
+    const Geom g = geom[b];
+    const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+    if (cell >= g.n_cols * g.n_rows) return;
+    const int n = bins[g.bin_off + cell + 1] - bins[g.bin_off + cell];
+    if (n > kBigRecCell) big[atomicAdd(big_count, 1)] = make_int2(b, cell);
+}
+
+__device__ __forceinline__ uint32_t rec_idx(const float4& r1) {
+    return __float_as_uint(r1.z) & 0x7fffffffu;
+}
+
+__global__ void __launch_bounds__(512) k_sort_big_recs(int N, const Geom* __restrict__ geom,
+                                                       const int32_t* __restrict__ bins,
+                                                       float4* __restrict__ rec,
+                                                       const int2* __restrict__ big,
+                                                       const int32_t* __restrict__ big_count) {
+    extern __shared__ float4 sr[];  // [2 kBigRecSmem] records, then the keys
+    unsigned long long* key = reinterpret_cast<unsigned long long*>(sr + 2 * kBigRecSmem);
+    const int nbig = *big_count;
+    for (int job = blockIdx.x; job < nbig; job += gridDim.x) {
+        const int b = big[job].x, cell = big[job].y;
+        const Geom g = geom[b];
+        const int s = bins[g.bin_off + cell], n = bins[g.bin_off + cell + 1] - s;
+        float4* R = rec + (static_cast<size_t>(b) * N + s) * 2;
+        int np2 = 1;
+        while (np2 < n) np2 <<= 1;
+        if (n <= kBigRecSmem) {
+            for (int k = threadIdx.x; k < np2; k += blockDim.x) {
+                if (k < n) {
+                    sr[2 * k] = R[2 * k];
+                    sr[2 * k + 1] = R[2 * k + 1];
+                    key[k] = (static_cast<unsigned long long>(rec_idx(sr[2 * k + 1])) << 32) | k;
+                } else {
+                    key[k] = ~0ull;
+                }
+            }
+            __syncthreads();
+            for (int size = 2; size <= np2; size <<= 1) {
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (int k = threadIdx.x; k < np2; k += blockDim.x) {
+                        const int partner = (stride == (size >> 1)) ? (k ^ (size - 1)) : (k ^ stride);
+                        if (partner > k) {
+                            const unsigned long long a = key[k], c = key[partner];
+                            if (a > c) {
+                                key[k] = c;
+                                key[partner] = a;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            for (int k = threadIdx.x; k < n; k += blockDim.x) {
+                const int src = static_cast<int>(key[k] & 0xffffffffu);
+                R[2 * k] = sr[2 * src];
+                R[2 * k + 1] = sr[2 * src + 1];
+            }
+            __syncthreads();
+        } else {
+            // in place in global memory (pathological cells): bitonic on the
+            // records, partners past n skipped (all comparators ascending)
+            for (int size = 2; size <= np2; size <<= 1) {
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (int k = threadIdx.x; k < np2; k += blockDim.x) {
+                        const int partner = (stride == (size >> 1)) ? (k ^ (size - 1)) : (k ^ stride);
+                        if (partner > k && partner < n) {
+                            const float4 a1 = R[2 * k + 1], c1 = R[2 * partner + 1];
+                            if (rec_idx(a1) > rec_idx(c1)) {
+                                const float4 a0 = R[2 * k], c0 = R[2 * partner];
+                                R[2 * k] = c0;
+                                R[2 * k + 1] = c1;
+                                R[2 * partner] = a0;
+                                R[2 * partner + 1] = a1;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+        }
+    }
+}
+
 // k_count with 4 points per thread: 4 independent position loads and cell
 // atomics in flight per thread (the single-point kernel is latency bound).
 __global__ void __launch_bounds__(256) k_count4(const float2* __restrict__ pos, int N,
@@ -727,6 +869,23 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
         e.r2f = static_cast<float>(c->cutoff * c->cutoff);
         k_scatter_emit<<<pgrid4, 256, 0, st>>>(e);
         GMI_LAUNCHED(ctx);
+        // cells the gather may split: index order
+        int2* d_big = static_cast<int2*>(
+            scratch(ctx, WS_BIG, sizeof(int2) * std::max<size_t>(1, BN / (kBigRecCell + 1) + 1)));
+        int32_t* d_bigcount = static_cast<int32_t*>(scratch(ctx, WS_BIGCOUNT, sizeof(int32_t)));
+        GMI_CUDA(cudaMemsetAsync(d_bigcount, 0, sizeof(int32_t), st));
+        k_find_big_cells<<<dim3((max_bins + 127) / 128, B), 128, 0, st>>>(c->geom_d, c->bins, d_big,
+                                                                          d_bigcount);
+        GMI_LAUNCHED(ctx);
+        const int rsmem = kBigRecSmem * (2 * sizeof(float4) + sizeof(unsigned long long));
+        static int set_dev = -1;
+        if (set_dev != ctx->device) {
+            set_dev = ctx->device;
+            GMI_CUDA(cudaFuncSetAttribute(k_sort_big_recs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          rsmem));
+        }
+        k_sort_big_recs<<<ctx->num_sms, 512, rsmem, st>>>(N, c->geom_d, c->bins, c->rec, d_big, d_bigcount);
+        GMI_LAUNCHED(ctx);
         host_trace("bin: scatter_emit launched");
         return;
     }
@@ -747,6 +906,23 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
     GMI_LAUNCHED(ctx);
     if (!hot) {
         GMI_CUDA(cudaMemcpyAsync(point_index_out, tmp, sizeof(int32_t) * BN, cudaMemcpyDeviceToDevice, st));
+    } else if (c->rec != nullptr) {
+        // wide-channel path: records + colours in index-ordered cells
+        ScatterEmitParams e{};
+        e.pos = p2;
+        e.col = col;
+        e.geom = c->geom_d;
+        e.bins = c->bins;
+        e.rec = c->rec;
+        e.ccol = c->ccol;
+        e.issue = d_issue;
+        e.N = N;
+        e.C = c->C;
+        e.classify = classify ? 1 : 0;
+        e.rf = static_cast<float>(c->cutoff);
+        e.r2f = static_cast<float>(c->cutoff * c->cutoff);
+        k_emit_rec<<<pgrid, 256, 0, st>>>(e, tmp);
+        GMI_LAUNCHED(ctx);
     } else {
         EmitParams e{};
         e.pos = p2;

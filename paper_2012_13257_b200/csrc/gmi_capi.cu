@@ -189,7 +189,8 @@ int do_forward(gmi_ctx* ctx, const float* pos, const float* col, int B, int N,
         // fast gather: unordered cells and the 32-byte record layout;
         // otherwise index-ordered cells in SoA (the generic gather's order)
         const bool fast = gmi_host::gather_fast_ok(c);
-        c->sort_cells = !fast;
+        // C > 4 (wide gather): records and colours in index-ordered cells
+        c->sort_cells = !fast || C > 4;
         if (fast) {
             c->rec = static_cast<float4*>(gmi_host::cache_alloc(c, sizeof(float4) * 2 * BN));
             if (C > 4)

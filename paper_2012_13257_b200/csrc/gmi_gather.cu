@@ -205,7 +205,22 @@ k_gather(GatherParams p) {
                     off = 0;
                     continue;
                 }
-                const int take = min(ge - gs, kCap - tot);
+                int take = ge - gs;
+                if (take > kCap - tot) {
+                    // split at a cell boundary (chunk membership must not
+                    // depend on K1's arrival order inside a cell): the
+                    // longest prefix of whole cells that fits
+                    const int room = kCap - tot;
+                    int e = gs;
+                    for (int cx = cx0 + 1; cx <= cx1 + 1; ++cx) {
+                        const int bnd = p.bins[r0 + cx];
+                        if (bnd - gs > room) break;
+                        e = max(e, bnd);
+                    }
+                    if (e > gs) take = e - gs;
+                    else if (tot > 0) break;  // the next cell opens the next chunk
+                    else take = kCap;         // one cell > kCap: index-ordered by K1
+                }
                 S.run_g[n] = gs;
                 S.run_beg[n] = tot;
                 tot += take;
@@ -570,6 +585,8 @@ bool gather_fast_ok(const gmi_cache* c) {
 // (f64 weight mode, or a radius whose bin table exceeds the staging tables).
 bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts) {
     if (!gather_fast_ok(c)) return false;
+    // C > 4: the wide-channel gather (gmi_wide.cu) on index-ordered cells
+    if (launch_gather_wide(ctx, c, image, counts)) return true;
     const double r = c->cutoff;
     GatherParams p{};
     gather_geometry(r, p.rc, p.ncol, p.dyb, p.nyb);

@@ -135,7 +135,7 @@ struct gmi_cache {
     // dims <= grid_cap (geom_h is empty; the geometry lives only in geom_d)
     int grid_cap = 0;
     int64_t grid_stride = 0;
-    bool sort_cells = true;   // within-cell index order (generic gather)
+    bool sort_cells = true;   // within-cell index order (generic and wide gathers)
     // hot layout (sorted by cell, then fine x-column, then index)
     float* sx = nullptr;      // [B][N]
     float* sy = nullptr;      // [B][N]
@@ -184,6 +184,10 @@ int host_axis_cells(double span, double cell, int cap);
 void launch_forward(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts);
 bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts);
 bool gather_fast_ok(const gmi_cache* c);
+// wide-channel path (C > 4, gmi_wide.cu); false when it does not apply
+bool launch_gather_wide(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts);
+bool launch_backward_wide(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
+                          float* d_colors, float* d_positions);
 void launch_special_forward(gmi_ctx* ctx, gmi_cache* c, float* image,
                             int32_t* counts);
 

@@ -237,13 +237,15 @@ def test_batch_equals_single_calls(gmi, ctx, orc):
         assert np.array_equal(dc[b], d1[0]) and np.array_equal(dp[b], p1[0])
 
 
-def test_deterministic_repeat(gmi, ctx, orc):
-    pos, col, up = orc.synth_batch(12, 2, 20000, 3, 256, 256)
-    a = gmi.forward_batch(pos, col, 256, 256, 1.5, 4.5, ctx=ctx)
-    b = gmi.forward_batch(pos, col, 256, 256, 1.5, 4.5, ctx=ctx)
+@pytest.mark.parametrize("C,sigma", [(3, 1.5), (64, 4.0)])
+def test_deterministic_repeat(gmi, ctx, orc, C, sigma):
+    pos, col, up = orc.synth_batch(12, 2, 20000, C, 256, 256, cluster_frac=0.05, cluster_px=16)
+    r = 3 * sigma
+    a = gmi.forward_batch(pos, col, 256, 256, sigma, r, ctx=ctx)
+    b = gmi.forward_batch(pos, col, 256, 256, sigma, r, ctx=ctx)
     assert np.array_equal(a[0], b[0])
-    ga = gmi.backward_batch(pos, col, a[1], up, 1.5, 4.5, ctx=ctx)
-    gb = gmi.backward_batch(pos, col, b[1], up, 1.5, 4.5, ctx=ctx)
+    ga = gmi.backward_batch(pos, col, a[1], up, sigma, r, ctx=ctx)
+    gb = gmi.backward_batch(pos, col, b[1], up, sigma, r, ctx=ctx)
     assert np.array_equal(ga[0], gb[0]) and np.array_equal(ga[1], gb[1])
 
 

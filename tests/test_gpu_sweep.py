@@ -23,6 +23,13 @@ CASES = [
     (8, 2, 8000, 3, 160, 40, 1.5, 4.0, 1, 0.0, 0.05),
     (9, 1, 20000, 3, 64, 64, 1.0, 3.0, 0, 0.5, 0.0),
     (10, 1, 1500, 5, 50, 90, 4.0, 12.0, 0, 0.0, 0.0),
+    # wide-channel path (C > 4): pass widths 16 / 32 / 64, ragged C, dense
+    # clusters (multi-chunk tiles), points outside the frame
+    (11, 2, 3000, 64, 96, 80, 4.0, 12.0, 0, 0.05, 0.0),
+    (12, 1, 4000, 33, 70, 50, 1.5, 4.5, 1, 0.3, 0.05),
+    (13, 1, 2500, 16, 64, 64, 2.0, 6.0, 0, 0.0, 0.1),
+    (14, 1, 6000, 20, 80, 64, 1.0, 3.0, 0, 0.6, 0.0),
+    (15, 1, 1200, 130, 48, 40, 1.0, 3.0, 0, 0.0, 0.0),
 ]
 
 
