@@ -221,8 +221,9 @@ k_gather_wide(GatherWideParams p) {
                         i10 = eb.x >= thr;
                         i11 = eb.y >= thr;
                     }
-                    const float2 wa = f2(i00 ? ex2(ea.x) : 0.f, i01 ? ex2(ea.y) : 0.f);
-                    const float2 wb = f2(i10 ? ex2(eb.x) : 0.f, i11 ? ex2(eb.y) : 0.f);
+                    // branch-free: ex2(-inf) = +0 for pairs outside the ball
+                    const float2 wa = f2(ex2(i00 ? ea.x : -INFINITY), ex2(i01 ? ea.y : -INFINITY));
+                    const float2 wb = f2(ex2(i10 ? eb.x : -INFINITY), ex2(i11 ? eb.y : -INFINITY));
                     Wa = __fadd2_rn(Wa, wa);
                     Wb = __fadd2_rn(Wb, wb);
                     const float4* cp = &S.col[k][cb * kJ];
@@ -529,45 +530,69 @@ k_backward_wide(BwdWideParams p) {
     const int c4 = ch0 + 4 * cl;       // its first channel
 
     if (staged) {
-        // 4 lanes per pixel (16 channels), pixels row-major over the region
-        const bool vec = (p.C % 4) == 0 && (reinterpret_cast<uintptr_t>(p.upstream) & 15) == 0 &&
-                         (reinterpret_cast<uintptr_t>(p.image) & 15) == 0;
-        for (int kb = 0; kb < area; kb += kBThreads / 4) {
-            const int k = kb + (tid >> 2);
-            const int yy = ry0 + k / wd, xx = rx0 + k % wd;
-            float u[4] = {0.f, 0.f, 0.f, 0.f};
-            float vp = 0.f;
-            if (k < area && xx < p.W && yy < p.H) {
-                const size_t pix = img_base + static_cast<size_t>(yy) * p.W + xx;
-                const float wv = p.wsum[pix];
-                if (wv > 0.f) {
-                    const float inv = 1.0f / wv;
-                    float up[4], im[4];
-                    if (vec && c4 + 3 < p.C) {
-                        const float4 a = *reinterpret_cast<const float4*>(p.upstream + pix * p.C + c4);
-                        const float4 o = *reinterpret_cast<const float4*>(p.image + pix * p.C + c4);
-                        up[0] = a.x; up[1] = a.y; up[2] = a.z; up[3] = a.w;
-                        im[0] = o.x; im[1] = o.y; im[2] = o.z; im[3] = o.w;
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            up[c] = c4 + c < p.C ? p.upstream[pix * p.C + c4 + c] : 0.f;
-                            im[c] = c4 + c < p.C ? p.image[pix * p.C + c4 + c] : 0.f;
-                        }
-                    }
+        // 4 lanes per pixel (16 channels), pixels row-major over the region,
+        // two pixels per thread and iteration with all loads issued up front
+        const bool full = (p.C % 4) == 0 && c4 + 3 < p.C &&
+                          (reinterpret_cast<uintptr_t>(p.upstream) & 15) == 0 &&
+                          (reinterpret_cast<uintptr_t>(p.image) & 15) == 0;
+        constexpr int kStep = kBThreads / 4;
+        auto adv = [&](int& r, int& cc) {
+            cc += kStep;
+            while (cc >= wd) {
+                cc -= wd;
+                ++r;
+            }
+        };
+        auto load = [&](bool live, int r, int cc, float& w, float4& up, float4& im) {
+            const int yy = ry0 + r, xx = rx0 + cc;
+            const bool in = live && xx < p.W && yy < p.H;
+            const size_t pix = img_base + (in ? static_cast<size_t>(yy) * p.W + xx : 0);
+            w = 0.f;
+            up = make_float4(0.f, 0.f, 0.f, 0.f);
+            im = up;
+            if (in) {
+                w = p.wsum[pix];
+                if (full) {
+                    up = *reinterpret_cast<const float4*>(p.upstream + pix * p.C + c4);
+                    im = *reinterpret_cast<const float4*>(p.image + pix * p.C + c4);
+                } else {
+                    float t[8];
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
-                        u[c] = up[c] * inv;
-                        vp = fmaf(u[c], im[c], vp);
+                        t[c] = c4 + c < p.C ? p.upstream[pix * p.C + c4 + c] : 0.f;
+                        t[4 + c] = c4 + c < p.C ? p.image[pix * p.C + c4 + c] : 0.f;
                     }
+                    up = make_float4(t[0], t[1], t[2], t[3]);
+                    im = make_float4(t[4], t[5], t[6], t[7]);
                 }
             }
+        };
+        auto put = [&](bool live, int k, float w, const float4& up, const float4& im) {
+            const float inv = w > 0.f ? 1.0f / w : 0.f;  // W == 0: fallback pixel, zeros
+            const float4 u = make_float4(up.x * inv, up.y * inv, up.z * inv, up.w * inv);
+            float vp = fmaf(u.w, im.w, fmaf(u.z, im.z, fmaf(u.y, im.y, u.x * im.x)));
             vp += __shfl_xor_sync(0xffffffffu, vp, 1);
             vp += __shfl_xor_sync(0xffffffffu, vp, 2);
-            if (k < area) {
-                s_u4[4 * k + cl] = make_float4(u[0], u[1], u[2], u[3]);
+            if (live) {
+                s_u4[4 * k + cl] = u;
                 if (cl == 0) s_v[k] = vp;
             }
+        };
+        int rA = (tid >> 2) / wd, cA = (tid >> 2) - rA * wd;
+        int rB = rA, cB = cA;
+        adv(rB, cB);
+        for (int kb = 0; kb < area; kb += 2 * kStep) {
+            const int kA = kb + (tid >> 2), kB = kA + kStep;
+            float wA, wB;
+            float4 uA, oA, uB, oB;
+            load(kA < area, rA, cA, wA, uA, oA);
+            load(kB < area, rB, cB, wB, uB, oB);
+            put(kA < area, kA, wA, uA, oA);
+            put(kB < area, kB, wB, uB, oB);
+            adv(rA, cA);
+            adv(rA, cA);
+            adv(rB, cB);
+            adv(rB, cB);
         }
         __syncthreads();
     }
@@ -639,14 +664,18 @@ k_backward_wide(BwdWideParams p) {
             float R[4] = {0.f, 0.f, 0.f, 0.f};
             float vr = 0.f;
             if (staged) {
-                int kk = (y - ry0) * wd + (xs - rx0) + h;
+                // this lane's pixels x = xs + h + 2j, j in [j0, j1), all in [xl, xr]
+                const int j0 = mfirst ? 1 : 0, j1 = mlast ? np - 1 : np;
+                const int kk0 = (y - ry0) * wd + (xs - rx0) + h + 2 * j0;
+                const float4* pu = s_u4 + 4 * kk0 + cl;
+                const float* pv = s_v + kk0;
+                xf += static_cast<float>(2 * j0);
 #pragma unroll 2
-                for (int j = 0; j < np; ++j) {
-                    const float4 u = s_u4[4 * kk + cl];
-                    const float v = s_v[kk];
+                for (int j = j0; j < j1; ++j) {
+                    const float4 u = *pu;
+                    const float v = *pv;
                     const float dx = xf - mx;
-                    float w = ex2(fmaf(dx * nk, dx, ey));
-                    if ((j == 0 && mfirst) || (j == np - 1 && mlast)) w = 0.f;
+                    const float w = ex2(fmaf(dx * nk, dx, ey));
                     const float wdx = w * dx;
                     R[0] = fmaf(w, u.x, R[0]);
                     R[1] = fmaf(w, u.y, R[1]);
@@ -659,7 +688,8 @@ k_backward_wide(BwdWideParams p) {
                     vx = fmaf(wdx, v, vx);
                     vr = fmaf(w, v, vr);
                     xf += 2.f;
-                    kk += 2;
+                    pu += 8;
+                    pv += 2;
                 }
             } else {
                 for (int j = 0; j < np; ++j) {
