@@ -316,9 +316,10 @@ void launch_wide_cb(gmi_ctx* ctx, const GatherWideParams& p, dim3 grid) {
 // K4 wide
 // ---------------------------------------------------------------------------
 constexpr int kBG = 16;                 // channels per group
-constexpr int kBThreads = 256;          // 8 warps, one point each at a time
-constexpr int kBSmem = 110 * 1024;      // staged bytes (68 per pixel), 2 CTAs/SM
-constexpr int kBRunMax = 64;            // cell rows per block
+constexpr int kBThreads = 256;          // 8 warps x 4 squads of 8 lanes
+constexpr int kPlanePx = 1600;          // ring capacity in pixels (68 B each): 2 CTAs/SM
+constexpr int kBSmem = kPlanePx * 68;
+constexpr int kBSeg = 16;               // cell rows per CTA
 
 struct BwdWideParams {
     const Geom* geom;
@@ -330,7 +331,8 @@ struct BwdWideParams {
     const float* image;      // [B][H][W][C]
     const float* upstream;   // [B][H][W][C]
     int B, N, C, W, H;
-    int bs;                  // cells per block side
+    int seg;                 // cell rows per CTA (one cell column)
+    int nseg_cap;            // row segments per column (CTA index = column * nseg_cap + segment)
     double r64, r2_64;
     float nk, inv_s2;
     float* d_col;            // [B][N][C]
@@ -342,44 +344,59 @@ __device__ __forceinline__ bool in_ref_w(int x, int y, float mx, float my, doubl
                   static_cast<double>(my)) <= r2_64;
 }
 
-// u (this lane's 4 channels of the group) and the group's v at one pixel,
-// straight from global memory (unstaged blocks); v is summed over the 4
-// channel lanes of the pixel (lanes cl = 0..3 of the calling quad).
-__device__ __forceinline__ void pixel_u4(const BwdWideParams& p, size_t img_base, int c0, int x,
-                                         int y, float4& u, float& v, unsigned qmask) {
-    u = make_float4(0.f, 0.f, 0.f, 0.f);
-    float vp = 0.f;
-    if (x >= 0 && x < p.W && y >= 0 && y < p.H) {
-        const size_t pix = img_base + static_cast<size_t>(y) * p.W + x;
-        const float wv = p.wsum[pix];
-        if (wv > 0.f) {
-            const float inv = 1.0f / wv;
-            float uu[4];
+// The 16 channels of group ch0 at one pixel: w (W of the pixel), up and out.
+__device__ __forceinline__ void load_px16(const BwdWideParams& p, size_t pix, int ch0, bool full,
+                                          float& w, float* up, float* im) {
+    w = p.wsum[pix];
+    if (full) {
+        const float4* u4 = reinterpret_cast<const float4*>(p.upstream + pix * p.C + ch0);
+        const float4* o4 = reinterpret_cast<const float4*>(p.image + pix * p.C + ch0);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uu[c] = 0.f;
-                if (c0 + c < p.C) {
-                    uu[c] = p.upstream[pix * p.C + c0 + c] * inv;
-                    vp = fmaf(uu[c], p.image[pix * p.C + c0 + c], vp);
-                }
-            }
-            u = make_float4(uu[0], uu[1], uu[2], uu[3]);
+        for (int j = 0; j < 4; ++j) {
+            const float4 a = u4[j], o = o4[j];
+            up[4 * j] = a.x; up[4 * j + 1] = a.y; up[4 * j + 2] = a.z; up[4 * j + 3] = a.w;
+            im[4 * j] = o.x; im[4 * j + 1] = o.y; im[4 * j + 2] = o.z; im[4 * j + 3] = o.w;
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < kBG; ++c) {
+            up[c] = ch0 + c < p.C ? p.upstream[pix * p.C + ch0 + c] : 0.f;
+            im[c] = ch0 + c < p.C ? p.image[pix * p.C + ch0 + c] : 0.f;
         }
     }
-    vp += __shfl_xor_sync(qmask, vp, 1);
-    vp += __shfl_xor_sync(qmask, vp, 2);
-    v = vp;
 }
 
+// u_c = up_c / W and v = sum_c u_c out_c (zeros for W == 0: fallback pixel)
+__device__ __forceinline__ float pixel_uv(float w, float* u, const float* im) {
+    const float inv = w > 0.f ? 1.0f / w : 0.f;
+    float v = 0.f;
+#pragma unroll
+    for (int c = 0; c < kBG; ++c) {
+        u[c] *= inv;
+        v = fmaf(u[c], im[c], v);
+    }
+    return v;
+}
+
+// Column walk: CTA = (image, cell column, segment of kBSeg cell rows, group).
+// The pixel rows a cell's points reach (the cell grown by r) live in a ring
+// of rows in shared memory: 4 planes of float4 (u, 16 channels) + 1 plane of
+// v, pixel-major inside a plane, so 8 lanes on 8 consecutive pixels read 128
+// contiguous bytes per LDS.128 (conflict-free).  Consecutive cells of the
+// column share all but cell rows, which are the only ones staged.
+// Squad = 8 lanes owning ONE point: the squad walks the point's exact disk
+// row by row, lane l taking pixels xl + l, xl + l + 8, ..; per pixel
+//     t = sum_c u_c c_ic - v,  d_col_c += w u_c,  d_pos += w t (q - mu)
+// with all 16 channels of the group in the lane's registers (no cross-lane
+// work per pixel).  Squad sums are combined by a fixed shuffle tree.
 __global__ void __launch_bounds__(kBThreads, 2)
 k_backward_wide(BwdWideParams p) {
-    extern __shared__ float4 s_u4[];      // [area][4] float4, then s_v[area]
-    __shared__ int s_run[kBRunMax + 1];
-    __shared__ int s_rung[kBRunMax];
+    extern __shared__ float4 s_u4[];      // planes [4][kPlanePx] float4, then s_v[kPlanePx]
+    float* s_v = reinterpret_cast<float*>(s_u4 + 4 * kPlanePx);
     __shared__ float s_red[4][kBThreads / 32];
-    __shared__ int s_region[5];
+    __shared__ int s_reg[5];
 
-    // ---- image / cell block of this CTA ----
+    // ---- image, cell column and row segment of this CTA ----
     int b = 0;
     {
         int lo = 0, hi = p.B;
@@ -392,366 +409,294 @@ k_backward_wide(BwdWideParams p) {
     }
     const Geom g = p.geom[b];
     const int local = blockIdx.x - p.blk_off[b];
-    const int nbx = (g.n_cols + p.bs - 1) / p.bs;
-    const int cx0 = (local % nbx) * p.bs, cy0 = (local / nbx) * p.bs;
-    if (cy0 >= g.n_rows) return;  // past this image's grid (device geometry)
-    const int cx1 = min(cx0 + p.bs, g.n_cols), cy1 = min(cy0 + p.bs, g.n_rows);
+    const int cx = local / p.nseg_cap, sgm = local % p.nseg_cap;
+    const int cyA = sgm * p.seg;
+    if (cx >= g.n_cols || cyA >= g.n_rows) return;  // past this image's grid
+    const int cyB = min(cyA + p.seg, g.n_rows);
     const int cg = blockIdx.y, ch0 = cg * kBG;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int sq = lane >> 3, sl = lane & 7;
     const size_t base = static_cast<size_t>(b) * p.N;
-
-    // ---- point runs (one per cell row of the block) ----
-    const int nrun = cy1 - cy0;
-    if (tid < 32) {
-        int carry = 0;
-        for (int k0 = 0; k0 < nrun; k0 += 32) {
-            const int k = k0 + tid;
-            int len = 0, gs = 0;
-            if (k < nrun) {
-                const int64_t r0 = g.bin_off + static_cast<int64_t>(cy0 + k) * g.n_cols;
-                gs = p.bins[r0 + cx0];
-                len = p.bins[r0 + cx1] - gs;
-            }
-            int incl = len;
-            for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (tid >= o) incl += t;
-            }
-            if (k < nrun) {
-                s_run[k] = carry + incl - len;
-                s_rung[k] = gs;
-            }
-            carry += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        if (tid == 0) s_run[nrun] = carry;
-    }
-    __syncthreads();
-    const int total = s_run[nrun];
-    if (total == 0) return;
-    auto slot_of = [&](int k) -> int {
-        int lo = 0, hi = nrun;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (s_run[mid] <= k) lo = mid;
-            else hi = mid;
-        }
-        return s_rung[lo] + (k - s_run[lo]);
-    };
-
-    // ---- pixel region reached by the block's points (as k_backward_points) ----
-    if (tid == 0) {
-        s_region[4] = -2;
-        if (!g.capped) {
-            const double pad = p.r64 + 1.0;
-            const int x0 = max(0, static_cast<int>(floor(g.ox + cx0 * g.cell - pad))) & ~1;
-            const int y0 = max(0, static_cast<int>(floor(g.oy + cy0 * g.cell - pad)));
-            const int x1 = min(p.W - 1, static_cast<int>(ceil(g.ox + cx1 * g.cell + pad))) | 1;
-            const int y1 = min(p.H - 1, static_cast<int>(ceil(g.oy + cy1 * g.cell + pad)));
-            const long wd = (x1 >= x0) ? (x1 - x0 + 1) : 0;
-            const long area = (y1 >= y0) ? wd * (y1 - y0 + 1) : 0;
-            if (area <= 0) {
-                s_region[4] = -1;
-            } else if (area * 68 <= kBSmem) {
-                s_region[0] = x0;
-                s_region[1] = y0;
-                s_region[2] = x1;
-                s_region[3] = y1;
-                s_region[4] = 1;
-            }
-        }
-    }
-    __syncthreads();
-    if (s_region[4] == -2) {
-        float mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
-        for (int k = tid; k < total; k += kBThreads) {
-            const float4 ra = p.rec[(base + slot_of(k)) * 2];
-            mnx = fminf(mnx, ra.x);
-            mny = fminf(mny, ra.y);
-            mxx = fmaxf(mxx, ra.x);
-            mxy = fmaxf(mxy, ra.y);
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            mnx = fminf(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
-            mny = fminf(mny, __shfl_xor_sync(0xffffffffu, mny, o));
-            mxx = fmaxf(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
-            mxy = fmaxf(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
-        }
-        if (lane == 0) {
-            s_red[0][warp] = mnx;
-            s_red[1][warp] = mny;
-            s_red[2][warp] = mxx;
-            s_red[3][warp] = mxy;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            for (int w = 1; w < kBThreads / 32; ++w) {
-                mnx = fminf(mnx, s_red[0][w]);
-                mny = fminf(mny, s_red[1][w]);
-                mxx = fmaxf(mxx, s_red[2][w]);
-                mxy = fmaxf(mxy, s_red[3][w]);
-            }
-            const float rr = static_cast<float>(p.r64) + 2.0f;
-            int x0 = max(0, static_cast<int>(floorf(fmaxf(mnx - rr, -1.0e9f))));
-            const int y0 = max(0, static_cast<int>(floorf(fmaxf(mny - rr, -1.0e9f))));
-            int x1 = min(p.W - 1, static_cast<int>(ceilf(fminf(mxx + rr, 1.0e9f))));
-            const int y1 = min(p.H - 1, static_cast<int>(ceilf(fminf(mxy + rr, 1.0e9f))));
-            x0 &= ~1;
-            x1 |= 1;
-            s_region[0] = x0;
-            s_region[1] = y0;
-            s_region[2] = x1;
-            s_region[3] = y1;
-            const long wd = (x1 >= x0) ? (x1 - x0 + 1) : 0;
-            const long area = (y1 >= y0) ? wd * (y1 - y0 + 1) : 0;
-            s_region[4] = (mnx <= mxx && area > 0 && area * 68 <= kBSmem) ? 1 : (area > 0 ? 0 : -1);
-        }
-        __syncthreads();
-    }
-    const int rx0 = s_region[0], ry0 = s_region[1], rx1 = s_region[2], ry1 = s_region[3];
-    const int mode = s_region[4];
-    if (mode < 0) {
-        // no frame pixel is reachable: gradients are zero
-        for (int k = tid; k < total; k += kBThreads) {
-            const int sk = slot_of(k);
-            const int i = static_cast<int>(__float_as_uint(p.rec[(base + sk) * 2 + 1].z) & 0x7fffffffu);
-            for (int c = ch0; c < min(p.C, ch0 + kBG); ++c) p.d_col[(base + i) * p.C + c] = 0.f;
-            float* dp = p.d_pos + (static_cast<size_t>(cg) * p.B * p.N + base + i) * 2;
-            dp[0] = 0.f;
-            dp[1] = 0.f;
-        }
-        return;
-    }
-    const bool staged = mode == 1;
-    const int wd = rx1 - rx0 + 1;  // even
-    const int area = wd * (ry1 - ry0 + 1);
-    float* s_v = reinterpret_cast<float*>(s_u4 + (staged ? 4 * area : 0));
     const size_t img_base = static_cast<size_t>(b) * p.H * p.W;
-    const int cl = lane & 3;           // channel quad of the lane
-    const int c4 = ch0 + 4 * cl;       // its first channel
-
-    if (staged) {
-        // 4 lanes per pixel (16 channels), pixels row-major over the region,
-        // two pixels per thread and iteration with all loads issued up front
-        const bool full = (p.C % 4) == 0 && c4 + 3 < p.C &&
-                          (reinterpret_cast<uintptr_t>(p.upstream) & 15) == 0 &&
-                          (reinterpret_cast<uintptr_t>(p.image) & 15) == 0;
-        constexpr int kStep = kBThreads / 4;
-        auto adv = [&](int& r, int& cc) {
-            cc += kStep;
-            while (cc >= wd) {
-                cc -= wd;
-                ++r;
-            }
-        };
-        auto load = [&](bool live, int r, int cc, float& w, float4& up, float4& im) {
-            const int yy = ry0 + r, xx = rx0 + cc;
-            const bool in = live && xx < p.W && yy < p.H;
-            const size_t pix = img_base + (in ? static_cast<size_t>(yy) * p.W + xx : 0);
-            w = 0.f;
-            up = make_float4(0.f, 0.f, 0.f, 0.f);
-            im = up;
-            if (in) {
-                w = p.wsum[pix];
-                if (full) {
-                    up = *reinterpret_cast<const float4*>(p.upstream + pix * p.C + c4);
-                    im = *reinterpret_cast<const float4*>(p.image + pix * p.C + c4);
-                } else {
-                    float t[8];
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        t[c] = c4 + c < p.C ? p.upstream[pix * p.C + c4 + c] : 0.f;
-                        t[4 + c] = c4 + c < p.C ? p.image[pix * p.C + c4 + c] : 0.f;
-                    }
-                    up = make_float4(t[0], t[1], t[2], t[3]);
-                    im = make_float4(t[4], t[5], t[6], t[7]);
-                }
-            }
-        };
-        auto put = [&](bool live, int k, float w, const float4& up, const float4& im) {
-            const float inv = w > 0.f ? 1.0f / w : 0.f;  // W == 0: fallback pixel, zeros
-            const float4 u = make_float4(up.x * inv, up.y * inv, up.z * inv, up.w * inv);
-            float vp = fmaf(u.w, im.w, fmaf(u.z, im.z, fmaf(u.y, im.y, u.x * im.x)));
-            vp += __shfl_xor_sync(0xffffffffu, vp, 1);
-            vp += __shfl_xor_sync(0xffffffffu, vp, 2);
-            if (live) {
-                s_u4[4 * k + cl] = u;
-                if (cl == 0) s_v[k] = vp;
-            }
-        };
-        int rA = (tid >> 2) / wd, cA = (tid >> 2) - rA * wd;
-        int rB = rA, cB = cA;
-        adv(rB, cB);
-        for (int kb = 0; kb < area; kb += 2 * kStep) {
-            const int kA = kb + (tid >> 2), kB = kA + kStep;
-            float wA, wB;
-            float4 uA, oA, uB, oB;
-            load(kA < area, rA, cA, wA, uA, oA);
-            load(kB < area, rB, cB, wB, uB, oB);
-            put(kA < area, kA, wA, uA, oA);
-            put(kB < area, kB, wB, uB, oB);
-            adv(rA, cA);
-            adv(rA, cA);
-            adv(rB, cB);
-            adv(rB, cB);
-        }
-        __syncthreads();
-    }
-
-    // ---- per point: one warp, 4 teams of 8 lanes on interleaved rows ----
     const float nk = p.nk;
     const float r2f = static_cast<float>(p.r2_64), rf = static_cast<float>(p.r64);
     const double r2_64 = p.r2_64;
-    const int xmin = max(rx0, 0), xmax = min(rx1, p.W - 1);
-    const int team = lane >> 3, h = (lane >> 2) & 1;
-    const unsigned qmask = 0xfu << (lane & ~3);
-    for (int k = warp; k < total; k += kBThreads / 32) {
-        const int s = slot_of(k);
-        const float4 ra = p.rec[(base + s) * 2];
-        const uint32_t raw = __float_as_uint(p.rec[(base + s) * 2 + 1].z);
-        const float mx = ra.x, my = ra.y;
-        const int i = static_cast<int>(raw & 0x7fffffffu);
-        const bool unsafe = (raw & kUnsafeBit) != 0;
-        float cc[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) cc[c] = c4 + c < p.C ? p.ccol[(base + s) * p.C + c4 + c] : 0.f;
-        float dcol[4] = {0.f, 0.f, 0.f, 0.f}, gxc[4] = {0.f, 0.f, 0.f, 0.f},
-              gyc[4] = {0.f, 0.f, 0.f, 0.f};
-        float vx = 0.f, vy = 0.f;
-        const float tx = truncf(mx);
-        const float fmu = mx - tx;  // exact
-        const int bx = static_cast<int>(tx);
-        const float pad = unsafe ? 1.0f : 1e-2f;
-        const int ya = max(ry0, static_cast<int>(ceilf(my - rf - pad))) + team;
-        const int yb = min(ry1, static_cast<int>(floorf(my + rf + pad)));
-        float yf = static_cast<float>(ya);
-        for (int y = ya; y <= yb; y += 4, yf += 4.f) {
-            float dy;
-            int xl, xr;
-            if (!unsafe) {
-                dy = yf - my;
-                const float h2f = fmaf(-dy, dy, r2f);
-                if (h2f < 0.f) continue;
-                const float sq = h2f * rsqrtf(fmaxf(h2f, 1e-30f));
-                constexpr float kMagic = 12582912.0f;
-                constexpr int kMagicBits = 0x4B400000;
-                xl = bx + (__float_as_int(__fadd_ru(fmu - sq, kMagic)) - kMagicBits);
-                xr = bx + (__float_as_int(__fadd_rd(fmu + sq, kMagic)) - kMagicBits);
-            } else {
-                const double dy64 = __dsub_rn(static_cast<double>(y), static_cast<double>(my));
-                const double h2 = __dsub_rn(r2_64, __dmul_rn(dy64, dy64));
-                if (h2 < 0.0) continue;
-                const float sq = sqrtf(static_cast<float>(h2));
-                xl = bx + static_cast<int>(ceilf(fmu - sq));
-                xr = bx + static_cast<int>(floorf(fmu + sq));
-                int a = xl - 2;
-                while (a <= xl + 2 && !in_ref_w(a, y, mx, my, r2_64)) ++a;
-                int z = xr + 2;
-                while (z >= xr - 2 && !in_ref_w(z, y, mx, my, r2_64)) --z;
-                xl = a;
-                xr = z;
-                dy = static_cast<float>(dy64);
+    // a point's in-ball pixels lie within its cell grown by r
+    const double pad = p.r64 + 0.25;
+    const bool full = (p.C % 4) == 0 && ch0 + kBG <= p.C &&
+                      (reinterpret_cast<uintptr_t>(p.upstream) & 15) == 0 &&
+                      (reinterpret_cast<uintptr_t>(p.image) & 15) == 0;
+    const bool cfull = (p.C % 4) == 0 && ch0 + kBG <= p.C &&
+                       (reinterpret_cast<uintptr_t>(p.ccol) & 15) == 0;
+
+    // uncapped grids bound a cell's points by the cell: the column's x-range
+    // is fixed and consecutive cells share rows
+    int rx0 = 0, rx1 = -1, wd = 0, rb = 0;
+    if (!g.capped) {
+        rx0 = max(0, static_cast<int>(floor(g.ox + cx * g.cell - pad)));
+        rx1 = min(p.W - 1, static_cast<int>(ceil(g.ox + (cx + 1) * g.cell + pad)));
+        wd = rx1 - rx0 + 1;
+        rb = wd > 0 ? kPlanePx / wd : 0;
+    }
+    int st_hi = -1;  // last staged row: the ring holds rows (st_hi - rb, st_hi]
+
+    for (int cy = cyA; cy < cyB; ++cy) {
+        const int64_t ci = g.bin_off + static_cast<int64_t>(cy) * g.n_cols + cx;
+        const int s0 = p.bins[ci], cnt = p.bins[ci + 1] - s0;
+        if (cnt == 0) continue;
+        int ry0, ry1, mode;  // mode 1: staged, 0: from global, -1: no pixel reachable
+        if (!g.capped) {
+            ry0 = max(0, static_cast<int>(floor(g.oy + cy * g.cell - pad)));
+            ry1 = min(p.H - 1, static_cast<int>(ceil(g.oy + (cy + 1) * g.cell + pad)));
+            mode = (wd <= 0 || ry1 < ry0) ? -1 : (ry1 - ry0 + 1 <= rb ? 1 : 0);
+        } else {
+            // clamped edge cells: the bbox of the cell's points grown by r
+            float mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
+            for (int k = tid; k < cnt; k += kBThreads) {
+                const float4 ra = p.rec[(base + s0 + k) * 2];
+                mnx = fminf(mnx, ra.x);
+                mny = fminf(mny, ra.y);
+                mxx = fmaxf(mxx, ra.x);
+                mxy = fmaxf(mxy, ra.y);
             }
-            xl = max(xl, xmin);
-            xr = min(xr, xmax);
-            if (xl > xr) continue;
-            const float ey = (dy * nk) * dy;
-            // pair-aligned span: pairs xs, xs+2, ..; the lane takes x = xs+2j+h
-            const int xs = xl - ((xl - rx0) & 1);
-            const int np = ((xr - xs) >> 1) + 1;
-            const bool mfirst = h == 0 && ((xl - rx0) & 1);
-            const bool mlast = h == 1 && !((xr - rx0) & 1);
-            float xf = static_cast<float>(xs + h);
-            float R[4] = {0.f, 0.f, 0.f, 0.f};
-            float vr = 0.f;
-            if (staged) {
-                // this lane's pixels x = xs + h + 2j, j in [j0, j1), all in [xl, xr]
-                const int j0 = mfirst ? 1 : 0, j1 = mlast ? np - 1 : np;
-                const int kk0 = (y - ry0) * wd + (xs - rx0) + h + 2 * j0;
-                const float4* pu = s_u4 + 4 * kk0 + cl;
-                const float* pv = s_v + kk0;
-                xf += static_cast<float>(2 * j0);
-#pragma unroll 2
-                for (int j = j0; j < j1; ++j) {
-                    const float4 u = *pu;
-                    const float v = *pv;
-                    const float dx = xf - mx;
-                    const float w = ex2(fmaf(dx * nk, dx, ey));
-                    const float wdx = w * dx;
-                    R[0] = fmaf(w, u.x, R[0]);
-                    R[1] = fmaf(w, u.y, R[1]);
-                    R[2] = fmaf(w, u.z, R[2]);
-                    R[3] = fmaf(w, u.w, R[3]);
-                    gxc[0] = fmaf(wdx, u.x, gxc[0]);
-                    gxc[1] = fmaf(wdx, u.y, gxc[1]);
-                    gxc[2] = fmaf(wdx, u.z, gxc[2]);
-                    gxc[3] = fmaf(wdx, u.w, gxc[3]);
-                    vx = fmaf(wdx, v, vx);
-                    vr = fmaf(w, v, vr);
-                    xf += 2.f;
-                    pu += 8;
-                    pv += 2;
+            for (int o = 16; o > 0; o >>= 1) {
+                mnx = fminf(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+                mny = fminf(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+                mxx = fmaxf(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+                mxy = fmaxf(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+            }
+            __syncthreads();  // s_red / s_reg and the ring free
+            if (lane == 0) {
+                s_red[0][warp] = mnx;
+                s_red[1][warp] = mny;
+                s_red[2][warp] = mxx;
+                s_red[3][warp] = mxy;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                for (int w = 1; w < kBThreads / 32; ++w) {
+                    mnx = fminf(mnx, s_red[0][w]);
+                    mny = fminf(mny, s_red[1][w]);
+                    mxx = fmaxf(mxx, s_red[2][w]);
+                    mxy = fmaxf(mxy, s_red[3][w]);
+                }
+                const float rr = static_cast<float>(p.r64) + 1.0f;
+                const int x0 = max(0, static_cast<int>(floorf(fmaxf(mnx - rr, -1.0e9f))));
+                const int y0 = max(0, static_cast<int>(floorf(fmaxf(mny - rr, -1.0e9f))));
+                const int x1 = min(p.W - 1, static_cast<int>(ceilf(fminf(mxx + rr, 1.0e9f))));
+                const int y1 = min(p.H - 1, static_cast<int>(ceilf(fminf(mxy + rr, 1.0e9f))));
+                s_reg[0] = x0;
+                s_reg[1] = x1;
+                s_reg[2] = y0;
+                s_reg[3] = y1;
+                s_reg[4] = (mnx <= mxx && x1 >= x0 && y1 >= y0) ? 1 : -1;
+            }
+            __syncthreads();
+            rx0 = s_reg[0];
+            rx1 = s_reg[1];
+            ry0 = s_reg[2];
+            ry1 = s_reg[3];
+            wd = rx1 - rx0 + 1;
+            rb = wd > 0 ? kPlanePx / wd : 0;
+            st_hi = -1;  // new x-range: nothing reusable
+            mode = s_reg[4] < 0 ? -1 : (ry1 - ry0 + 1 <= rb ? 1 : 0);
+        }
+        if (mode < 0) {
+            // no frame pixel is reachable: gradients are zero
+            for (int k = tid; k < cnt; k += kBThreads) {
+                const int i = static_cast<int>(
+                    __float_as_uint(p.rec[(base + s0 + k) * 2 + 1].z) & 0x7fffffffu);
+                for (int c = ch0; c < min(p.C, ch0 + kBG); ++c) p.d_col[(base + i) * p.C + c] = 0.f;
+                float* dp = p.d_pos + (static_cast<size_t>(cg) * p.B * p.N + base + i) * 2;
+                dp[0] = 0.f;
+                dp[1] = 0.f;
+            }
+            continue;
+        }
+        if (mode == 1 && ry1 > st_hi) {
+            // ---- stage the rows this cell adds (lane per pixel) ----
+            const int ys = max(st_hi + 1, ry0);
+            const int area = (ry1 - ys + 1) * wd;
+            __syncthreads();  // the previous cell's points are done with the ring
+            int r = tid / wd, cc = tid - r * wd;
+            int pr = (ys + r) % rb;
+            for (int k = tid; k < area; k += kBThreads) {
+                const int yy = ys + r, xx = rx0 + cc;
+                float w = 0.f, u[kBG], im[kBG];
+#pragma unroll
+                for (int c = 0; c < kBG; ++c) {
+                    u[c] = 0.f;
+                    im[c] = 0.f;
+                }
+                if (xx < p.W && yy < p.H)
+                    load_px16(p, img_base + static_cast<size_t>(yy) * p.W + xx, ch0, full, w, u, im);
+                const float v = pixel_uv(w, u, im);
+                const int q = pr * wd + cc;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    s_u4[j * kPlanePx + q] = make_float4(u[4 * j], u[4 * j + 1], u[4 * j + 2], u[4 * j + 3]);
+                s_v[q] = v;
+                cc += kBThreads;
+                while (cc >= wd) {
+                    cc -= wd;
+                    ++r;
+                    if (++pr == rb) pr = 0;
+                }
+            }
+            st_hi = ry1;
+            __syncthreads();
+        }
+        const bool staged = mode == 1;
+        const int xmin = max(rx0, 0), xmax = min(rx1, p.W - 1);
+
+        // ---- per point: a squad of 8 lanes ----
+        for (int kb = warp * 4; kb < cnt; kb += kBThreads / 8) {
+            const int k = kb + sq;
+            const bool live = k < cnt;
+            const int s = s0 + (live ? k : 0);
+            const float4 ra = p.rec[(base + s) * 2];
+            const uint32_t raw = __float_as_uint(p.rec[(base + s) * 2 + 1].z);
+            const float mx = ra.x, my = ra.y;
+            const int i = static_cast<int>(raw & 0x7fffffffu);
+            const bool unsafe = (raw & kUnsafeBit) != 0;
+            float cc[kBG];
+            if (cfull) {
+                const float4* c4 = reinterpret_cast<const float4*>(p.ccol + (base + s) * p.C + ch0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float4 t = c4[j];
+                    cc[4 * j] = t.x; cc[4 * j + 1] = t.y; cc[4 * j + 2] = t.z; cc[4 * j + 3] = t.w;
                 }
             } else {
-                for (int j = 0; j < np; ++j) {
-                    float4 u;
-                    float v;
-                    pixel_u4(p, img_base, c4, xs + 2 * j + h, y, u, v, qmask);
-                    const float dx = xf - mx;
-                    float w = ex2(fmaf(dx * nk, dx, ey));
-                    if ((j == 0 && mfirst) || (j == np - 1 && mlast)) w = 0.f;
-                    const float wdx = w * dx;
-                    R[0] = fmaf(w, u.x, R[0]);
-                    R[1] = fmaf(w, u.y, R[1]);
-                    R[2] = fmaf(w, u.z, R[2]);
-                    R[3] = fmaf(w, u.w, R[3]);
-                    gxc[0] = fmaf(wdx, u.x, gxc[0]);
-                    gxc[1] = fmaf(wdx, u.y, gxc[1]);
-                    gxc[2] = fmaf(wdx, u.z, gxc[2]);
-                    gxc[3] = fmaf(wdx, u.w, gxc[3]);
-                    vx = fmaf(wdx, v, vx);
-                    vr = fmaf(w, v, vr);
-                    xf += 2.f;
+#pragma unroll
+                for (int c = 0; c < kBG; ++c)
+                    cc[c] = ch0 + c < p.C ? p.ccol[(base + s) * p.C + ch0 + c] : 0.f;
+            }
+            float dcol[kBG];
+#pragma unroll
+            for (int c = 0; c < kBG; ++c) dcol[c] = 0.f;
+            float gx = 0.f, gy = 0.f;
+            const float tx = truncf(mx);
+            const float fmu = mx - tx;  // exact
+            const int bx = static_cast<int>(tx);
+            const float pd = unsafe ? 1.0f : 1e-2f;
+            const int ya = max(ry0, static_cast<int>(ceilf(my - rf - pd)));
+            const int yb = live ? min(ry1, static_cast<int>(floorf(my + rf + pd))) : ya - 1;
+            int prow = staged && ya <= yb ? ya % rb : 0;
+            float yf = static_cast<float>(ya);
+            for (int y = ya; y <= yb; ++y, yf += 1.f) {
+                const int pr = prow;
+                if (staged && ++prow == rb) prow = 0;
+                float dy;
+                int xl, xr;
+                if (!unsafe) {
+                    dy = yf - my;
+                    const float h2f = fmaf(-dy, dy, r2f);
+                    if (h2f < 0.f) continue;
+                    const float sqv = h2f * rsqrtf(fmaxf(h2f, 1e-30f));
+                    constexpr float kMagic = 12582912.0f;
+                    constexpr int kMagicBits = 0x4B400000;
+                    xl = bx + (__float_as_int(__fadd_ru(fmu - sqv, kMagic)) - kMagicBits);
+                    xr = bx + (__float_as_int(__fadd_rd(fmu + sqv, kMagic)) - kMagicBits);
+                } else {
+                    const double dy64 = __dsub_rn(static_cast<double>(y), static_cast<double>(my));
+                    const double h2 = __dsub_rn(r2_64, __dmul_rn(dy64, dy64));
+                    if (h2 < 0.0) continue;
+                    const float sqv = sqrtf(static_cast<float>(h2));
+                    xl = bx + static_cast<int>(ceilf(fmu - sqv));
+                    xr = bx + static_cast<int>(floorf(fmu + sqv));
+                    int a = xl - 2;
+                    while (a <= xl + 2 && !in_ref_w(a, y, mx, my, r2_64)) ++a;
+                    int z = xr + 2;
+                    while (z >= xr - 2 && !in_ref_w(z, y, mx, my, r2_64)) --z;
+                    xl = a;
+                    xr = z;
+                    dy = static_cast<float>(dy64);
                 }
+                xl = max(xl, xmin);
+                xr = min(xr, xmax);
+                // e = nk dx^2 + nk dy^2 with the forward's fp32 operations
+                const float ey = (dy * nk) * dy;
+                const int x0l = xl + sl;
+                float xf = static_cast<float>(x0l);
+                if (staged) {
+                    const int q0 = pr * wd - rx0;
+                    for (int x = x0l; x <= xr; x += 8, xf += 8.f) {
+                        const int q = q0 + x;
+                        const float4 u0 = s_u4[q], u1 = s_u4[kPlanePx + q];
+                        const float4 u2 = s_u4[2 * kPlanePx + q], u3 = s_u4[3 * kPlanePx + q];
+                        const float v = s_v[q];
+                        const float u[kBG] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w,
+                                              u2.x, u2.y, u2.z, u2.w, u3.x, u3.y, u3.z, u3.w};
+                        const float dx = xf - mx;
+                        const float w = ex2(fmaf(dx * nk, dx, ey));
+                        // t = sum_c c_ic u_c - v  (= dot / W, engine.cpp:219-221)
+                        float t = -v;
+#pragma unroll
+                        for (int c = 0; c < kBG; ++c) t = fmaf(u[c], cc[c], t);
+                        const float a = w * t;
+                        gx = fmaf(a, dx, gx);
+                        gy = fmaf(a, dy, gy);
+#pragma unroll
+                        for (int c = 0; c < kBG; ++c) dcol[c] = fmaf(w, u[c], dcol[c]);
+                    }
+                } else {
+                    for (int x = x0l; x <= xr; x += 8, xf += 8.f) {
+                        float w0, u[kBG], im[kBG];
+                        load_px16(p, img_base + static_cast<size_t>(y) * p.W + x, ch0, full, w0, u, im);
+                        const float v = pixel_uv(w0, u, im);
+                        const float dx = xf - mx;
+                        const float w = ex2(fmaf(dx * nk, dx, ey));
+                        float t = -v;
+#pragma unroll
+                        for (int c = 0; c < kBG; ++c) t = fmaf(u[c], cc[c], t);
+                        const float a = w * t;
+                        gx = fmaf(a, dx, gx);
+                        gy = fmaf(a, dy, gy);
+#pragma unroll
+                        for (int c = 0; c < kBG; ++c) dcol[c] = fmaf(w, u[c], dcol[c]);
+                    }
+                }
+            }
+            // ---- squad sums: reduce-scatter of d_col (lane sl keeps channels
+            // 2 sl, 2 sl + 1), full sums of the position terms ----
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const bool up = (sl & 4) != 0;
+                const float send = up ? dcol[c] : dcol[c + 8];
+                const float keep = up ? dcol[c + 8] : dcol[c];
+                dcol[c] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
             }
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                dcol[c] += R[c];
-                gyc[c] = fmaf(dy, R[c], gyc[c]);
+                const bool up = (sl & 2) != 0;
+                const float send = up ? dcol[c] : dcol[c + 4];
+                const float keep = up ? dcol[c + 4] : dcol[c];
+                dcol[c] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
             }
-            vy = fmaf(dy, vr, vy);
-        }
-        // combine the two pixel halves and the four teams (fixed tree)
 #pragma unroll
-        for (int o = 4; o < 32; o <<= 1) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                dcol[c] += __shfl_xor_sync(0xffffffffu, dcol[c], o);
-                gxc[c] += __shfl_xor_sync(0xffffffffu, gxc[c], o);
-                gyc[c] += __shfl_xor_sync(0xffffffffu, gyc[c], o);
+            for (int c = 0; c < 2; ++c) {
+                const bool up = (sl & 1) != 0;
+                const float send = up ? dcol[c] : dcol[c + 2];
+                const float keep = up ? dcol[c + 2] : dcol[c];
+                dcol[c] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
             }
-            vx += __shfl_xor_sync(0xffffffffu, vx, o);
-            vy += __shfl_xor_sync(0xffffffffu, vy, o);
-        }
-        // d_pos of this group: sum_c c_ic G_c over the 4 channel lanes - v
-        float gx = cc[0] * gxc[0], gy = cc[0] * gyc[0];
 #pragma unroll
-        for (int c = 1; c < 4; ++c) {
-            gx = fmaf(cc[c], gxc[c], gx);
-            gy = fmaf(cc[c], gyc[c], gy);
-        }
-        gx += __shfl_xor_sync(0xffffffffu, gx, 1);
-        gy += __shfl_xor_sync(0xffffffffu, gy, 1);
-        gx += __shfl_xor_sync(0xffffffffu, gx, 2);
-        gy += __shfl_xor_sync(0xffffffffu, gy, 2);
-        if (lane < 4) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-                if (c4 + c < p.C) p.d_col[(base + i) * p.C + c4 + c] = dcol[c];
-        }
-        if (lane == 0) {
-            float* dp = p.d_pos + (static_cast<size_t>(cg) * p.B * p.N + base + i) * 2;
-            dp[0] = (gx - vx) * p.inv_s2;
-            dp[1] = (gy - vy) * p.inv_s2;
+            for (int o = 1; o < 8; o <<= 1) {
+                gx += __shfl_xor_sync(0xffffffffu, gx, o);
+                gy += __shfl_xor_sync(0xffffffffu, gy, o);
+            }
+            if (live) {
+                const int c0 = ch0 + 2 * sl;
+                float* dc = p.d_col + (base + i) * p.C + c0;
+                if (c0 < p.C) dc[0] = dcol[0];
+                if (c0 + 1 < p.C) dc[1] = dcol[1];
+                if (sl == 0) {
+                    float* dp = p.d_pos + (static_cast<size_t>(cg) * p.B * p.N + base + i) * 2;
+                    dp[0] = gx * p.inv_s2;
+                    dp[1] = gy * p.inv_s2;
+                }
+            }
         }
     }
 }
@@ -814,23 +759,17 @@ bool launch_backward_wide(gmi_ctx* ctx, const gmi_cache* c, const float* upstrea
     if (c->C <= 4 || c->rec == nullptr || c->ccol == nullptr || c->wsum64 != nullptr) return false;
     cudaStream_t st = ctx->stream;
     const int groups = (c->C + kBG - 1) / kBG;
-    // cells per block side so that the staged region (~(bs cell + 2r + 4)^2
-    // pixels of 68 B) fits the budget
-    const double cell = c->cutoff;
-    const double side_px = std::sqrt(static_cast<double>(kBSmem) / 68.0);
-    int bs = static_cast<int>(std::floor((side_px - 2.0 * c->cutoff - 4.0) / cell));
-    bs = std::max(1, std::min(bs, kBRunMax));
+    // CTA = one cell column x a segment of kBSeg cell rows
+    int max_rows = c->grid_cap;
+    if (!c->geom_h.empty()) {
+        max_rows = 1;
+        for (const auto& g : c->geom_h) max_rows = std::max(max_rows, g.n_rows);
+    }
+    const int nseg_cap = (max_rows + kBSeg - 1) / kBSeg;
     std::vector<int32_t> off(c->B + 1, 0);
     for (int b = 0; b < c->B; ++b) {
-        int nb;
-        if (c->geom_h.empty()) {
-            const int side = (c->grid_cap + bs - 1) / bs;
-            nb = side * side;
-        } else {
-            const auto& g = c->geom_h[b];
-            nb = ((g.n_cols + bs - 1) / bs) * ((g.n_rows + bs - 1) / bs);
-        }
-        off[b + 1] = off[b] + nb;
+        const int ncols = c->geom_h.empty() ? c->grid_cap : c->geom_h[b].n_cols;
+        off[b + 1] = off[b] + ncols * nseg_cap;
     }
     int32_t* d_off = static_cast<int32_t*>(scratch(ctx, WS_BLKOFF, sizeof(int32_t) * (c->B + 1)));
     GMI_CUDA(cudaMemcpyAsync(d_off, off.data(), sizeof(int32_t) * (c->B + 1),
@@ -849,7 +788,8 @@ bool launch_backward_wide(gmi_ctx* ctx, const gmi_cache* c, const float* upstrea
     p.C = c->C;
     p.W = c->W;
     p.H = c->H;
-    p.bs = bs;
+    p.seg = kBSeg;
+    p.nseg_cap = nseg_cap;
     p.r64 = c->cutoff;
     p.r2_64 = c->cutoff * c->cutoff;
     p.nk = static_cast<float>(-1.4426950408889634 / (2.0 * c->sigma * c->sigma));
