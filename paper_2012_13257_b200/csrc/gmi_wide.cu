@@ -316,7 +316,7 @@ void launch_wide_cb(gmi_ctx* ctx, const GatherWideParams& p, dim3 grid) {
 // K4 wide
 // ---------------------------------------------------------------------------
 constexpr int kBG = 16;                 // channels per group
-constexpr int kBThreads = 256;          // 8 warps x 4 squads of 8 lanes
+constexpr int kBThreads = 256;          // 8 warps (one point each) x 4 squads
 constexpr int kPlanePx = 1600;          // ring capacity in pixels (68 B each): 2 CTAs/SM
 constexpr int kBSmem = kPlanePx * 68;
 constexpr int kBSeg = 16;               // cell rows per CTA
@@ -384,11 +384,12 @@ __device__ __forceinline__ float pixel_uv(float w, float* u, const float* im) {
 // v, pixel-major inside a plane, so 8 lanes on 8 consecutive pixels read 128
 // contiguous bytes per LDS.128 (conflict-free).  Consecutive cells of the
 // column share all but cell rows, which are the only ones staged.
-// Squad = 8 lanes owning ONE point: the squad walks the point's exact disk
-// row by row, lane l taking pixels xl + l, xl + l + 8, ..; per pixel
+// A warp owns one point; its 4 squads of 8 lanes take interleaved rows of the
+// point's exact disk, lane l of a squad the pixels xl + l, xl + l + 8, ..;
+// per pixel
 //     t = sum_c u_c c_ic - v,  d_col_c += w u_c,  d_pos += w t (q - mu)
 // with all 16 channels of the group in the lane's registers (no cross-lane
-// work per pixel).  Squad sums are combined by a fixed shuffle tree.
+// work per pixel).  Lane sums are combined by a fixed shuffle tree.
 __global__ void __launch_bounds__(kBThreads, 2)
 k_backward_wide(BwdWideParams p) {
     extern __shared__ float4 s_u4[];      // planes [4][kPlanePx] float4, then s_v[kPlanePx]
@@ -549,11 +550,17 @@ k_backward_wide(BwdWideParams p) {
         const bool staged = mode == 1;
         const int xmin = max(rx0, 0), xmax = min(rx1, p.W - 1);
 
-        // ---- per point: a squad of 8 lanes ----
-        for (int kb = warp * 4; kb < cnt; kb += kBThreads / 8) {
-            const int k = kb + sq;
-            const bool live = k < cnt;
-            const int s = s0 + (live ? k : 0);
+        // ---- per point: one warp, its 4 squads on interleaved rows ----
+        for (int k = warp; k < cnt; k += kBThreads / 32) {
+            const int s = s0 + k;
+            if (k + kBThreads / 32 < cnt && lane < 3) {
+                // the warp's next point: record and colour lines into L1
+                const int sn = s + kBThreads / 32;
+                const char* a = lane == 0 ? reinterpret_cast<const char*>(p.rec + (base + sn) * 2)
+                                          : reinterpret_cast<const char*>(p.ccol + (base + sn) * p.C + ch0) +
+                                                (lane - 1) * 32;
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+            }
             const float4 ra = p.rec[(base + s) * 2];
             const uint32_t raw = __float_as_uint(p.rec[(base + s) * 2 + 1].z);
             const float mx = ra.x, my = ra.y;
@@ -580,13 +587,16 @@ k_backward_wide(BwdWideParams p) {
             const float fmu = mx - tx;  // exact
             const int bx = static_cast<int>(tx);
             const float pd = unsafe ? 1.0f : 1e-2f;
-            const int ya = max(ry0, static_cast<int>(ceilf(my - rf - pd)));
-            const int yb = live ? min(ry1, static_cast<int>(floorf(my + rf + pd))) : ya - 1;
+            const int ya = max(ry0, static_cast<int>(ceilf(my - rf - pd))) + sq;
+            const int yb = min(ry1, static_cast<int>(floorf(my + rf + pd)));
             int prow = staged && ya <= yb ? ya % rb : 0;
             float yf = static_cast<float>(ya);
-            for (int y = ya; y <= yb; ++y, yf += 1.f) {
+            for (int y = ya; y <= yb; y += 4, yf += 4.f) {
                 const int pr = prow;
-                if (staged && ++prow == rb) prow = 0;
+                if (staged) {
+                    prow += 4;
+                    while (prow >= rb) prow -= rb;
+                }
                 float dy;
                 int xl, xr;
                 if (!unsafe) {
@@ -631,9 +641,11 @@ k_backward_wide(BwdWideParams p) {
                         const float dx = xf - mx;
                         const float w = ex2(fmaf(dx * nk, dx, ey));
                         // t = sum_c c_ic u_c - v  (= dot / W, engine.cpp:219-221)
-                        float t = -v;
+                        // four partial sums: short dependency chains
+                        float t4[4] = {-v, 0.f, 0.f, 0.f};
 #pragma unroll
-                        for (int c = 0; c < kBG; ++c) t = fmaf(u[c], cc[c], t);
+                        for (int c = 0; c < kBG; ++c) t4[c & 3] = fmaf(u[c], cc[c], t4[c & 3]);
+                        const float t = (t4[0] + t4[1]) + (t4[2] + t4[3]);
                         const float a = w * t;
                         gx = fmaf(a, dx, gx);
                         gy = fmaf(a, dy, gy);
@@ -647,9 +659,11 @@ k_backward_wide(BwdWideParams p) {
                         const float v = pixel_uv(w0, u, im);
                         const float dx = xf - mx;
                         const float w = ex2(fmaf(dx * nk, dx, ey));
-                        float t = -v;
+                        // four partial sums: short dependency chains
+                        float t4[4] = {-v, 0.f, 0.f, 0.f};
 #pragma unroll
-                        for (int c = 0; c < kBG; ++c) t = fmaf(u[c], cc[c], t);
+                        for (int c = 0; c < kBG; ++c) t4[c & 3] = fmaf(u[c], cc[c], t4[c & 3]);
+                        const float t = (t4[0] + t4[1]) + (t4[2] + t4[3]);
                         const float a = w * t;
                         gx = fmaf(a, dx, gx);
                         gy = fmaf(a, dy, gy);
@@ -658,8 +672,13 @@ k_backward_wide(BwdWideParams p) {
                     }
                 }
             }
-            // ---- squad sums: reduce-scatter of d_col (lane sl keeps channels
-            // 2 sl, 2 sl + 1), full sums of the position terms ----
+            // ---- warp sums: the 4 squads, then a reduce-scatter of d_col
+            // inside the squad (lane sl keeps channels 2 sl, 2 sl + 1) ----
+#pragma unroll
+            for (int o = 8; o < 32; o <<= 1) {
+#pragma unroll
+                for (int c = 0; c < kBG; ++c) dcol[c] += __shfl_xor_sync(0xffffffffu, dcol[c], o);
+            }
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 const bool up = (sl & 4) != 0;
@@ -682,11 +701,11 @@ k_backward_wide(BwdWideParams p) {
                 dcol[c] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
             }
 #pragma unroll
-            for (int o = 1; o < 8; o <<= 1) {
+            for (int o = 1; o < 32; o <<= 1) {
                 gx += __shfl_xor_sync(0xffffffffu, gx, o);
                 gy += __shfl_xor_sync(0xffffffffu, gy, o);
             }
-            if (live) {
+            if (sq == 0) {
                 const int c0 = ch0 + 2 * sl;
                 float* dc = p.d_col + (base + i) * p.C + c0;
                 if (c0 < p.C) dc[0] = dcol[0];
