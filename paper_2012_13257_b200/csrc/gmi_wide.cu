@@ -51,7 +51,7 @@ __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b
 // ---------------------------------------------------------------------------
 constexpr int kWT = 16;          // tile side (pixels)
 constexpr int kWThreads = 256;   // 8 warps
-constexpr int kWCap = 256;       // staged candidates per chunk
+constexpr int kWCap = 384;       // staged candidates per chunk (tile-filtered)
 constexpr int kWRuns = 32;       // cell rows per run group
 
 template <int CB>
@@ -62,6 +62,8 @@ struct SmemWide {
     int run_beg[kWRuns + 1];
     int run_g[kWRuns];
     int rect[4];                 // cx0, cx1, cy0, cy1
+    int wcnt[kWThreads / 32];    // kept candidates per warp (chunk fill)
+    int e_resume;
 };
 
 struct GatherWideParams {
@@ -152,24 +154,59 @@ k_gather_wide(GatherWideParams p) {
         }
         __syncthreads();
         const int total = S.run_beg[nr];
-        for (int c0 = 0; c0 < total; c0 += kWCap) {
-            const int n = min(kWCap, total - c0);
-            // ---- stage positions / flags ----
-            for (int k = tid; k < n; k += kWThreads) {
-                const int e = c0 + k;
-                int lo = 0, hi = nr;
-                while (hi - lo > 1) {
-                    const int mid = (lo + hi) >> 1;
-                    if (S.run_beg[mid] <= e) lo = mid;
-                    else hi = mid;
+        // chunks: the candidates whose disk can reach the tile (conservative
+        // fp32 test), compacted in run order, up to kWCap per chunk
+        const float tcx = static_cast<float>(x0) + 7.5f, tcy = static_cast<float>(y0) + 7.5f;
+        for (int e0 = 0; e0 < total;) {
+            int n = 0;
+            while (e0 < total && n < kWCap) {
+                const int e = e0 + tid;
+                bool keep = false;
+                int slot = 0;
+                float4 pt = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (e < total) {
+                    int lo = 0, hi = nr;
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (S.run_beg[mid] <= e) lo = mid;
+                        else hi = mid;
+                    }
+                    slot = S.run_g[lo] + (e - S.run_beg[lo]);
+                    const float4 ra = p.rec[(base + slot) * 2];
+                    const float rz = p.rec[(base + slot) * 2 + 1].z;
+                    pt = make_float4(ra.x, ra.y, rz, 0.f);
+                    const float ddx = fmaxf(fabsf(ra.x - tcx) - 7.5f, 0.f);
+                    const float ddy = fmaxf(fabsf(ra.y - tcy) - 7.5f, 0.f);
+                    keep = fmaf(ddx, ddx, ddy * ddy) <= p.rhit2;
                 }
-                const int slot = S.run_g[lo] + (e - S.run_beg[lo]);
-                S.slot[k] = slot;
-                const float4 ra = p.rec[(base + slot) * 2];
-                const float rz = p.rec[(base + slot) * 2 + 1].z;
-                S.pt[k] = make_float4(ra.x, ra.y, rz, 0.f);
+                const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                if (lane == 0) S.wcnt[warp] = __popc(bal);
+                __syncthreads();
+                int woff = 0, blk = 0;
+#pragma unroll
+                for (int w = 0; w < kWThreads / 32; ++w) {
+                    const int c = S.wcnt[w];
+                    woff += w < warp ? c : 0;
+                    blk += c;
+                }
+                const int pos = n + woff + __popc(bal & ((1u << lane) - 1u));
+                if (keep && pos < kWCap) {
+                    S.pt[pos] = pt;
+                    S.slot[pos] = slot;
+                }
+                if (n + blk > kWCap) {
+                    // full: the next chunk resumes at the first kept candidate left out
+                    if (keep && pos == kWCap) S.e_resume = e;
+                    __syncthreads();
+                    e0 = S.e_resume;
+                    n = kWCap;
+                } else {
+                    n += blk;
+                    e0 += kWThreads;
+                    __syncthreads();  // S.wcnt reused by the next block
+                }
             }
-            __syncthreads();
+            if (n == 0) break;
             // ---- stage this pass's colours ----
             for (int e = tid; e < n * CB; e += kWThreads) {
                 const int k = e / CB, j = e % CB;
