@@ -73,6 +73,11 @@ struct GatherWideParams {
     const float* ccol;   // [B][N][C] colours in bin order
     int N, C, W, H;
     int nsg;             // channel passes of 4 CB channels
+    int tiles_x, tiles_y;
+    int heavy_cap;       // CTA slots reserved for heavy tiles (launched first)
+    const int32_t* heavy_list;   // heavy tiles (linear b * ty * tx index)
+    const int32_t* heavy_count;
+    const uint8_t* heavy_mark;   // per tile: 1 = processed from the heavy list
     double r64, r2_64;
     float rhit2;         // (r + 1e-3)^2: conservative block test
     float nk, thr;
@@ -93,12 +98,28 @@ k_gather_wide(GatherWideParams p) {
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int cb = lane >> 3, q = lane & 7;
-    const int sg = static_cast<int>(blockIdx.z) % p.nsg;
-    const int b = static_cast<int>(blockIdx.z) / p.nsg;
+    // CTA -> tile: the first heavy_cap slots take the heavy (clustered)
+    // tiles so that they start first; the rest walk the tiles in order and
+    // skip the heavy ones
+    const int sg = blockIdx.y;
+    int tile;
+    {
+        const int slot = blockIdx.x;
+        if (slot < p.heavy_cap) {
+            if (slot >= min(*p.heavy_count, p.heavy_cap)) return;
+            tile = p.heavy_list[slot];
+        } else {
+            tile = slot - p.heavy_cap;
+            if (p.heavy_mark[tile]) return;
+        }
+    }
+    const int ntx = p.tiles_x, nty = p.tiles_y;
+    const int b = tile / (ntx * nty);
+    const int tyx = tile - b * ntx * nty;
     const int sgc0 = sg * 4 * CB;
     const int ch0 = sgc0 + cb * CB;
     const int nch = max(0, min(CB, p.C - ch0));
-    const int x0 = blockIdx.x * kWT, y0 = blockIdx.y * kWT;
+    const int x0 = (tyx % ntx) * kWT, y0 = (tyx / ntx) * kWT;
     const int bx0 = x0 + 8 * (warp & 1), by0 = y0 + 4 * (warp >> 1);
     const int xa = bx0 + 2 * (q & 3), ya = by0 + 2 * (q >> 2);
     const Geom g = p.geom[b];
@@ -336,6 +357,39 @@ k_gather_wide(GatherWideParams p) {
     }
 }
 
+// Per tile: the number of candidates (cells overlapping the tile grown by r);
+// tiles above kHeavy go to the heavy list (processed by the first CTAs).
+constexpr int kHeavy = 8 * kWCap;
+
+__global__ void k_wide_tile_load(const Geom* __restrict__ geom, const int32_t* __restrict__ bins,
+                                 int tiles_x, int tiles_y, int B, double r64, int cap,
+                                 int32_t* __restrict__ heavy_list, int32_t* heavy_count,
+                                 uint8_t* __restrict__ mark) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= B * tiles_x * tiles_y) return;
+    const int b = t / (tiles_x * tiles_y), tyx = t - b * tiles_x * tiles_y;
+    const int x0 = (tyx % tiles_x) * kWT, y0 = (tyx / tiles_x) * kWT;
+    const Geom g = geom[b];
+    const int cx0 = cell_of(static_cast<double>(x0) - r64, g.ox, g.cell, g.n_cols);
+    const int cx1 = cell_of(static_cast<double>(x0 + kWT - 1) + r64, g.ox, g.cell, g.n_cols);
+    const int cy0 = cell_of(static_cast<double>(y0) - r64, g.oy, g.cell, g.n_rows);
+    const int cy1 = cell_of(static_cast<double>(y0 + kWT - 1) + r64, g.oy, g.cell, g.n_rows);
+    long tot = 0;
+    for (int cy = cy0; cy <= cy1 && tot <= kHeavy; ++cy) {
+        const int64_t r0 = g.bin_off + static_cast<int64_t>(cy) * g.n_cols;
+        tot += bins[r0 + cx1 + 1] - bins[r0 + cx0];
+    }
+    uint8_t m = 0;
+    if (tot > kHeavy) {
+        const int slot = atomicAdd(heavy_count, 1);
+        if (slot < cap) {
+            heavy_list[slot] = t;
+            m = 1;
+        }
+    }
+    mark[t] = m;
+}
+
 template <int CB, bool kCount>
 void launch_wide_cb(gmi_ctx* ctx, const GatherWideParams& p, dim3 grid) {
     const int smem = static_cast<int>(sizeof(SmemWide<CB>));
@@ -369,7 +423,11 @@ struct BwdWideParams {
     const float* upstream;   // [B][H][W][C]
     int B, N, C, W, H;
     int seg;                 // cell rows per CTA (one cell column)
-    int nseg_cap;            // row segments per column (CTA index = column * nseg_cap + segment)
+    int nseg_cap;            // row segments per column (unit = column * nseg_cap + segment)
+    int heavy_cap;           // CTA slots reserved for heavy units (launched first)
+    const int32_t* heavy_list;
+    const int32_t* heavy_count;
+    const uint8_t* heavy_mark;
     double r64, r2_64;
     float nk, inv_s2;
     float* d_col;            // [B][N][C]
@@ -434,19 +492,28 @@ k_backward_wide(BwdWideParams p) {
     __shared__ float s_red[4][kBThreads / 32];
     __shared__ int s_reg[5];
 
-    // ---- image, cell column and row segment of this CTA ----
+    // ---- image, cell column and row segment of this CTA: the first
+    // heavy_cap slots take the heavy (clustered) units so they start first ----
+    int unit;
+    if (static_cast<int>(blockIdx.x) < p.heavy_cap) {
+        if (static_cast<int>(blockIdx.x) >= min(*p.heavy_count, p.heavy_cap)) return;
+        unit = p.heavy_list[blockIdx.x];
+    } else {
+        unit = blockIdx.x - p.heavy_cap;
+        if (p.heavy_mark[unit]) return;
+    }
     int b = 0;
     {
         int lo = 0, hi = p.B;
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
-            if (p.blk_off[mid] <= static_cast<int>(blockIdx.x)) lo = mid;
+            if (p.blk_off[mid] <= unit) lo = mid;
             else hi = mid;
         }
         b = lo;
     }
     const Geom g = p.geom[b];
-    const int local = blockIdx.x - p.blk_off[b];
+    const int local = unit - p.blk_off[b];
     const int cx = local / p.nseg_cap, sgm = local % p.nseg_cap;
     const int cyA = sgm * p.seg;
     if (cx >= g.n_cols || cyA >= g.n_rows) return;  // past this image's grid
@@ -757,6 +824,43 @@ k_backward_wide(BwdWideParams p) {
     }
 }
 
+// Per backward unit (cell column segment): its number of points; units
+// above kHeavyB go to the heavy list (processed by the first CTAs).
+constexpr int kHeavyB = 4096;
+
+__global__ void k_wide_unit_load(const Geom* __restrict__ geom, const int32_t* __restrict__ bins,
+                                 const int32_t* __restrict__ blk_off, int B, int seg, int nseg_cap,
+                                 int cap, int32_t* __restrict__ heavy_list, int32_t* heavy_count,
+                                 uint8_t* __restrict__ mark) {
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= blk_off[B]) return;
+    int lo = 0, hi = B;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (blk_off[mid] <= u) lo = mid;
+        else hi = mid;
+    }
+    const Geom g = geom[lo];
+    const int local = u - blk_off[lo];
+    const int cx = local / nseg_cap, cyA = (local % nseg_cap) * seg;
+    uint8_t m = 0;
+    if (cx < g.n_cols && cyA < g.n_rows) {
+        long tot = 0;
+        for (int cy = cyA; cy < min(cyA + seg, g.n_rows); ++cy) {
+            const int64_t ci = g.bin_off + static_cast<int64_t>(cy) * g.n_cols + cx;
+            tot += bins[ci + 1] - bins[ci];
+        }
+        if (tot > kHeavyB) {
+            const int slot = atomicAdd(heavy_count, 1);
+            if (slot < cap) {
+                heavy_list[slot] = u;
+                m = 1;
+            }
+        }
+    }
+    mark[u] = m;
+}
+
 // d_pos = sum over channel groups, in group order (deterministic)
 __global__ void k_sum_groups_w(const float* __restrict__ part, float* __restrict__ d_pos,
                                size_t n2, int groups) {
@@ -799,7 +903,22 @@ bool launch_gather_wide(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* count
     // channels per lane: the smallest block with 4 CB >= min(C, 64)
     const int cb = c->C <= 16 ? 4 : (c->C <= 32 ? 8 : 16);
     p.nsg = (c->C + 4 * cb - 1) / (4 * cb);
-    const dim3 grid((c->W + kWT - 1) / kWT, (c->H + kWT - 1) / kWT, c->B * p.nsg);
+    p.tiles_x = (c->W + kWT - 1) / kWT;
+    p.tiles_y = (c->H + kWT - 1) / kWT;
+    const int ntiles = c->B * p.tiles_x * p.tiles_y;
+    p.heavy_cap = std::min(4096, ntiles);
+    // scratch: [heavy count][heavy list][marks]
+    char* ws = static_cast<char*>(scratch(ctx, WS_TMP, sizeof(int32_t) * (1 + p.heavy_cap) + ntiles));
+    int32_t* d_cnt = reinterpret_cast<int32_t*>(ws);
+    p.heavy_count = d_cnt;
+    p.heavy_list = d_cnt + 1;
+    p.heavy_mark = reinterpret_cast<uint8_t*>(ws + sizeof(int32_t) * (1 + p.heavy_cap));
+    GMI_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(int32_t), ctx->stream));
+    k_wide_tile_load<<<(ntiles + 255) / 256, 256, 0, ctx->stream>>>(
+        c->geom_d, c->bins, p.tiles_x, p.tiles_y, c->B, r, p.heavy_cap, d_cnt + 1, d_cnt,
+        reinterpret_cast<uint8_t*>(ws + sizeof(int32_t) * (1 + p.heavy_cap)));
+    GMI_LAUNCHED(ctx);
+    const dim3 grid(p.heavy_cap + ntiles, p.nsg);
     GMI_CUDA(cudaMemsetAsync(c->special_count_d, 0, sizeof(int32_t), ctx->stream));
     const bool cnt = counts != nullptr;
     switch (cb) {
@@ -861,7 +980,20 @@ bool launch_backward_wide(gmi_ctx* ctx, const gmi_cache* c, const float* upstrea
             GMI_CUDA(cudaFuncSetAttribute(k_backward_wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           kBSmem));
         }
-        k_backward_wide<<<dim3(off[c->B], groups), kBThreads, kBSmem, st>>>(p);
+        const int nunits = off[c->B];
+        p.heavy_cap = std::min(2048, nunits);
+        char* ws = static_cast<char*>(scratch(ctx, WS_TMP, sizeof(int32_t) * (1 + p.heavy_cap) + nunits));
+        int32_t* d_cnt = reinterpret_cast<int32_t*>(ws);
+        uint8_t* d_mark = reinterpret_cast<uint8_t*>(ws + sizeof(int32_t) * (1 + p.heavy_cap));
+        p.heavy_count = d_cnt;
+        p.heavy_list = d_cnt + 1;
+        p.heavy_mark = d_mark;
+        GMI_CUDA(cudaMemsetAsync(d_cnt, 0, sizeof(int32_t), st));
+        k_wide_unit_load<<<(nunits + 255) / 256, 256, 0, st>>>(c->geom_d, c->bins, d_off, c->B, kBSeg,
+                                                                nseg_cap, p.heavy_cap, d_cnt + 1, d_cnt,
+                                                                d_mark);
+        GMI_LAUNCHED(ctx);
+        k_backward_wide<<<dim3(p.heavy_cap + nunits, groups), kBThreads, kBSmem, st>>>(p);
         GMI_LAUNCHED(ctx);
     }
     if (groups > 1) {
