@@ -16,4 +16,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
    --log-file $O/launches_cfg3.csv python bench.py --steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline > $O/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_gather|k_backward_points|k_scatter_emit|k_count4' -c 4 \
    -o $O/full python tools/prof_small.py 4 > $O/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_gather_wide|k_backward_wide' -c 2 \
+   -o $O/wide python tools/prof_cfg5.py 2 > $O/ncu_wide.log 2>&1
+python tools/cfg5_cluster_split.py > $O/cfg5_cluster_split.txt 2>&1
 ls -la $O
