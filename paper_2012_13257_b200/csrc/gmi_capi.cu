@@ -466,6 +466,9 @@ int gmi_ctx_destroy(gmi_ctx* ctx) {
     if (ctx == nullptr) return GMI_OK;
     return guarded([&]() -> int {
         cudaSetDevice(ctx->device);
+        // the grow-only scratch slots go back to the pool with the context
+        for (int s = 0; s < WS_COUNT; ++s)
+            if (ctx->ws_ptr[s]) cudaFreeAsync(ctx->ws_ptr[s], ctx->stream);
         cudaStreamSynchronize(ctx->stream);
         if (ctx->d_issue) cudaFree(ctx->d_issue);
         if (ctx->h_issue) cudaFreeHost(ctx->h_issue);
