@@ -411,6 +411,9 @@ def main():
         e0.record(stream)
         for _ in range(args.e2e_steps):
             e2e_step()
+        # the host calls return with their downloads queued (asynchronous
+        # mode): the end event waits for them on the device
+        ctx.join_host_copies()
         e1.record(stream)
         torch.cuda.synchronize(dev)
         e2e_ms = e0.elapsed_time(e1) / args.e2e_steps

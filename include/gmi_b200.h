@@ -70,8 +70,12 @@ typedef struct gmi_config {
 enum {
     /* Report validation errors asynchronously: forward/backward return as
      * soon as the work is queued and a later gmi_ctx_synchronize() returns
-     * the first error.  Default (0): every call synchronises its stream and
-     * returns the reference's error synchronously. */
+     * the first error.  This includes the host-buffer calls
+     * (gmi_forward_host / gmi_backward_host): their host outputs are
+     * complete, and their host inputs may be reused, after
+     * gmi_ctx_synchronize() — so a backward's upload overlaps the preceding
+     * forward's download.  Default (0): every call synchronises and returns
+     * the reference's error synchronously. */
     GMI_CTX_ASYNC_ERRORS = 1u << 0,
     /* Bit-deterministic fallback-gradient routing (default on). */
     GMI_CTX_NONDETERMINISTIC = 1u << 1
@@ -89,6 +93,10 @@ void* gmi_ctx_stream(const gmi_ctx* ctx);
 int gmi_ctx_set_flags(gmi_ctx* ctx, uint32_t flags);
 /* Waits for queued work; returns the first pending asynchronous error. */
 int gmi_ctx_synchronize(gmi_ctx* ctx);
+/* Makes the ctx stream wait (on the device, no host block) for the copies
+ * queued by asynchronous host-buffer calls, e.g. before recording an event
+ * that must cover their downloads. */
+int gmi_ctx_join_host_copies(gmi_ctx* ctx);
 /* Number of kernels this ctx has launched (for bench gpu_launches). */
 uint64_t gmi_ctx_launch_count(const gmi_ctx* ctx);
 

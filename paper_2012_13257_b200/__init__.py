@@ -150,6 +150,10 @@ class Context:
     def synchronize(self) -> None:
         _check(lib.gmi_ctx_synchronize(self._h))
 
+    def join_host_copies(self) -> None:
+        """The ctx stream waits (device-side) for queued host-buffer copies."""
+        _check(lib.gmi_ctx_join_host_copies(self._h))
+
     @property
     def launch_count(self) -> int:
         return int(lib.gmi_ctx_launch_count(self._h))

@@ -39,6 +39,7 @@ SIGNATURES = {
     "gmi_ctx_stream": (_vp, [_vp]),
     "gmi_ctx_set_flags": (C.c_int, [_vp, C.c_uint32]),
     "gmi_ctx_synchronize": (C.c_int, [_vp]),
+    "gmi_ctx_join_host_copies": (C.c_int, [_vp]),
     "gmi_ctx_launch_count": (C.c_uint64, [_vp]),
     "gmi_ctx_set_profiling": (C.c_int, [_vp, C.c_int]),
     "gmi_ctx_phase_times": (C.c_int, [_vp, _dp, C.POINTER(C.c_uint64), C.c_int]),

@@ -105,7 +105,25 @@ int collect_issue(gmi_ctx* ctx, int B) {
     return GMI_OK;
 }
 
+// The ctx stream waits for the copy streams of the host-buffer API.
+void join_copy_streams(gmi_ctx* ctx) {
+    for (cudaStream_t cs : {ctx->s_in, ctx->s_out}) {
+        if (cs == nullptr) continue;
+        cudaEvent_t ev;
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) continue;
+        cudaEventRecord(ev, cs);
+        cudaStreamWaitEvent(ctx->stream, ev, 0);
+        cudaEventDestroy(ev);
+    }
+}
+
 void free_cache_buffers(gmi_cache* c) {
+    if (c->d2h_done != nullptr) {
+        // an asynchronous gmi_forward_host may still be downloading the image
+        cudaStreamWaitEvent(c->ctx->stream, c->d2h_done, 0);
+        cudaEventDestroy(c->d2h_done);
+        c->d2h_done = nullptr;
+    }
     for (gmi_cache* part : c->parts) {
         free_cache_buffers(part);
         delete part;
@@ -511,7 +529,19 @@ int gmi_ctx_synchronize(gmi_ctx* ctx) {
         if (ctx == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "ctx is null");
         GMI_CUDA(cudaSetDevice(ctx->device));
         GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+        // host-buffer downloads queued by asynchronous host-API calls
+        if (ctx->s_in) GMI_CUDA(cudaStreamSynchronize(ctx->s_in));
+        if (ctx->s_out) GMI_CUDA(cudaStreamSynchronize(ctx->s_out));
         if (ctx->d_issue_cap > 0) return collect_issue(ctx, ctx->d_issue_cap);
+        return GMI_OK;
+    });
+}
+
+int gmi_ctx_join_host_copies(gmi_ctx* ctx) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "ctx is null");
+        GMI_CUDA(cudaSetDevice(ctx->device));
+        join_copy_streams(ctx);
         return GMI_OK;
     });
 }
@@ -671,10 +701,19 @@ int gmi_forward_host(gmi_ctx* ctx, const float* positions, const float* colors, 
                                          cudaMemcpyDeviceToHost, ctx->s_out));
             }
             ctx->flags = saved;
-            GMI_CUDA(cudaStreamSynchronize(ctx->s_out));
-            GMI_CUDA(cudaStreamSynchronize(ctx->s_in));
-            if (rc == GMI_OK) rc = collect_issue(ctx, batch);
-            if (rc == GMI_OK) {
+            GMI_CUDA(cudaEventCreateWithFlags(&c->d2h_done, cudaEventDisableTiming));
+            GMI_CUDA(cudaEventRecord(c->d2h_done, ctx->s_out));
+            // GMI_CTX_ASYNC_ERRORS: return with the image download still
+            // queued on the copy stream (complete after gmi_ctx_synchronize),
+            // so a following gmi_backward_host uploads its upstream while
+            // this image comes down (PCIe is full duplex)
+            const bool async = (saved & GMI_CTX_ASYNC_ERRORS) != 0;
+            if (!async) {
+                GMI_CUDA(cudaStreamSynchronize(ctx->s_out));
+                GMI_CUDA(cudaStreamSynchronize(ctx->s_in));
+            }
+            if (rc == GMI_OK && !async) rc = collect_issue(ctx, batch);
+            if (rc == GMI_OK && !async) {
                 for (gmi_cache* part : c->parts) {
                     int32_t nspec = 0;
                     GMI_CUDA(cudaMemcpyAsync(&nspec, part->special_count_d, sizeof(int32_t),
@@ -763,13 +802,17 @@ int gmi_backward_host(gmi_ctx* ctx, const float* positions, const float* colors,
             GMI_CUDA(cudaMemcpyAsync(d_positions + o * N * 2, dp + o * N * 2, sizeof(float) * n * N * 2,
                                      cudaMemcpyDeviceToHost, ctx->s_out));
         }
-        cudaEvent_t out_done = E.get();
-        GMI_CUDA(cudaEventRecord(out_done, ctx->s_out));
-        GMI_CUDA(cudaStreamWaitEvent(ctx->stream, out_done, 0));
-        gmi_host::dfree(ctx, dup);
-        gmi_host::dfree(ctx, dc);
-        gmi_host::dfree(ctx, dp);
-        GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+        // staging buffers return to the pool behind the downloads (stream-
+        // ordered on the copy stream, which follows the last chunk's kernels),
+        // so the ctx stream — and the next call's uploads — need not wait
+        GMI_CUDA(cudaFreeAsync(dup, ctx->s_out));
+        GMI_CUDA(cudaFreeAsync(dc, ctx->s_out));
+        GMI_CUDA(cudaFreeAsync(dp, ctx->s_out));
+        // GMI_CTX_ASYNC_ERRORS: gradients complete after gmi_ctx_synchronize
+        if (!(ctx->flags & GMI_CTX_ASYNC_ERRORS)) {
+            GMI_CUDA(cudaStreamSynchronize(ctx->s_out));
+            GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
         return GMI_OK;
     });
 }

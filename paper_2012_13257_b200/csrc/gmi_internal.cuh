@@ -160,6 +160,9 @@ struct gmi_cache {
     // part_b0[k] + parts[k]->B), each a complete cache of its own
     std::vector<gmi_cache*> parts;
     std::vector<int> part_b0;
+    // recorded on the copy stream after the image download (host API); the
+    // buffers are freed behind it
+    cudaEvent_t d2h_done = nullptr;
 };
 
 namespace gmi_host {

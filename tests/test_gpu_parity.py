@@ -308,3 +308,20 @@ def test_optimize_points_matches_reference(gmi, ctx, opt):
     assert_close(out["points"].colors, rc, what="colors")
     steps_logged = sorted({e[0] for e in out["trajectory"]})
     assert steps_logged == [0, 4, 6]
+
+
+def test_async_host_api_matches_sync(gmi, ctx, orc):
+    # GMI_CTX_ASYNC_ERRORS: the host-buffer calls return with their copies
+    # queued; after gmi_ctx_synchronize the outputs equal the synchronous ones
+    pos, col, up = orc.synth_batch(21, 4, 3000, 3, 100, 90)
+    img, cache = gmi.forward_batch(pos, col, 100, 90, 1.0, 3.0, ctx=ctx)
+    dc, dp = gmi.backward_batch(pos, col, cache, up, 1.0, 3.0, ctx=ctx)
+    actx = gmi.Context(0)
+    actx.set_flags(1)
+    for _ in range(2):
+        img2, cache2 = gmi.forward_batch(pos, col, 100, 90, 1.0, 3.0, ctx=actx)
+        dc2, dp2 = gmi.backward_batch(pos, col, cache2, up, 1.0, 3.0, ctx=actx)
+        del cache2
+        actx.synchronize()
+        assert np.array_equal(img, img2)
+        assert np.array_equal(dc, dc2) and np.array_equal(dp, dp2)
