@@ -44,6 +44,7 @@ typedef enum gmi_status {
     GMI_ERR_CONFIG_INVALID = 6,
     GMI_ERR_CACHE_MISMATCH = 7,
     GMI_ERR_INVALID_DIMENSIONS = 8,
+    GMI_ERR_INVALID_FACTOR = 9,
     /* B200-side failures (no reference equivalent) */
     GMI_ERR_CUDA = 100,
     GMI_ERR_INVALID_ARGUMENT = 101,
@@ -212,6 +213,24 @@ int gmi_optimize_points_host(gmi_ctx* ctx, float* positions, float* colors, int3
                              int32_t num_points, int32_t channels, const gmi_config* cfg,
                              const float* target, int32_t steps, double learning_rate,
                              uint32_t flags, double* loss_curve);
+
+/* ---- run_benchmark's GMM branch (benchmark.cpp:88-107) for one image ------
+ * image: HOST H x W x C.  Known points at the block centres of `lowres`
+ * (HOST lh x lw x C, lh = ceil(H/factor), lw = ceil(W/factor);
+ * point_set_from_lowres, benchmark.cpp:24-39) or, lowres == NULL, of the
+ * block means of `image` computed on the device (block_mean_downsample,
+ * imaging.cpp:306-350).  One forward per sigma over the full W x H frame
+ * (make_config: cutoff 3 sigma, NearestPoint), L1 against `image` (l1_metric,
+ * imaging.cpp:376-386): l1[k] and ms[k] (device time of that forward; ms may
+ * be NULL) per sigma; *best = the first sigma with the smallest L1
+ * (benchmark.cpp:101-106); best_image (HOST H x W x C, may be NULL) receives
+ * that forward's output.  sigmas == NULL: auto_sigma_candidates(factor) =
+ * {0.4, 0.5, 0.6} * factor (benchmark.cpp:48-50), n_sigma must be 3.
+ * factor < 1: GMI_ERR_INVALID_FACTOR (benchmark.cpp:62-68). */
+int gmi_gmm_benchmark_host(gmi_ctx* ctx, const float* image, int32_t width, int32_t height,
+                           int32_t channels, int32_t factor, const float* lowres,
+                           const double* sigmas, int32_t n_sigma, double* l1, double* ms,
+                           int32_t* best, float* best_image);
 
 #ifdef __cplusplus
 } /* extern "C" */

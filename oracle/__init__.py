@@ -115,6 +115,31 @@ class Reference:
         if rc != 0:
             raise OracleError(rc, self.lib.ref_last_error().decode())
 
+    def run_benchmark_gmm(self, image, factor, sigma=None, box=True):
+        """gmi::run_benchmark (benchmark.cpp:53-120), method "gmm", one image,
+        one factor -> (l1, sigma_used, wall_time_ms)."""
+        img = np.ascontiguousarray(image, np.float64)
+        h, w, ch = img.shape
+        L = self.lib
+        L.ref_run_benchmark_gmm.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                            C.c_int, _dp, _dp, _dp]
+        l1, su, ms = C.c_double(), C.c_double(), C.c_double()
+        self._check(L.ref_run_benchmark_gmm(_ptr(img, _dp), w, h, ch, factor,
+                                            0.0 if sigma is None else float(sigma), int(box),
+                                            C.byref(l1), C.byref(su), C.byref(ms)))
+        return l1.value, su.value, ms.value
+
+    def block_mean_downsample(self, image, factor):
+        """gmi::block_mean_downsample (imaging.cpp:343-350)."""
+        img = np.ascontiguousarray(image, np.float64)
+        h, w, ch = img.shape
+        lh, lw = (h + factor - 1) // factor, (w + factor - 1) // factor
+        out = np.zeros((lh, lw, ch))
+        L = self.lib
+        L.ref_block_mean_downsample.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
+        self._check(L.ref_block_mean_downsample(_ptr(img, _dp), w, h, ch, factor, _ptr(out, _dp)))
+        return out
+
     def optimize_points(self, pos, col, target, sigma, cutoff, steps, lr, opt_pos=True,
                         opt_col=False, fallback=0):
         """gmi::optimize_points (optimize.cpp:47-98) -> (positions, colors, loss_curve)."""
@@ -389,3 +414,64 @@ class Oracle:
         self.lib.orc_synth_batch(seed, batch, n, channels, width, height, cluster_frac, cluster_px,
                                  _ptr(pos, _fp), _ptr(col, _fp), _ptr(up, _fp))
         return pos, col, up
+
+
+# ---------------------------------------------------------------------------
+# run_benchmark's GMM branch (benchmark.cpp:88-107), restated on top of the
+# C oracle's forward.
+
+
+def block_mean_downsample(image, factor):
+    """grid_subsample colours (imaging.cpp:306-341): per block, the f64 sum in
+    row-major order times 1/area; block_mean_downsample (343-350) lays them
+    out as an lh x lw x C raster."""
+    img = np.asarray(image, np.float64)
+    h, w, ch = img.shape
+    lh, lw = (h + factor - 1) // factor, (w + factor - 1) // factor
+    pad = np.zeros((lh * factor, lw * factor, ch))
+    pad[:h, :w] = img
+    blocks = pad.reshape(lh, factor, lw, factor, ch)
+    total = np.zeros((lh, lw, ch))
+    for r in range(factor):           # the reference's loop order, sequential
+        for c in range(factor):       # per block (padding adds exact zeros)
+            total = total + blocks[:, r, :, c, :]
+    rows = np.minimum(h, (np.arange(lh) + 1) * factor) - np.arange(lh) * factor
+    cols = np.minimum(w, (np.arange(lw) + 1) * factor) - np.arange(lw) * factor
+    inv_area = 1.0 / (rows[:, None] * cols[None, :]).astype(np.float64)
+    return total * inv_area[:, :, None]
+
+
+def point_set_from_lowres(lowres, factor):
+    """point_set_from_lowres (benchmark.cpp:24-39): block centres."""
+    lh, lw, ch = lowres.shape
+    half = (factor - 1) / 2.0
+    bc, br = np.meshgrid(np.arange(lw), np.arange(lh))
+    pos = np.stack([bc.ravel() * float(factor) + half, br.ravel() * float(factor) + half], 1)
+    return pos, np.asarray(lowres, np.float64).reshape(-1, ch)
+
+
+def l1_metric(a, b):
+    """l1_metric (imaging.cpp:376-386): sequential f64 sum / size."""
+    d = np.abs(np.asarray(a, np.float64).ravel() - np.asarray(b, np.float64).ravel())
+    return float(np.cumsum(d)[-1] / d.size) if d.size else 0.0
+
+
+def gmm_benchmark(orc, image, factor, sigmas=None, lowres=None):
+    """The GMM row of run_benchmark for one image and factor with the C
+    oracle's forward: (l1 per sigma, index of the first smallest)."""
+    img = np.asarray(image, np.float64)
+    h, w, _ = img.shape
+    if lowres is None:
+        lowres = block_mean_downsample(img, factor)
+    pos, col = point_set_from_lowres(lowres, factor)
+    if sigmas is None:
+        sigmas = [0.4 * factor, 0.5 * factor, 0.6 * factor]  # benchmark.cpp:48-50
+    l1 = []
+    for s in sigmas:
+        out = orc.forward(pos, col, w, h, s, 3.0 * s)["image"]
+        l1.append(l1_metric(out, img))
+    best = 0
+    for k in range(1, len(l1)):
+        if l1[k] < l1[best]:
+            best = k
+    return l1, best

@@ -2,7 +2,8 @@
 //
 // extern "C" shim over the UNMODIFIED reference implementation, compiled
 // from the reference's own sources where they lie
-// (/root/reference/proj/src/{core,bin_grid,engine,oracle,validate}.cpp) by
+// (/root/reference/proj/src/{core,bin_grid,engine,oracle,validate,optimize,
+// imaging,resample,benchmark}.cpp) by
 // oracle/Makefile into oracle/_ref/libgmi_ref.so.  It lets the Python test
 // harness and bench.py's cpu_baseline / --impl reference legs call the
 // reference's C++ API (gmi::forward / gmi::backward / gmi::build_bin_grid /
@@ -19,8 +20,10 @@
 #include <string>
 #include <vector>
 
+#include "gmi/benchmark.hpp"
 #include "gmi/bin_grid.hpp"
 #include "gmi/engine.hpp"
+#include "gmi/imaging.hpp"
 #include "gmi/optimize.hpp"
 #include "gmi/oracle.hpp"
 #include "gmi/rng.hpp"
@@ -301,6 +304,39 @@ int ref_optimize_points(const double* pos, const double* col, int n, int channel
         }
         std::memcpy(out_col, r.points.colors.data(), sizeof(double) * r.points.colors.size());
         std::memcpy(loss_curve, r.loss_curve.data(), sizeof(double) * r.loss_curve.size());
+    });
+}
+
+// gmi::run_benchmark (benchmark.cpp:53-120) restricted to the "gmm" method
+// for one image and one factor: the row's l1, sigma_used and wall_time_ms.
+// sigma <= 0: the auto sweep (auto_sigma_candidates, benchmark.cpp:48-50).
+// box != 0: BoxAverage downsampling, else Bicubic (benchmark.cpp:73-80).
+int ref_run_benchmark_gmm(const double* image, int width, int height, int channels, int factor,
+                          double sigma, int box, double* l1, double* sigma_used, double* ms) {
+    return guarded([&] {
+        gmi::ImageBuffer img = gmi::ImageBuffer::zeros(height, width, channels);
+        img.data.assign(image, image + static_cast<std::size_t>(height) * width * channels);
+        gmi::BenchmarkOptions opt;
+        opt.factors = {factor};
+        opt.methods = {"gmm"};
+        if (sigma > 0.0) opt.sigma = sigma;
+        opt.downsample = box ? gmi::DownsampleMode::BoxAverage : gmi::DownsampleMode::Bicubic;
+        const std::vector<gmi::BenchmarkRow> rows = gmi::run_benchmark({{"img", img}}, opt);
+        *l1 = rows.at(0).l1;
+        *sigma_used = rows.at(0).sigma_used.value_or(0.0);
+        *ms = rows.at(0).wall_time_ms;
+    });
+}
+
+// gmi::block_mean_downsample (imaging.cpp:343-350) and gmi::l1_metric
+// (imaging.cpp:376-386).
+int ref_block_mean_downsample(const double* image, int width, int height, int channels,
+                              int factor, double* out) {
+    return guarded([&] {
+        gmi::ImageBuffer img = gmi::ImageBuffer::zeros(height, width, channels);
+        img.data.assign(image, image + static_cast<std::size_t>(height) * width * channels);
+        const gmi::ImageBuffer low = gmi::block_mean_downsample(img, factor);
+        std::memcpy(out, low.data.data(), sizeof(double) * low.data.size());
     });
 }
 

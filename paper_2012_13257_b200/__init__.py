@@ -38,14 +38,15 @@ from ._lib import GmiConfig, lib
 __all__ = [
     "ForwardCache", "GmiError", "PointSet", "backward", "forward", "gaussian_weight",
     "forward_batch", "backward_batch", "Context", "bin_grid", "forward_counts",
-    "default_context", "optimize_points", "ERROR_NAMES", "__version__",
+    "default_context", "optimize_points", "gmm_benchmark", "ERROR_NAMES", "__version__",
 ]
 
 __version__ = "0.1.0"
 
 # gmi::ErrorCode names (core.hpp:35-50), index = code - 1
 ERROR_NAMES = ["NonFiniteValue", "ColorOutOfRange", "EmptyPointSet", "ShapeMismatch",
-               "InvalidCellSize", "ConfigInvalid", "CacheMismatch", "InvalidDimensions"]
+               "InvalidCellSize", "ConfigInvalid", "CacheMismatch", "InvalidDimensions",
+               "InvalidFactor"]
 
 
 class GmiError(RuntimeError):
@@ -440,6 +441,47 @@ def optimize_points(points: PointSet, target, sigma: float, radius: float = 0.0,
     return {"points": pts, "loss_curve": np.asarray(loss_curve), "trajectory": trajectory,
             "mean_displacement": float(d.mean()) if n else 0.0,
             "max_displacement": float(d.max()) if n else 0.0}
+
+
+def gmm_benchmark(image, factor: int, sigma: float | None = None, lowres=None,
+                  ctx: Context | None = None) -> dict:
+    """The "gmm" row of run_benchmark (benchmark.cpp:88-107) for one image and
+    one factor, on the GPU: known points at the block centres of `lowres`
+    (default: the block means of `image`, block_mean_downsample), one forward
+    per sigma (default: the auto sweep {0.4, 0.5, 0.6} x factor), L1 against
+    `image`.  Returns the BenchmarkRow fields (factor, method, sigma_used, l1,
+    wall_time_ms = device time of that forward) plus the whole sweep and the
+    chosen reconstruction."""
+    ctx = ctx or default_context()
+    img = np.ascontiguousarray(np.asarray(image, np.float32))
+    if img.ndim == 2:
+        img = img[:, :, None]
+    h, w, ch = img.shape
+    sig = None if sigma is None else np.array([float(sigma)], np.float64)
+    n = 3 if sig is None else 1
+    low = None
+    if lowres is not None:
+        low = np.ascontiguousarray(np.asarray(lowres, np.float32))
+        if low.ndim == 2:
+            low = low[:, :, None]
+        if low.shape != ((h + factor - 1) // factor, (w + factor - 1) // factor, ch):
+            raise GmiError(4, "lowres must be ceil(H/factor) x ceil(W/factor) x C")
+    l1 = np.zeros(n)
+    ms = np.zeros(n)
+    best = C.c_int32()
+    out = np.empty_like(img)
+    fp = C.POINTER(C.c_float)
+    dp = C.POINTER(C.c_double)
+    _check(lib.gmi_gmm_benchmark_host(ctx.handle, img.ctypes.data_as(fp), w, h, ch, int(factor),
+                                      low.ctypes.data_as(fp) if low is not None else None,
+                                      sig.ctypes.data_as(dp) if sig is not None else None, n,
+                                      l1.ctypes.data_as(dp), ms.ctypes.data_as(dp), C.byref(best),
+                                      out.ctypes.data_as(fp)))
+    sigmas = [0.4 * factor, 0.5 * factor, 0.6 * factor] if sig is None else [float(sigma)]
+    b = best.value
+    return {"factor": int(factor), "method": "gmm", "sigma_used": sigmas[b], "l1": float(l1[b]),
+            "wall_time_ms": float(ms[b]), "sigmas": sigmas, "l1_per_sigma": l1.tolist(),
+            "ms_per_sigma": ms.tolist(), "image": out}
 
 
 def forward_counts(cache: ForwardCache) -> np.ndarray:

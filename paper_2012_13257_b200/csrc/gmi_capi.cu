@@ -381,6 +381,58 @@ int do_optimize(gmi_ctx* ctx, float* pos, float* col, int B, int N, int C,
     return rc;
 }
 
+// ---- run_benchmark's GMM branch (benchmark.cpp:88-107) ----
+// grid_subsample colours (imaging.cpp:306-341): thread per (block, channel),
+// the f64 sum in the reference's row-major order times 1/area.
+__global__ void k_block_mean(const float* __restrict__ img, int W, int H, int C, int f, int lw,
+                             int lh, float* __restrict__ low) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= lw * lh * C) return;
+    const int ch = k % C, blk = k / C, bc = blk % lw, br = blk / lw;
+    const int r0 = br * f, r1 = min(H, r0 + f), c0 = bc * f, c1 = min(W, c0 + f);
+    const double inv_area = 1.0 / static_cast<double>((r1 - r0) * (c1 - c0));
+    double sum = 0.0;
+    for (int r = r0; r < r1; ++r)
+        for (int c = c0; c < c1; ++c)
+            sum = __dadd_rn(sum, static_cast<double>(img[(static_cast<size_t>(r) * W + c) * C + ch]));
+    low[k] = static_cast<float>(__dmul_rn(sum, inv_area));
+}
+
+// point_set_from_lowres (benchmark.cpp:24-39): block centres, exact in fp32.
+__global__ void k_block_centres(float* __restrict__ pos, int lw, int lh, int f) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= lw * lh) return;
+    const double half = (f - 1) / 2.0;
+    pos[2 * k] = static_cast<float>((k % lw) * static_cast<double>(f) + half);
+    pos[2 * k + 1] = static_cast<float>((k / lw) * static_cast<double>(f) + half);
+}
+
+// l1_metric (imaging.cpp:376-386): per-block f64 partial sums of |a - b|,
+// summed in block order by k_l1_finalize (deterministic).
+__global__ void k_l1_partial(const float* __restrict__ a, const float* __restrict__ b, size_t n,
+                             double* __restrict__ partial) {
+    __shared__ double red[kLossThreads / 32];
+    double s = 0.0;
+    for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<size_t>(gridDim.x) * blockDim.x)
+        s += fabs(static_cast<double>(a[k]) - static_cast<double>(b[k]));
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kLossThreads / 32; ++w) t += red[w];
+        partial[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_l1_finalize(const double* __restrict__ partial, int nblk, double inv,
+                              double* __restrict__ out) {
+    double t = 0.0;
+    for (int k = 0; k < nblk; ++k) t += partial[k];
+    *out = t * inv;
+}
+
 }  // namespace
 
 void host_trace(const char* what) {
@@ -442,6 +494,7 @@ const char* gmi_error_name(int code) {
         case GMI_ERR_CONFIG_INVALID: return "ConfigInvalid";
         case GMI_ERR_CACHE_MISMATCH: return "CacheMismatch";
         case GMI_ERR_INVALID_DIMENSIONS: return "InvalidDimensions";
+        case GMI_ERR_INVALID_FACTOR: return "InvalidFactor";
         case GMI_ERR_CUDA: return "CudaError";
         case GMI_ERR_INVALID_ARGUMENT: return "InvalidArgument";
         case GMI_ERR_OUT_OF_MEMORY: return "OutOfMemory";
@@ -1026,6 +1079,102 @@ int gmi_optimize_points(gmi_ctx* ctx, float* positions, float* colors, int32_t b
         GMI_CUDA(cudaSetDevice(ctx->device));
         return do_optimize(ctx, positions, colors, batch, num_points, channels, cfg, target, steps,
                            learning_rate, flags, loss_curve);
+    });
+}
+
+int gmi_gmm_benchmark_host(gmi_ctx* ctx, const float* image, int32_t width, int32_t height,
+                           int32_t channels, int32_t factor, const float* lowres,
+                           const double* sigmas, int32_t n_sigma, double* l1, double* ms,
+                           int32_t* best, float* best_image) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr || image == nullptr || l1 == nullptr || best == nullptr)
+            return fail(GMI_ERR_INVALID_ARGUMENT, "null argument");
+        if (width < 1 || height < 1 || channels < 1)
+            return fail(GMI_ERR_INVALID_DIMENSIONS, "image must be at least 1x1x1");
+        // benchmark.cpp:62-68
+        if (factor < 1) return fail(GMI_ERR_INVALID_FACTOR, "factors must be positive integers");
+        std::vector<double> sig;
+        if (sigmas == nullptr) {
+            sig = {0.4 * factor, 0.5 * factor, 0.6 * factor};  // auto_sigma_candidates
+            if (n_sigma != 3) return fail(GMI_ERR_INVALID_ARGUMENT, "auto sweep has 3 sigmas");
+        } else {
+            if (n_sigma < 1) return fail(GMI_ERR_INVALID_ARGUMENT, "n_sigma must be >= 1");
+            sig.assign(sigmas, sigmas + n_sigma);
+        }
+        GMI_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t st = ctx->stream;
+        const int lw = (width + factor - 1) / factor, lh = (height + factor - 1) / factor;
+        const int N = lw * lh;
+        const size_t hwc = static_cast<size_t>(height) * width * channels;
+        float* dimg = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * hwc));
+        float* dlow = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * N * channels));
+        float* dpos = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * N * 2));
+        float* dout = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * hwc * sig.size()));
+        const int nblk = static_cast<int>(std::min<size_t>((hwc + kLossThreads - 1) / kLossThreads,
+                                                           2 * static_cast<size_t>(ctx->num_sms)));
+        double* partial = static_cast<double*>(gmi_host::dalloc(ctx, sizeof(double) * nblk));
+        double* dl1 = static_cast<double*>(gmi_host::dalloc(ctx, sizeof(double) * sig.size()));
+        int rc = GMI_OK;
+        std::vector<cudaEvent_t> ev(2 * sig.size(), nullptr);
+        try {
+            GMI_CUDA(cudaMemcpyAsync(dimg, image, sizeof(float) * hwc, cudaMemcpyHostToDevice, st));
+            if (lowres != nullptr) {
+                GMI_CUDA(cudaMemcpyAsync(dlow, lowres, sizeof(float) * N * channels,
+                                         cudaMemcpyHostToDevice, st));
+            } else {
+                // block_mean_downsample (imaging.cpp:343-350)
+                k_block_mean<<<(N * channels + 255) / 256, 256, 0, st>>>(dimg, width, height, channels,
+                                                                         factor, lw, lh, dlow);
+                GMI_LAUNCHED(ctx);
+            }
+            k_block_centres<<<(N + 255) / 256, 256, 0, st>>>(dpos, lw, lh, factor);
+            GMI_LAUNCHED(ctx);
+            for (auto& e : ev) GMI_CUDA(cudaEventCreate(&e));
+            for (size_t k = 0; k < sig.size() && rc == GMI_OK; ++k) {
+                // make_config(sigma, full) (core.hpp:90-94): cutoff 3 sigma
+                const gmi_config cfg{sig[k], 3.0 * sig[k], GMI_FALLBACK_NEAREST, width, height};
+                rc = check_config(&cfg);
+                if (rc != GMI_OK) break;
+                gmi_cache c;
+                c.ctx = ctx;
+                GMI_CUDA(cudaEventRecord(ev[2 * k], st));
+                rc = do_forward(ctx, dpos, dlow, 1, N, channels, &cfg, dout + k * hwc, &c, nullptr);
+                GMI_CUDA(cudaEventRecord(ev[2 * k + 1], st));
+                free_cache_buffers(&c);
+                if (rc != GMI_OK) break;
+                k_l1_partial<<<nblk, kLossThreads, 0, st>>>(dout + k * hwc, dimg, hwc, partial);
+                GMI_LAUNCHED(ctx);
+                k_l1_finalize<<<1, 1, 0, st>>>(partial, nblk, 1.0 / static_cast<double>(hwc), dl1 + k);
+                GMI_LAUNCHED(ctx);
+            }
+            if (rc == GMI_OK) {
+                GMI_CUDA(cudaMemcpyAsync(l1, dl1, sizeof(double) * sig.size(), cudaMemcpyDeviceToHost, st));
+                GMI_CUDA(cudaStreamSynchronize(st));
+                // the first sigma with the smallest L1 (benchmark.cpp:101-106)
+                int b = 0;
+                for (size_t k = 1; k < sig.size(); ++k)
+                    if (l1[k] < l1[b]) b = static_cast<int>(k);
+                *best = b;
+                if (ms != nullptr)
+                    for (size_t k = 0; k < sig.size(); ++k) {
+                        float t = 0.f;
+                        GMI_CUDA(cudaEventElapsedTime(&t, ev[2 * k], ev[2 * k + 1]));
+                        ms[k] = t;
+                    }
+                if (best_image != nullptr)
+                    GMI_CUDA(cudaMemcpyAsync(best_image, dout + b * hwc, sizeof(float) * hwc,
+                                             cudaMemcpyDeviceToHost, st));
+            }
+        } catch (...) {
+            for (auto e : ev) if (e) cudaEventDestroy(e);
+            throw;
+        }
+        for (auto e : ev) if (e) cudaEventDestroy(e);
+        for (void* q : {static_cast<void*>(dimg), static_cast<void*>(dlow), static_cast<void*>(dpos),
+                        static_cast<void*>(dout), static_cast<void*>(partial), static_cast<void*>(dl1)})
+            gmi_host::dfree(ctx, q);
+        GMI_CUDA(cudaStreamSynchronize(st));
+        return rc;
     });
 }
 

@@ -325,3 +325,34 @@ def test_async_host_api_matches_sync(gmi, ctx, orc):
         actx.synchronize()
         assert np.array_equal(img, img2)
         assert np.array_equal(dc, dc2) and np.array_equal(dp, dp2)
+
+
+@pytest.mark.parametrize("factor,ch", [(2, 3), (3, 1), (4, 3), (8, 3)])
+def test_gmm_benchmark_matches_reference(gmi, ctx, orc, factor, ch):
+    # the GMM row of run_benchmark on the device vs the restatement (pinned
+    # to the reference in test_oracle.py) and, when built, the reference
+    import oracle
+    rng = np.random.default_rng(factor)
+    yy, xx = np.mgrid[0:67, 0:75]
+    base = 0.5 + 0.4 * np.sin(xx / 7.0)[:, :, None] * np.cos(yy / 5.0)[:, :, None]
+    img = np.clip(base + 0.05 * rng.standard_normal((67, 75, ch)), 0, 1).astype(np.float32)
+    row = gmi.gmm_benchmark(img, factor, ctx=ctx)
+    l1, best = oracle.gmm_benchmark(orc, img.astype(np.float64), factor)
+    assert row["sigmas"][best] == row["sigma_used"]
+    np.testing.assert_allclose(row["l1_per_sigma"], l1, rtol=1e-5, atol=1e-7)
+    if oracle.reference_available():
+        rl1, rsig, _ = oracle.Reference().run_benchmark_gmm(img.astype(np.float64), factor)
+        assert rsig == row["sigma_used"]
+        assert abs(rl1 - row["l1"]) <= 1e-7 + 1e-5 * rl1
+    # a caller-supplied low-resolution raster and a fixed sigma
+    low = oracle.block_mean_downsample(img.astype(np.float64), factor).astype(np.float32)
+    row2 = gmi.gmm_benchmark(img, factor, sigma=0.45 * factor, lowres=low, ctx=ctx)
+    l1b, _ = oracle.gmm_benchmark(orc, img.astype(np.float64), factor, sigmas=[0.45 * factor],
+                                  lowres=low.astype(np.float64))
+    np.testing.assert_allclose(row2["l1"], l1b[0], rtol=1e-5, atol=1e-7)
+
+
+def test_gmm_benchmark_invalid_factor(gmi, ctx):
+    with pytest.raises(gmi.GmiError) as e:
+        gmi.gmm_benchmark(np.zeros((8, 8, 1), np.float32), 0, ctx=ctx)
+    assert e.value.code == 9

@@ -192,3 +192,19 @@ def test_reference_oracle_untruncated(ref):
         ref.free_cache(f)
         o = ref.oracle_forward(p, c, w, h, s)
         np.testing.assert_allclose(f["image"], o, rtol=1e-12, atol=1e-300)
+
+
+def test_gmm_benchmark_restatement_matches_reference(ref):
+    # run_benchmark's GMM branch (benchmark.cpp:88-107): block means, block
+    # centres, the sigma sweep and l1_metric, restated on the C oracle
+    import oracle
+    orc = oracle.Oracle()
+    rng = np.random.default_rng(5)
+    img = rng.uniform(0, 1, (29, 34, 3)).astype(np.float32).astype(np.float64)
+    for f in (1, 2, 3, 5):
+        assert np.array_equal(oracle.block_mean_downsample(img, f), ref.block_mean_downsample(img, f))
+        l1, best = oracle.gmm_benchmark(orc, img, f)
+        rl1, rsig, _ = ref.run_benchmark_gmm(img, f)
+        assert l1[best] == rl1 and [0.4 * f, 0.5 * f, 0.6 * f][best] == rsig
+    l1, best = oracle.gmm_benchmark(orc, img[:, :, :1], 4, sigmas=[1.7])
+    assert l1[0] == ref.run_benchmark_gmm(img[:, :, :1], 4, sigma=1.7)[0]
