@@ -47,6 +47,31 @@ CONFIGS = {
 }
 
 
+def pcie_duplex_gbps(dev, mib: int = 256) -> float:
+    """Pinned host<->device copy rate with both directions in flight (GB/s
+    each way, best of 3): the ceiling of the host-buffer (e2e) step."""
+    import torch
+    n = mib << 18
+    h1, h2 = torch.empty(n, pin_memory=True), torch.empty(n, pin_memory=True)
+    d1, d2 = torch.empty(n, device=dev), torch.empty(n, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    best = 1e9
+    for _ in range(3):
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        with torch.cuda.stream(s1):
+            d1.copy_(h1, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+        torch.cuda.current_stream(dev).wait_stream(s1)
+        torch.cuda.current_stream(dev).wait_stream(s2)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        best = min(best, e0.elapsed_time(e1))
+    return 4 * n / (best * 1e-3) / 1e9
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -423,6 +448,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
         e2e_value = world * B * W * H / (e2e_ms * 1e-3) / 1e6
+        pcie = pcie_duplex_gbps(dev)
     # forward_host uploads positions+colours and downloads the image;
     # backward_host uploads upstream and downloads both gradients
     h2d = B * N * 4 * (2 + C) + (0 if fwd_only else B * H * W * C * 4)
@@ -455,7 +481,13 @@ def main():
                           "step_frac": round(step_fp32_frac, 4),
                           "counts": "fwd 6+C, bwd 11+2C FP32 instr per (pixel,point) pair (SURVEY §8d)"},
         "e2e": ({"value": round(e2e_value, 2), "unit": "Mpix/s", "h2d_bytes_per_step": h2d,
-                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3)} if e2e_ms else None),
+                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3),
+                 # the e2e bound: both directions' bytes at the measured
+                 # pinned full-duplex PCIe rate of this box
+                 "roofline": {"bound": "pcie_duplex", "peak_GBps_each_way": round(pcie, 1),
+                              "bound_ms": round(max(h2d, d2h) / (pcie * 1e9) * 1e3, 3),
+                              "frac": round(max(h2d, d2h) / (pcie * 1e9) * 1e3 / e2e_ms, 4)}}
+                if e2e_ms else None),
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
