@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(256) k_emit_rec(ScatterEmitParams p, const int
 // capacity) get their records in ascending original index, so chunk
 // membership — and the summation order — is independent of the atomic
 // arrival order (bit-deterministic results for clustered inputs).
-constexpr int kBigRecCell = 1024;   // = the fast gather's chunk capacity (kCap)
+constexpr int kBigRecCell = 640;    // = the fast gather's chunk capacity (kCap)
 constexpr int kBigRecSmem = 4096;   // cells up to this size sort in shared memory
 
 __global__ void k_find_big_cells(const Geom* __restrict__ geom, const int32_t* __restrict__ bins,

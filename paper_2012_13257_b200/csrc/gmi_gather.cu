@@ -38,7 +38,7 @@ namespace {
 constexpr int kTW = 64, kTH = 16;
 constexpr int kNW = kTH / 2;       // warps (row pairs)
 constexpr int kNT = kNW * 32;      // threads
-constexpr int kCap = 1024;         // staged candidates per chunk
+constexpr int kCap = 640;          // staged candidates per chunk (= K1's kBigRecCell)
 constexpr int kRsMax = 32;         // cell-row runs per chunk
 constexpr int kColMax = 128;       // 1-px columns across the tile's reach
 constexpr int kBinMax = 2048;      // (column, row-pair) bins (+1 flag bin)
@@ -46,16 +46,16 @@ constexpr int kMultiCap = kNW * (kColMax + 1);  // multi-bin list, shares wcs
 
 template <int CC>
 struct SmemGather {
+    union {
+        // the chunk's 32-byte records in run order, bulk-copied by TMA:
+        // R[2k] = (x, y, c0, c1), R[2k+1] = (c2, c3, idx | flag, 0)
+        float4 R[2 * kCap];
+        uint16_t wl[kNW][kCap];            // per-warp column-major lists (after C)
+    } u;
     float4 A[kCap];                        // mu_x, mu_y, c0, c1   (bin order)
     float2 Bc[CC > 2 ? kCap : 1];          // c2, c3
-    int idx[kCap];                         // original index (+ flag bit)
-    union {
-        struct {
-            int key[kCap];                 // bin of staged candidate k (-1: dropped)
-            int slot[kCap];                // its slot in the image's SoA
-        } st;
-        uint16_t wl[kNW][kCap];            // per-warp column-major lists
-    } u;
+    int idx[kCap];                         // original index
+    int key[kCap];                         // bin of staged record k (-1: dropped)
     int bin[kBinMax + 2];                  // counts -> inclusive ends -> starts
     union {
         uint16_t wcs[kNW][kColMax + 1];    // per-warp column starts in wl
@@ -67,13 +67,13 @@ struct SmemGather {
     int n_multi;
     int n_runs, cur_cy, cur_off, done, pre;
     int cx0, cx1, cy1;
+    unsigned long long mbar;               // TMA completion barrier
 };
 
 struct GatherParams {
     const Geom* geom;
     const int32_t* bins;
     const float4* rec;  // [B][N][2]: (x, y, c0, c1) (c2, c3, idx|flag, 0)
-    const float* ccol;  // C > 4: [B][N][C] colours in bin order
     int N, C, W, H;
     int ncol, nyb, dyb, rc;   // bin geometry (see launch_gather_fast)
     uint8_t qlo[32], qhi[32]; // per-lane column window [qlo, qhi]
@@ -89,21 +89,18 @@ struct GatherParams {
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
-template <int CC, bool kCount, bool kMulti>
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int CC, bool kCount>
 __global__ void __launch_bounds__(kNT, 4)
 k_gather(GatherParams p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     SmemGather<CC>& S = *reinterpret_cast<SmemGather<CC>*>(smem_raw);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // grid (tiles_x, tiles_y, B * groups): channel group g = blockIdx.z %
-    // groups handles channels [4g, 4g + 4) (C > 4: the weights are
-    // recomputed per group; group 0 owns W, counts and the fallback list)
-    const int groups = kMulti ? (p.C + CC - 1) / CC : 1;
-    const int grp = kMulti ? static_cast<int>(blockIdx.z) % groups : 0;
-    const int ch0 = grp * CC;
-    const int nch = kMulti ? min(CC, p.C - ch0) : p.C;
-    const int b = kMulti ? static_cast<int>(blockIdx.z) / groups : static_cast<int>(blockIdx.z);
+    const int b = static_cast<int>(blockIdx.z);
     const int y0 = blockIdx.y * kTH;
     const int x0 = blockIdx.x * kTW;
     const Geom g = p.geom[b];
@@ -140,8 +137,14 @@ k_gather(GatherParams p) {
     // flagged points: generous band test (decided exactly by the f64 predicate)
     const float fb_lo = static_cast<float>(ya) - static_cast<float>(p.r64) - 1.0f;
     const float fb_hi = static_cast<float>(ya + 1) + static_cast<float>(p.r64) + 1.0f;
+    const uint32_t mbar = smem_u32(&S.mbar);
+    uint32_t phase = 0;
 
     if (warp == 0) {
+        if (lane == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
         // the f64 cell rectangle (four lanes in parallel)
         // one convergent call: lane 0/1 -> x bounds, lane 2/3 -> y bounds
         const bool ax = lane < 2;
@@ -245,31 +248,58 @@ k_gather(GatherParams p) {
         if (n_runs == 0) break;
         const int total = S.run_beg[n_runs];
 
-        // ---- A: bin of every staged candidate + histogram ----
-        for (int rs = warp; rs < n_runs; rs += kNW) {
-            const int gs = S.run_g[rs], rb = S.run_beg[rs], len = S.run_beg[rs + 1] - rb;
-            for (int j = lane; j < len; j += 32) {
-                const int slot = gs + j;
-                const float4 ra = p.rec[(base + slot) * 2];
-                const float mx = ra.x, my = ra.y;
-                const bool flag = (__float_as_uint(p.rec[(base + slot) * 2 + 1].z) & kUnsafeBit) != 0;
-                int key = -1;
-                const double dx = static_cast<double>(mx) - cxo;
-                const double dy = static_cast<double>(my) - cyo;
-                if (!flag) {
-                    if (dx >= 0.0 && dy >= 0.0) {
-                        const double qf = floor(dx), yf = floor(dy * 0.5);
-                        if (qf < ncol && yf < nyb)
-                            key = static_cast<int>(qf) * nyb + static_cast<int>(yf);
-                    }
-                } else if (static_cast<double>(mx) >= xlo - 1.0 && static_cast<double>(mx) <= xhi + 1.0 &&
-                           static_cast<double>(my) >= ylo - 1.0 && static_cast<double>(my) <= yhi + 1.0) {
-                    key = nbins;  // the flag bin
-                }
-                if (key >= 0) atomicAdd(&S.bin[key], 1);
-                S.u.st.key[rb + j] = key;
-                S.u.st.slot[rb + j] = slot;
+        // ---- stage: one TMA bulk copy per run of consecutive records ----
+        if (warp == 0) {
+            if (lane == 0) {
+                // order the previous chunk's generic reads of R before the
+                // async-proxy writes, then announce the chunk's bytes
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                             ::"r"(mbar), "r"(static_cast<uint32_t>(total) * 32u) : "memory");
             }
+            __syncwarp();
+            if (lane < n_runs) {
+                const int rb = S.run_beg[lane], len = S.run_beg[lane + 1] - rb;
+                if (len > 0)
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                        ::"r"(smem_u32(&S.u.R[2 * rb])), "l"(p.rec + (base + S.run_g[lane]) * 2),
+                          "r"(static_cast<uint32_t>(len) * 32u), "r"(mbar)
+                        : "memory");
+            }
+        }
+        {
+            uint32_t ok = 0;
+            while (!ok) {
+                asm volatile(
+                    "{\n\t.reg .pred P1;\n\t"
+                    "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                    "selp.b32 %0, 1, 0, P1;\n\t}"
+                    : "=r"(ok) : "r"(mbar), "r"(phase) : "memory");
+            }
+            phase ^= 1u;
+        }
+
+        // ---- A: bin of every staged candidate + histogram ----
+        for (int k = tid; k < total; k += kNT) {
+            const float4 ra = S.u.R[2 * k];
+            const float mx = ra.x, my = ra.y;
+            const bool flag = (__float_as_uint(S.u.R[2 * k + 1].z) & kUnsafeBit) != 0;
+            int key = -1;
+            const double dx = static_cast<double>(mx) - cxo;
+            const double dy = static_cast<double>(my) - cyo;
+            if (!flag) {
+                if (dx >= 0.0 && dy >= 0.0) {
+                    const double qf = floor(dx), yf = floor(dy * 0.5);
+                    if (qf < ncol && yf < nyb)
+                        key = static_cast<int>(qf) * nyb + static_cast<int>(yf);
+                }
+            } else if (static_cast<double>(mx) >= xlo - 1.0 && static_cast<double>(mx) <= xhi + 1.0 &&
+                       static_cast<double>(my) >= ylo - 1.0 && static_cast<double>(my) <= yhi + 1.0) {
+                key = nbins;  // the flag bin
+            }
+            if (key >= 0) atomicAdd(&S.bin[key], 1);
+            S.key[k] = key;
         }
         __syncthreads();
 
@@ -308,22 +338,13 @@ k_gather(GatherParams p) {
         }
         __syncthreads();
 
-        // ---- C: scatter (ends -> starts by atomic decrement) ----
+        // ---- C: scatter into bin order, dense (ends -> starts by decrement) ----
         for (int k = tid; k < total; k += kNT) {
-            const int key = S.u.st.key[k];
+            const int key = S.key[k];
             if (key < 0) continue;
             const int pos = atomicSub(&S.bin[key], 1) - 1;
-            const int slot = S.u.st.slot[k];
-            float4 ra = p.rec[(base + slot) * 2];
-            float4 rb = p.rec[(base + slot) * 2 + 1];
-            if (kMulti) {
-                // C > 4: this group's channels from the bin-ordered colours
-                const float* cs = p.ccol + (base + slot) * p.C + ch0;
-                ra.z = cs[0];
-                ra.w = nch > 1 ? cs[1] : 0.f;
-                rb.x = nch > 2 ? cs[2] : 0.f;
-                rb.y = nch > 3 ? cs[3] : 0.f;
-            }
+            const float4 ra = S.u.R[2 * k];
+            const float4 rb = S.u.R[2 * k + 1];
             S.A[pos] = ra;
             if (CC > 2) S.Bc[pos] = f2(rb.x, rb.y);
             S.idx[pos] = static_cast<int>(__float_as_uint(rb.z) & 0x7fffffffu);
@@ -493,13 +514,12 @@ k_gather(GatherParams p) {
     for (int py = 0; py < 2; ++py) {
         const int qy = ya + py;
         const float2 wr = py ? Wb : Wa;
-        // both pixels inside and non-fallback, C == CC, 8-byte aligned: 64-bit
-        // stores of the pixel pair
+        // both pixels inside and non-fallback, 8-byte aligned: 64-bit stores
+        // of the pixel pair
         const size_t bpr = (static_cast<size_t>(b) * p.H + qy) * p.W + xa;
         const bool al = ((reinterpret_cast<uintptr_t>(p.image + bpr * CC) |
                           reinterpret_cast<uintptr_t>(p.wsum + bpr)) & 7) == 0;
-        if (qy < p.H && xa + 1 < p.W && wr.x > 0.f && wr.y > 0.f && nch == p.C && !kCount && al) {
-            const size_t bp = bpr;
+        if (qy < p.H && xa + 1 < p.W && wr.x > 0.f && wr.y > 0.f && !kCount && al) {
             const float ia = 1.0f / wr.x, ib = 1.0f / wr.y;
             float o[2 * CC];
 #pragma unroll
@@ -508,10 +528,10 @@ k_gather(GatherParams p) {
                 o[c] = norm(nm.x, wr.x, ia);
                 o[CC + c] = norm(nm.y, wr.y, ib);
             }
-            float2* out2 = reinterpret_cast<float2*>(p.image + bp * CC);
+            float2* out2 = reinterpret_cast<float2*>(p.image + bpr * CC);
 #pragma unroll
             for (int j = 0; j < CC; ++j) out2[j] = f2(o[2 * j], o[2 * j + 1]);
-            if (grp == 0) *reinterpret_cast<float2*>(p.wsum + bp) = wr;
+            *reinterpret_cast<float2*>(p.wsum + bpr) = wr;
             continue;
         }
 #pragma unroll
@@ -520,21 +540,17 @@ k_gather(GatherParams p) {
             if (qx >= p.W || qy >= p.H) continue;
             const float w = py ? (px ? Wb.y : Wb.x) : (px ? Wa.y : Wa.x);
             const size_t bp = (static_cast<size_t>(b) * p.H + qy) * p.W + qx;
-            float* out = p.image + bp * p.C + ch0;
+            float* out = p.image + bp * p.C;
             if (w > 0.f) {
                 const float inv = 1.0f / w;
 #pragma unroll
                 for (int c = 0; c < CC; ++c) {
-                    if (c >= nch) continue;
                     const float num = py ? (px ? Nb[c].y : Nb[c].x) : (px ? Na[c].y : Na[c].x);
-                    const float q0 = num * inv;
-                    out[c] = fmaf(fmaf(-q0, w, num), inv, q0);
+                    out[c] = norm(num, w, inv);
                 }
-                if (grp == 0) {
-                    p.wsum[bp] = w;
-                    if (kCount) p.counts[bp] = py ? (px ? cnt11 : cnt10) : (px ? cnt01 : cnt00);
-                }
-            } else if (grp == 0) {
+                p.wsum[bp] = w;
+                if (kCount) p.counts[bp] = py ? (px ? cnt11 : cnt10) : (px ? cnt01 : cnt00);
+            } else {
                 // empty neighbourhood: fallback pixel (K3)
                 p.wsum[bp] = 0.f;
                 if (kCount) p.counts[bp] = 0;
@@ -546,16 +562,16 @@ k_gather(GatherParams p) {
     }
 }
 
-template <int CC, bool kCount, bool kMulti = false>
+template <int CC, bool kCount>
 void launch_cc(gmi_ctx* ctx, const GatherParams& p, dim3 grid) {
     const int smem = static_cast<int>(sizeof(SmemGather<CC>));
     static int set_dev = -1;  // attribute set once per device
     if (set_dev != ctx->device) {
         set_dev = ctx->device;
-    GMI_CUDA(cudaFuncSetAttribute(k_gather<CC, kCount, kMulti>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        GMI_CUDA(cudaFuncSetAttribute(k_gather<CC, kCount>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      smem));
     }
-    k_gather<CC, kCount, kMulti><<<grid, kNT, smem, ctx->stream>>>(p);
+    k_gather<CC, kCount><<<grid, kNT, smem, ctx->stream>>>(p);
     GMI_LAUNCHED(ctx);
 }
 
@@ -587,6 +603,7 @@ bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* count
     if (!gather_fast_ok(c)) return false;
     // C > 4: the wide-channel gather (gmi_wide.cu) on index-ordered cells
     if (launch_gather_wide(ctx, c, image, counts)) return true;
+    if (c->C > 4) return false;
     const double r = c->cutoff;
     GatherParams p{};
     gather_geometry(r, p.rc, p.ncol, p.dyb, p.nyb);
@@ -598,7 +615,6 @@ bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* count
     p.geom = c->geom_d;
     p.bins = c->bins;
     p.rec = c->rec;
-    p.ccol = c->ccol;
     p.N = c->N;
     p.C = c->C;
     p.W = c->W;
@@ -616,18 +632,14 @@ bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* count
     p.special = c->special;
     p.special_count = c->special_count_d;
     p.special_cap = c->special_cap;
-    const int cc = c->C <= 4 ? c->C : 4;
-    const dim3 grid((c->W + kTW - 1) / kTW, (c->H + kTH - 1) / kTH, c->B * ((c->C + cc - 1) / cc));
+    const dim3 grid((c->W + kTW - 1) / kTW, (c->H + kTH - 1) / kTH, c->B);
     GMI_CUDA(cudaMemsetAsync(c->special_count_d, 0, sizeof(int32_t), ctx->stream));
     const bool cnt = counts != nullptr;
-    switch (cc) {
+    switch (c->C) {
         case 1: cnt ? launch_cc<1, true>(ctx, p, grid) : launch_cc<1, false>(ctx, p, grid); break;
         case 2: cnt ? launch_cc<2, true>(ctx, p, grid) : launch_cc<2, false>(ctx, p, grid); break;
         case 3: cnt ? launch_cc<3, true>(ctx, p, grid) : launch_cc<3, false>(ctx, p, grid); break;
-        default:
-            if (c->C > 4) cnt ? launch_cc<4, true, true>(ctx, p, grid) : launch_cc<4, false, true>(ctx, p, grid);
-            else cnt ? launch_cc<4, true>(ctx, p, grid) : launch_cc<4, false>(ctx, p, grid);
-            break;
+        default: cnt ? launch_cc<4, true>(ctx, p, grid) : launch_cc<4, false>(ctx, p, grid); break;
     }
     return true;
 }
