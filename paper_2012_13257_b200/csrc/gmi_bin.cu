@@ -162,7 +162,7 @@ __global__ void k_scan_segments(int32_t* __restrict__ tile_sum,
 
 __global__ void k_scan_apply(int32_t* __restrict__ data,
                              const ScanTile* __restrict__ tiles,
-                             const int32_t* __restrict__ tile_off) {
+                             const int32_t* __restrict__ tile_off, int inclusive) {
     __shared__ int buf[kScanTile];
     __shared__ int warp_tot[32];
     __shared__ int total;
@@ -181,8 +181,9 @@ __global__ void k_scan_apply(int32_t* __restrict__ data,
     int ex = block_exclusive_scan(s, warp_tot, &total) + tile_off[blockIdx.x];
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
-        buf[threadIdx.x * kPer + j] = ex;
+        if (!inclusive) buf[threadIdx.x * kPer + j] = ex;
         ex += v[j];
+        if (inclusive) buf[threadIdx.x * kPer + j] = ex;
     }
     __syncthreads();
     for (int k = threadIdx.x; k < t.len; k += blockDim.x) data[t.start + k] = buf[k];
@@ -434,17 +435,19 @@ __device__ __forceinline__ bool point_ambiguous_fast(float mx, float my, float r
     return amb;
 }
 
-// Hot layout straight from the atomic cell ranks (no within-cell ordering:
-// the fast gather canonicalises its own bins and the backward is
-// order-independent): thread per point (4 per thread for memory-level
-// parallelism), coalesced reads of the point, ONE 32-byte record written at
-// bin_start[cell] + rank — (x, y, c0, c1) (c2, c3, idx | ambiguity flag, 0) —
-// plus colour validation (core.cpp:80-92).
+// Hot layout straight from atomic slots (no within-cell ordering: the fast
+// gather canonicalises its own bins and the backward is order-independent):
+// thread per point (4 per thread for memory-level parallelism), coalesced
+// reads of the point, its cell recomputed (bit-identical to k_count_red) and
+// a slot taken by decrementing the cell's end (the inclusive scan), so the
+// ends become bin_start with no rank or cell-id arrays in between; ONE
+// 32-byte record written at the slot — (x, y, c0, c1) (c2, c3, idx |
+// ambiguity flag, 0) — plus colour validation (core.cpp:80-92).
 struct ScatterEmitParams {
     const float2* pos;
     const float* col;
     const Geom* geom;
-    const int32_t* bins;
+    int32_t* bins;          // k_scatter_emit: cell ends, decremented to starts
     const int32_t* cellid;
     const int32_t* rank;
     float4* rec;
@@ -460,7 +463,8 @@ constexpr int kEmitPer = 4;
 __global__ void __launch_bounds__(256) k_scatter_emit(ScatterEmitParams p) {
     const int b = blockIdx.y;
     const size_t base = static_cast<size_t>(b) * p.N;
-    const int64_t boff = p.geom[b].bin_off;
+    const Geom g = p.geom[b];
+    const double inv = 1.0 / g.cell;
     const int i0 = blockIdx.x * (blockDim.x * kEmitPer) + threadIdx.x;
     int dst[kEmitPer];
     float2 v[kEmitPer];
@@ -468,12 +472,20 @@ __global__ void __launch_bounds__(256) k_scatter_emit(ScatterEmitParams p) {
 #pragma unroll
     for (int u = 0; u < kEmitPer; ++u) {
         const int i = i0 + u * blockDim.x;
-        dst[u] = -1;
         if (i < p.N) {
-            dst[u] = p.bins[boff + p.cellid[base + i]] + p.rank[base + i];
             v[u] = p.pos[base + i];
 #pragma unroll
             for (int ch = 0; ch < 4; ++ch) c[u][ch] = ch < p.C ? p.col[(base + i) * p.C + ch] : 0.f;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kEmitPer; ++u) {
+        const int i = i0 + u * blockDim.x;
+        dst[u] = -1;
+        if (i < p.N) {
+            const int cx = cell_of_fast(static_cast<double>(v[u].x), g.ox, g.cell, inv, g.n_cols);
+            const int cy = cell_of_fast(static_cast<double>(v[u].y), g.oy, g.cell, inv, g.n_rows);
+            dst[u] = atomicSub(p.bins + g.bin_off + cy * g.n_cols + cx, 1) - 1;  // bin_grid.cpp:67
         }
     }
 #pragma unroll
@@ -652,6 +664,33 @@ __global__ void __launch_bounds__(512) k_sort_big_recs(int N, const Geom* __rest
     }
 }
 
+// Cell counts only (fire-and-forget reductions, no ranks stored): the fast
+// path's count pass; k_scatter_emit recomputes the cell and takes its slot.
+__global__ void __launch_bounds__(256) k_count_red(const float2* __restrict__ pos, int N,
+                                                   const Geom* __restrict__ geom,
+                                                   int32_t* __restrict__ bins) {
+    const int b = blockIdx.y;
+    const Geom g = geom[b];
+    const double inv = 1.0 / g.cell;
+    const size_t base = static_cast<size_t>(b) * N;
+    const int i0 = blockIdx.x * (blockDim.x * kEmitPer) + threadIdx.x;
+    float2 v[kEmitPer];
+#pragma unroll
+    for (int u = 0; u < kEmitPer; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < N) v[u] = pos[base + i];
+    }
+#pragma unroll
+    for (int u = 0; u < kEmitPer; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < N) {
+            const int cx = cell_of_fast(static_cast<double>(v[u].x), g.ox, g.cell, inv, g.n_cols);
+            const int cy = cell_of_fast(static_cast<double>(v[u].y), g.oy, g.cell, inv, g.n_rows);
+            atomicAdd(bins + g.bin_off + cy * g.n_cols + cx, 1);  // bin_grid.cpp:67
+        }
+    }
+}
+
 // k_count with 4 points per thread: 4 independent position loads and cell
 // atomics in flight per thread (the single-point kernel is latency bound).
 __global__ void __launch_bounds__(256) k_count4(const float2* __restrict__ pos, int N,
@@ -706,8 +745,10 @@ int host_axis_cells(double span, double cell, int cap) {
 // Scan tiles over segments [seg_start[b], seg_start[b] + seg_len[b]).
 // `equal`: all segments have the same length (device geometry); the tile
 // table then depends only on (B, stride) and is cached in the context.
+// inclusive: data[k] = sum of counts [0, k] (cell ends), else exclusive.
 static void scan_segments(gmi_ctx* ctx, int32_t* data, const std::vector<int64_t>& seg_start,
-                          const std::vector<int64_t>& seg_len, bool equal = false) {
+                          const std::vector<int64_t>& seg_len, bool equal = false,
+                          bool inclusive = false) {
     cudaStream_t st = ctx->stream;
     const int B = static_cast<int>(seg_start.size());
     if (equal && ctx->eq_B == B && ctx->eq_stride == seg_len[0]) {
@@ -719,7 +760,7 @@ static void scan_segments(gmi_ctx* ctx, int32_t* data, const std::vector<int64_t
         GMI_LAUNCHED(ctx);
         k_scan_segments<<<B, 1024, 0, st>>>(d_tsum, d_segoff);
         GMI_LAUNCHED(ctx);
-        k_scan_apply<<<nt, kScanThreads, 0, st>>>(data, d_tiles, d_tsum);
+        k_scan_apply<<<nt, kScanThreads, 0, st>>>(data, d_tiles, d_tsum, inclusive ? 1 : 0);
         GMI_LAUNCHED(ctx);
         return;
     }
@@ -750,7 +791,7 @@ static void scan_segments(gmi_ctx* ctx, int32_t* data, const std::vector<int64_t
     GMI_LAUNCHED(ctx);
     k_scan_segments<<<B, 1024, 0, st>>>(d_tsum, d_segoff);
     GMI_LAUNCHED(ctx);
-    k_scan_apply<<<nt, kScanThreads, 0, st>>>(data, d_tiles, d_tsum);
+    k_scan_apply<<<nt, kScanThreads, 0, st>>>(data, d_tiles, d_tsum, inclusive ? 1 : 0);
     GMI_LAUNCHED(ctx);
 }
 
@@ -840,25 +881,21 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
 
     // ---- count (atomic arrival rank in the cell) + segmented scan ----
     const size_t BN = static_cast<size_t>(B) * N;
-    int32_t* cellid = static_cast<int32_t*>(scratch(ctx, WS_CELLID, sizeof(int32_t) * BN));
-    int32_t* rank = static_cast<int32_t*>(scratch(ctx, WS_RANK, sizeof(int32_t) * BN));
     const dim3 pgrid((N + 255) / 256, B);
     const dim3 pgrid4((N + 256 * kEmitPer - 1) / (256 * kEmitPer), B);
-    k_count4<<<pgrid4, 256, 0, st>>>(p2, N, c->geom_d, c->bins, cellid, rank);
-    GMI_LAUNCHED(ctx);
-    host_trace("bin: count launched");
-    scan_segments(ctx, c->bins, seg_start, seg_len, c->geom_h.empty());
-
     const bool classify = c->wsum64 == nullptr;
     if (hot && !c->sort_cells) {
-        // fast path: 32-byte records at bin_start + arrival rank
+        // fast path: counts -> inclusive scan (cell ends) -> 32-byte records
+        // at slots taken from the ends, which leaves bin_start behind
+        k_count_red<<<pgrid4, 256, 0, st>>>(p2, N, c->geom_d, c->bins);
+        GMI_LAUNCHED(ctx);
+        host_trace("bin: count launched");
+        scan_segments(ctx, c->bins, seg_start, seg_len, c->geom_h.empty(), true);
         ScatterEmitParams e{};
         e.pos = p2;
         e.col = col;
         e.geom = c->geom_d;
         e.bins = c->bins;
-        e.cellid = cellid;
-        e.rank = rank;
         e.rec = c->rec;
         e.ccol = c->ccol;
         e.issue = d_issue;
@@ -890,7 +927,14 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
         return;
     }
 
-    // ---- scatter + per-cell index order (the reference's point_index) ----
+    // ---- count (atomic arrival rank) + scan + scatter + per-cell index order
+    // (the reference's point_index) ----
+    int32_t* cellid = static_cast<int32_t*>(scratch(ctx, WS_CELLID, sizeof(int32_t) * BN));
+    int32_t* rank = static_cast<int32_t*>(scratch(ctx, WS_RANK, sizeof(int32_t) * BN));
+    k_count4<<<pgrid4, 256, 0, st>>>(p2, N, c->geom_d, c->bins, cellid, rank);
+    GMI_LAUNCHED(ctx);
+    host_trace("bin: count launched");
+    scan_segments(ctx, c->bins, seg_start, seg_len, c->geom_h.empty());
     int32_t* tmp = static_cast<int32_t*>(scratch(ctx, WS_TMP, sizeof(int32_t) * BN));
     k_scatter<<<pgrid, 256, 0, st>>>(N, c->geom_d, c->bins, cellid, rank, tmp);
     GMI_LAUNCHED(ctx);
