@@ -427,21 +427,29 @@ def main():
                                                      hup.ctypes.data_as(fp), hdc.ctypes.data_as(fp),
                                                      hdp.ctypes.data_as(fp)))
             gmi.lib.gmi_cache_free(h)
+            # a user's step ends when its host outputs are complete (the
+            # asynchronous calls overlap the backward's upload with the
+            # forward's download inside the step)
+            ctx.synchronize()
 
         # W untimed warm-up steps here too: the first host-buffer steps grow
         # the stream-ordered memory pool (pinned staging of ~2.3 GB per step)
+        diag = os.environ.get("GMI_E2E_DIAG") is not None
         for _ in range(max(2, args.warmup)):
+            t0 = time.perf_counter()
             e2e_step()
+            if diag:
+                print(f"e2e warm-up step {1e3 * (time.perf_counter() - t0):.1f} ms", file=sys.stderr)
         barrier()
         torch.cuda.synchronize(dev)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
             e2e_step()
-        # the host calls return with their downloads queued (asynchronous
-        # mode): the end event waits for them on the device
-        ctx.join_host_copies()
+            if diag:
+                print(f"e2e timed step {1e3 * (time.perf_counter() - t0):.1f} ms", file=sys.stderr)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         e2e_ms = e0.elapsed_time(e1) / args.e2e_steps

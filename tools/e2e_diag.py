@@ -6,8 +6,8 @@ sys.path.insert(0, os.getcwd())
 import torch
 import paper_2012_13257_b200 as gmi
 B, N, C, W, H, sigma, cutoff = 64, 262144, 3, 1024, 1024, 1.5, 4.5
-if len(sys.argv) > 1:
-    B = int(sys.argv[1])
+if len(sys.argv) > 1 and sys.argv[1] == "4":  # BASELINE configs[3]
+    B, N, C, W, H, sigma, cutoff = 1, 16777216, 3, 8192, 8192, 1.0, 3.0
 dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev); g.manual_seed(1)
 pos = torch.empty(B, N, 2, device=dev)
