@@ -356,3 +356,17 @@ def test_gmm_benchmark_invalid_factor(gmi, ctx):
     with pytest.raises(gmi.GmiError) as e:
         gmi.gmm_benchmark(np.zeros((8, 8, 1), np.float32), 0, ctx=ctx)
     assert e.value.code == 9
+
+
+def test_async_host_api_defers_validation_errors(gmi, orc):
+    # GMI_CTX_ASYNC_ERRORS: a host-buffer forward returns at once and the
+    # reference's NonFiniteValue surfaces at gmi_ctx_synchronize
+    pos, col, _ = orc.synth_batch(23, 2, 500, 3, 40, 30)
+    pos[1, 77, 0] = np.nan
+    actx = gmi.Context(0)
+    actx.set_flags(1)
+    _, cache = gmi.forward_batch(pos, col, 40, 30, 1.0, 3.0, ctx=actx)
+    with pytest.raises(gmi.GmiError) as e:
+        actx.synchronize()
+    assert e.value.code == 1 and "77" in str(e.value)
+    del cache
