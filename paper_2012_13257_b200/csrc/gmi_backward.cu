@@ -664,12 +664,7 @@ __global__ void k_merge_special(const double* __restrict__ acc, float* __restric
 template <int CG, int LPP>
 void launch_points_lpp(gmi_ctx* ctx, const BwdParams& p, int nblocks, int groups) {
     const int smem = kSmemBudget;
-    static int set_dev = -1;  // attribute set once per device
-    if (set_dev != ctx->device) {
-        set_dev = ctx->device;
-        GMI_CUDA(cudaFuncSetAttribute(k_backward_points<CG, LPP>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    }
+    GMI_SMEM_ONCE(ctx, (k_backward_points<CG, LPP>), smem);
     k_backward_points<CG, LPP><<<dim3(nblocks, groups), kThreads, smem, ctx->stream>>>(p);
     GMI_LAUNCHED(ctx);
 }

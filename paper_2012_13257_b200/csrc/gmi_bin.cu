@@ -915,12 +915,7 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
                                                                           d_bigcount);
         GMI_LAUNCHED(ctx);
         const int rsmem = kBigRecSmem * (2 * sizeof(float4) + sizeof(unsigned long long));
-        static int set_dev = -1;
-        if (set_dev != ctx->device) {
-            set_dev = ctx->device;
-            GMI_CUDA(cudaFuncSetAttribute(k_sort_big_recs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          rsmem));
-        }
+        GMI_SMEM_ONCE(ctx, k_sort_big_recs, rsmem);
         k_sort_big_recs<<<ctx->num_sms, 512, rsmem, st>>>(N, c->geom_d, c->bins, c->rec, d_big, d_bigcount);
         GMI_LAUNCHED(ctx);
         host_trace("bin: scatter_emit launched");

@@ -565,12 +565,7 @@ k_gather(GatherParams p) {
 template <int CC, bool kCount>
 void launch_cc(gmi_ctx* ctx, const GatherParams& p, dim3 grid) {
     const int smem = static_cast<int>(sizeof(SmemGather<CC>));
-    static int set_dev = -1;  // attribute set once per device
-    if (set_dev != ctx->device) {
-        set_dev = ctx->device;
-        GMI_CUDA(cudaFuncSetAttribute(k_gather<CC, kCount>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      smem));
-    }
+    GMI_SMEM_ONCE(ctx, (k_gather<CC, kCount>), smem);
     k_gather<CC, kCount><<<grid, kNT, smem, ctx->stream>>>(p);
     GMI_LAUNCHED(ctx);
 }

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -24,6 +25,19 @@ struct GmiFail {
             throw GmiFail{e_ == cudaErrorMemoryAllocation ? GMI_ERR_OUT_OF_MEMORY \
                                                           : GMI_ERR_CUDA, \
                           std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+        }                                                                 \
+    } while (0)
+
+// Raises a kernel's dynamic shared-memory limit once per device (a per-call-
+// site bitmask of devices; thread-safe for one host thread per GPU).
+#define GMI_SMEM_ONCE(ctx, kernel, bytes)                                 \
+    do {                                                                  \
+        static std::atomic<uint64_t> done_{0};                            \
+        const uint64_t bit_ = 1ull << ((ctx)->device & 63);              \
+        if (!(done_.load(std::memory_order_acquire) & bit_)) {            \
+            GMI_CUDA(cudaFuncSetAttribute(kernel,                         \
+                cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));     \
+            done_.fetch_or(bit_, std::memory_order_release);              \
         }                                                                 \
     } while (0)
 

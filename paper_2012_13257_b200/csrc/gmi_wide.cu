@@ -393,12 +393,7 @@ __global__ void k_wide_tile_load(const Geom* __restrict__ geom, const int32_t* _
 template <int CB, bool kCount>
 void launch_wide_cb(gmi_ctx* ctx, const GatherWideParams& p, dim3 grid) {
     const int smem = static_cast<int>(sizeof(SmemWide<CB>));
-    static int set_dev = -1;  // attribute set once per device
-    if (set_dev != ctx->device) {
-        set_dev = ctx->device;
-        GMI_CUDA(cudaFuncSetAttribute(k_gather_wide<CB, kCount>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    }
+    GMI_SMEM_ONCE(ctx, (k_gather_wide<CB, kCount>), smem);
     k_gather_wide<CB, kCount><<<grid, kWThreads, smem, ctx->stream>>>(p);
     GMI_LAUNCHED(ctx);
 }
@@ -974,12 +969,7 @@ bool launch_backward_wide(gmi_ctx* ctx, const gmi_cache* c, const float* upstrea
     float* part = static_cast<float*>(scratch(ctx, WS_PART, sizeof(float) * n2 * groups));
     p.d_pos = groups > 1 ? part : d_positions;
     if (off[c->B] > 0) {
-        static int set_dev = -1;
-        if (set_dev != ctx->device) {
-            set_dev = ctx->device;
-            GMI_CUDA(cudaFuncSetAttribute(k_backward_wide, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          kBSmem));
-        }
+        GMI_SMEM_ONCE(ctx, k_backward_wide, kBSmem);
         const int nunits = off[c->B];
         p.heavy_cap = std::min(2048, nunits);
         char* ws = static_cast<char*>(scratch(ctx, WS_TMP, sizeof(int32_t) * (1 + p.heavy_cap) + nunits));
