@@ -45,6 +45,11 @@ typedef enum gmi_status {
     GMI_ERR_CACHE_MISMATCH = 7,
     GMI_ERR_INVALID_DIMENSIONS = 8,
     GMI_ERR_INVALID_FACTOR = 9,
+    GMI_ERR_INVALID_COUNT = 10,
+    GMI_ERR_UNSUPPORTED_FORMAT = 11,
+    GMI_ERR_CORRUPT_FILE = 12,
+    GMI_ERR_EMPTY_LOG = 13,
+    GMI_ERR_IO_ERROR = 14,
     /* B200-side failures (no reference equivalent) */
     GMI_ERR_CUDA = 100,
     GMI_ERR_INVALID_ARGUMENT = 101,

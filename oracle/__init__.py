@@ -129,6 +129,42 @@ class Reference:
                                             C.byref(l1), C.byref(su), C.byref(ms)))
         return l1.value, su.value, ms.value
 
+    # ---- files (imaging.cpp:235-304, 433-494) ----
+    def save_point_set(self, pos, col, path):
+        pos, col = _d(pos), _d(col)
+        L = self.lib
+        L.ref_save_point_set.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_char_p]
+        self._check(L.ref_save_point_set(_ptr(pos, _dp), _ptr(col, _dp), col.shape[0], col.shape[1],
+                                         path.encode()))
+
+    def load_point_set(self, path, cap=1 << 20):
+        L = self.lib
+        L.ref_load_point_set.argtypes = [C.c_char_p, C.c_int, _ip, _ip, _dp, _dp]
+        n, ch = C.c_int(), C.c_int()
+        pos = np.zeros((cap, 2))
+        col = np.zeros(cap * 3)
+        self._check(L.ref_load_point_set(path.encode(), cap, C.byref(n), C.byref(ch), _ptr(pos, _dp),
+                                         _ptr(col, _dp)))
+        return pos[:n.value].copy(), col[:n.value * ch.value].reshape(n.value, ch.value).copy()
+
+    def save_image(self, img, path):
+        img = _d(img)
+        if img.ndim == 2:
+            img = img[:, :, None]
+        L = self.lib
+        L.ref_save_image.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_char_p]
+        self._check(L.ref_save_image(_ptr(img, _dp), img.shape[0], img.shape[1], img.shape[2],
+                                     path.encode()))
+
+    def load_image(self, path, cap=1 << 24):
+        L = self.lib
+        L.ref_load_image.argtypes = [C.c_char_p, C.c_long, _ip, _ip, _ip, _dp]
+        h, w, ch = C.c_int(), C.c_int(), C.c_int()
+        out = np.zeros(cap)
+        self._check(L.ref_load_image(path.encode(), cap, C.byref(h), C.byref(w), C.byref(ch),
+                                     _ptr(out, _dp)))
+        return out[:h.value * w.value * ch.value].reshape(h.value, w.value, ch.value).copy()
+
     def block_mean_downsample(self, image, factor):
         """gmi::block_mean_downsample (imaging.cpp:343-350)."""
         img = np.ascontiguousarray(image, np.float64)

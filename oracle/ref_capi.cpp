@@ -340,4 +340,44 @@ int ref_block_mean_downsample(const double* image, int width, int height, int ch
     });
 }
 
+// Point-set and image files (imaging.cpp:235-304, 433-494).
+int ref_save_point_set(const double* pos, const double* col, int n, int channels, const char* path) {
+    return guarded([&] { gmi::save_point_set(make_points(pos, col, n, channels), path); });
+}
+
+// Loads into caller buffers of capacity cap points (n/channels always set).
+int ref_load_point_set(const char* path, int cap, int* n, int* channels, double* pos, double* col) {
+    return guarded([&] {
+        const gmi::PointSet ps = gmi::load_point_set(path);
+        *n = ps.size();
+        *channels = ps.channels;
+        if (ps.size() <= cap) {
+            for (int i = 0; i < ps.size(); ++i) {
+                pos[2 * i] = ps.positions[i].x;
+                pos[2 * i + 1] = ps.positions[i].y;
+            }
+            std::memcpy(col, ps.colors.data(), sizeof(double) * ps.colors.size());
+        }
+    });
+}
+
+int ref_save_image(const double* img, int height, int width, int channels, const char* path) {
+    return guarded([&] {
+        gmi::ImageBuffer b = gmi::ImageBuffer::zeros(height, width, channels);
+        b.data.assign(img, img + static_cast<std::size_t>(height) * width * channels);
+        gmi::save_image(b, path);
+    });
+}
+
+int ref_load_image(const char* path, long cap, int* height, int* width, int* channels, double* out) {
+    return guarded([&] {
+        const gmi::ImageBuffer b = gmi::load_image(path);
+        *height = b.height;
+        *width = b.width;
+        *channels = b.channels;
+        if (static_cast<long>(b.data.size()) <= cap)
+            std::memcpy(out, b.data.data(), sizeof(double) * b.data.size());
+    });
+}
+
 }  // extern "C"

@@ -39,6 +39,7 @@ __all__ = [
     "ForwardCache", "GmiError", "PointSet", "backward", "forward", "gaussian_weight",
     "forward_batch", "backward_batch", "Context", "bin_grid", "forward_counts",
     "default_context", "optimize_points", "gmm_benchmark", "ERROR_NAMES", "__version__",
+    "load_point_set", "save_point_set", "load_image", "save_image",
 ]
 
 __version__ = "0.1.0"
@@ -46,7 +47,8 @@ __version__ = "0.1.0"
 # gmi::ErrorCode names (core.hpp:35-50), index = code - 1
 ERROR_NAMES = ["NonFiniteValue", "ColorOutOfRange", "EmptyPointSet", "ShapeMismatch",
                "InvalidCellSize", "ConfigInvalid", "CacheMismatch", "InvalidDimensions",
-               "InvalidFactor"]
+               "InvalidFactor", "InvalidCount", "UnsupportedFormat", "CorruptFile", "EmptyLog",
+               "IoError"]
 
 
 class GmiError(RuntimeError):
@@ -527,3 +529,6 @@ def bin_grid(positions, cell_size: float, ctx: Context | None = None):
                         bin_start=bin_start[off:off + nb], point_index=point_index[k]))
         off += nb
     return out[0] if single else out
+
+
+from .formats import load_image, load_point_set, save_image, save_point_set  # noqa: E402

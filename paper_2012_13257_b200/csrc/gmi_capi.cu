@@ -495,6 +495,11 @@ const char* gmi_error_name(int code) {
         case GMI_ERR_CACHE_MISMATCH: return "CacheMismatch";
         case GMI_ERR_INVALID_DIMENSIONS: return "InvalidDimensions";
         case GMI_ERR_INVALID_FACTOR: return "InvalidFactor";
+        case GMI_ERR_INVALID_COUNT: return "InvalidCount";
+        case GMI_ERR_UNSUPPORTED_FORMAT: return "UnsupportedFormat";
+        case GMI_ERR_CORRUPT_FILE: return "CorruptFile";
+        case GMI_ERR_EMPTY_LOG: return "EmptyLog";
+        case GMI_ERR_IO_ERROR: return "IoError";
         case GMI_ERR_CUDA: return "CudaError";
         case GMI_ERR_INVALID_ARGUMENT: return "InvalidArgument";
         case GMI_ERR_OUT_OF_MEMORY: return "OutOfMemory";
