@@ -219,6 +219,14 @@ int gmi_optimize_points_host(gmi_ctx* ctx, float* positions, float* colors, int3
                              const float* target, int32_t steps, double learning_rate,
                              uint32_t flags, double* loss_curve);
 
+/* ---- device memory for callers without a framework (the zero-copy Python
+ * path): cudaMalloc / cudaFree on the ctx's device, and a copy
+ * ordered on the ctx stream (kind: 0 host->device, 1 device->host,
+ * 2 device->device; host memory may be pageable; returns after the copy). */
+int gmi_device_alloc(gmi_ctx* ctx, size_t bytes, void** out);
+int gmi_device_free(gmi_ctx* ctx, void* ptr);
+int gmi_memcpy(gmi_ctx* ctx, void* dst, const void* src, size_t bytes, int32_t kind);
+
 /* ---- run_benchmark's GMM branch (benchmark.cpp:88-107) for one image ------
  * image: HOST H x W x C.  Known points at the block centres of `lowres`
  * (HOST lh x lw x C, lh = ceil(H/factor), lw = ceil(W/factor);

@@ -40,6 +40,7 @@ __all__ = [
     "forward_batch", "backward_batch", "Context", "bin_grid", "forward_counts",
     "default_context", "optimize_points", "gmm_benchmark", "ERROR_NAMES", "__version__",
     "load_point_set", "save_point_set", "load_image", "save_image",
+    "DeviceArray", "forward_cuda", "backward_cuda",
 ]
 
 __version__ = "0.1.0"
@@ -532,3 +533,4 @@ def bin_grid(positions, cell_size: float, ctx: Context | None = None):
 
 
 from .formats import load_image, load_point_set, save_image, save_point_set  # noqa: E402
+from .device import DeviceArray, backward_cuda, forward_cuda  # noqa: E402

@@ -71,6 +71,9 @@ SIGNATURES = {
     "gmi_optimize_points_host": (C.c_int, [_vp, _fp, _fp, C.c_int32, C.c_int32, C.c_int32,
                                            C.POINTER(GmiConfig), _fp, C.c_int32, C.c_double,
                                            C.c_uint32, _dp]),
+    "gmi_device_alloc": (C.c_int, [_vp, C.c_size_t, C.POINTER(_vp)]),
+    "gmi_device_free": (C.c_int, [_vp, _vp]),
+    "gmi_memcpy": (C.c_int, [_vp, _vp, _vp, C.c_size_t, C.c_int32]),
     "gmi_gmm_benchmark_host": (C.c_int, [_vp, _fp, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                          _fp, _dp, C.c_int32, _dp, _dp, C.POINTER(C.c_int32),
                                          _fp]),

@@ -1087,6 +1087,41 @@ int gmi_optimize_points(gmi_ctx* ctx, float* positions, float* colors, int32_t b
     });
 }
 
+int gmi_device_alloc(gmi_ctx* ctx, size_t bytes, void** out) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr || out == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "null argument");
+        GMI_CUDA(cudaSetDevice(ctx->device));
+        *out = nullptr;
+        GMI_CUDA(cudaMalloc(out, std::max<size_t>(bytes, 16)));
+        return GMI_OK;
+    });
+}
+
+int gmi_device_free(gmi_ctx* ctx, void* ptr) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr) return fail(GMI_ERR_INVALID_ARGUMENT, "ctx is null");
+        if (ptr == nullptr) return GMI_OK;
+        GMI_CUDA(cudaSetDevice(ctx->device));
+        GMI_CUDA(cudaStreamSynchronize(ctx->stream));  // queued work may still use it
+        GMI_CUDA(cudaFree(ptr));
+        return GMI_OK;
+    });
+}
+
+int gmi_memcpy(gmi_ctx* ctx, void* dst, const void* src, size_t bytes, int32_t kind) {
+    return guarded([&]() -> int {
+        if (ctx == nullptr || (bytes > 0 && (dst == nullptr || src == nullptr)))
+            return fail(GMI_ERR_INVALID_ARGUMENT, "null argument");
+        if (kind < 0 || kind > 2) return fail(GMI_ERR_INVALID_ARGUMENT, "kind must be 0, 1 or 2");
+        GMI_CUDA(cudaSetDevice(ctx->device));
+        const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
+                                           : (kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice);
+        GMI_CUDA(cudaMemcpyAsync(dst, src, bytes, k, ctx->stream));
+        GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+        return GMI_OK;
+    });
+}
+
 int gmi_gmm_benchmark_host(gmi_ctx* ctx, const float* image, int32_t width, int32_t height,
                            int32_t channels, int32_t factor, const float* lowres,
                            const double* sigmas, int32_t n_sigma, double* l1, double* ms,
