@@ -665,22 +665,28 @@ k_backward_wide(BwdWideParams p) {
             const float mx = ra.x, my = ra.y;
             const int i = static_cast<int>(raw & 0x7fffffffu);
             const bool unsafe = (raw & kUnsafeBit) != 0;
-            float cc[kBG];
+            // channel pairs in f32x2: the 32 FMAs per pixel as 16 FFMA2 (half
+            // the issue slots, the same per-channel operations)
+            float2 cc2[kBG / 2];
             if (cfull) {
                 const float4* c4 = reinterpret_cast<const float4*>(p.ccol + (base + s) * p.C + ch0);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const float4 t = c4[j];
-                    cc[4 * j] = t.x; cc[4 * j + 1] = t.y; cc[4 * j + 2] = t.z; cc[4 * j + 3] = t.w;
+                    cc2[2 * j] = f2(t.x, t.y);
+                    cc2[2 * j + 1] = f2(t.z, t.w);
                 }
             } else {
 #pragma unroll
-                for (int c = 0; c < kBG; ++c)
-                    cc[c] = ch0 + c < p.C ? p.ccol[(base + s) * p.C + ch0 + c] : 0.f;
+                for (int k = 0; k < kBG / 2; ++k) {
+                    const int c = ch0 + 2 * k;
+                    cc2[k] = f2(c < p.C ? p.ccol[(base + s) * p.C + c] : 0.f,
+                                c + 1 < p.C ? p.ccol[(base + s) * p.C + c + 1] : 0.f);
+                }
             }
-            float dcol[kBG];
+            float2 dc2[kBG / 2];
 #pragma unroll
-            for (int c = 0; c < kBG; ++c) dcol[c] = 0.f;
+            for (int k = 0; k < kBG / 2; ++k) dc2[k] = f2(0.f, 0.f);
             float gx = 0.f, gy = 0.f;
             const float tx = truncf(mx);
             const float fmu = mx - tx;  // exact
@@ -735,21 +741,26 @@ k_backward_wide(BwdWideParams p) {
                         const float4 u0 = s_u4[q], u1 = s_u4[kPlanePx + q];
                         const float4 u2 = s_u4[2 * kPlanePx + q], u3 = s_u4[3 * kPlanePx + q];
                         const float v = s_v[q];
-                        const float u[kBG] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w,
-                                              u2.x, u2.y, u2.z, u2.w, u3.x, u3.y, u3.z, u3.w};
+                        const float2 uu[kBG / 2] = {f2(u0.x, u0.y), f2(u0.z, u0.w), f2(u1.x, u1.y),
+                                                    f2(u1.z, u1.w), f2(u2.x, u2.y), f2(u2.z, u2.w),
+                                                    f2(u3.x, u3.y), f2(u3.z, u3.w)};
                         const float dx = xf - mx;
                         const float w = ex2(fmaf(dx * nk, dx, ey));
-                        // t = sum_c c_ic u_c - v  (= dot / W, engine.cpp:219-221)
-                        // four partial sums: short dependency chains
-                        float t4[4] = {-v, 0.f, 0.f, 0.f};
+                        // t = sum_c c_ic u_c - v  (= dot / W, engine.cpp:219-221):
+                        // four partial sums (chains c mod 4) as two f32x2
+                        float2 ta = f2(-v, 0.f), tb = f2(0.f, 0.f);
 #pragma unroll
-                        for (int c = 0; c < kBG; ++c) t4[c & 3] = fmaf(u[c], cc[c], t4[c & 3]);
-                        const float t = (t4[0] + t4[1]) + (t4[2] + t4[3]);
+                        for (int k = 0; k < kBG / 2; k += 2) {
+                            ta = __ffma2_rn(uu[k], cc2[k], ta);
+                            tb = __ffma2_rn(uu[k + 1], cc2[k + 1], tb);
+                        }
+                        const float t = (ta.x + ta.y) + (tb.x + tb.y);
                         const float a = w * t;
                         gx = fmaf(a, dx, gx);
                         gy = fmaf(a, dy, gy);
+                        const float2 w2 = f2(w, w);
 #pragma unroll
-                        for (int c = 0; c < kBG; ++c) dcol[c] = fmaf(w, u[c], dcol[c]);
+                        for (int k = 0; k < kBG / 2; ++k) dc2[k] = __ffma2_rn(w2, uu[k], dc2[k]);
                     }
                 } else {
                     for (int x = x0l; x <= xr; x += 8, xf += 8.f) {
@@ -758,18 +769,28 @@ k_backward_wide(BwdWideParams p) {
                         const float v = pixel_uv(w0, u, im);
                         const float dx = xf - mx;
                         const float w = ex2(fmaf(dx * nk, dx, ey));
-                        // four partial sums: short dependency chains
-                        float t4[4] = {-v, 0.f, 0.f, 0.f};
+                        float2 ta = f2(-v, 0.f), tb = f2(0.f, 0.f);
 #pragma unroll
-                        for (int c = 0; c < kBG; ++c) t4[c & 3] = fmaf(u[c], cc[c], t4[c & 3]);
-                        const float t = (t4[0] + t4[1]) + (t4[2] + t4[3]);
+                        for (int k = 0; k < kBG / 2; k += 2) {
+                            ta = __ffma2_rn(f2(u[2 * k], u[2 * k + 1]), cc2[k], ta);
+                            tb = __ffma2_rn(f2(u[2 * k + 2], u[2 * k + 3]), cc2[k + 1], tb);
+                        }
+                        const float t = (ta.x + ta.y) + (tb.x + tb.y);
                         const float a = w * t;
                         gx = fmaf(a, dx, gx);
                         gy = fmaf(a, dy, gy);
+                        const float2 w2 = f2(w, w);
 #pragma unroll
-                        for (int c = 0; c < kBG; ++c) dcol[c] = fmaf(w, u[c], dcol[c]);
+                        for (int k = 0; k < kBG / 2; ++k)
+                            dc2[k] = __ffma2_rn(w2, f2(u[2 * k], u[2 * k + 1]), dc2[k]);
                     }
                 }
+            }
+            float dcol[kBG];
+#pragma unroll
+            for (int k = 0; k < kBG / 2; ++k) {
+                dcol[2 * k] = dc2[k].x;
+                dcol[2 * k + 1] = dc2[k].y;
             }
             // ---- warp sums: the 4 squads, then a reduce-scatter of d_col
             // inside the squad (lane sl keeps channels 2 sl, 2 sl + 1) ----
