@@ -251,6 +251,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gmi", choices=["gmi", "reference"])
     ap.add_argument("--batch", type=int, default=None)
+    ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
+                    help="replay each timed step as one captured CUDA graph (auto: every "
+                         "config but the multi-GPU row bands, whose step holds a collective)")
     ap.add_argument("--config", type=int, default=3, choices=sorted(CONFIGS),
                     help="BASELINE.json config (1-based); 3 is the headline")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -354,8 +357,47 @@ def main():
             dist.barrier()
 
     # ---- device-resident timed region ----
-    ctx.set_profiling(True)
-    ctx.phase_times(reset=True)
+    # Each timed step replays ONE captured CUDA graph of the whole step
+    # (binning, gather, special pixels, backward and the cache's stream-
+    # ordered allocations and frees): no host launch gaps between kernels.
+    # Per-phase times come from an eager profiled pass (events cannot sit in
+    # the graph); if capture is unavailable the steps run eagerly.
+    def capture_step():
+        ctx.set_profiling(True)
+        ctx.phase_times(reset=True)
+        for _ in range(args.warmup):
+            c = step()
+            del c
+        ctx.synchronize()
+        pm, pc = ctx.phase_times(reset=True)
+        ctx.set_profiling(False)
+        torch.cuda.synchronize(dev)
+        n0 = ctx.launch_count
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            c = step()
+            del c
+        n = ctx.launch_count - n0
+        with torch.cuda.stream(stream):  # replay() launches on the current stream
+            for _ in range(2):
+                g.replay()
+        torch.cuda.synchronize(dev)
+        return g, n, pm, pc
+
+    use_graph = args.graph == "on" or (args.graph == "auto" and not band)
+    graph, graph_note = None, None
+    if use_graph:
+        warm.clear()
+        try:
+            graph, per_step_launches, phase_ms, phase_calls = capture_step()
+        except Exception as exc:
+            graph = None
+            graph_note = f"graph capture failed ({type(exc).__name__}): eager steps"
+            ctx.set_profiling(False)
+            torch.cuda.synchronize(dev)
+    if graph is None:
+        ctx.set_profiling(True)
+        ctx.phase_times(reset=True)
     barrier()
     torch.cuda.synchronize(dev)
     launches0 = ctx.launch_count
@@ -365,6 +407,10 @@ def main():
     with ClockSampler(local) as clocks:
         ev0.record(stream)
         for _ in range(args.steps):
+            if graph is not None:
+                with torch.cuda.stream(stream):  # replay() launches on the current stream
+                    graph.replay()
+                continue
             caches.append(step())
             if len(caches) > 2:
                 caches.pop(0)
@@ -372,10 +418,12 @@ def main():
         torch.cuda.synchronize(dev)
     ms = ev0.elapsed_time(ev1)
     barrier()
-    launches = ctx.launch_count - launches0
+    launches = (per_step_launches * args.steps if graph is not None
+                else ctx.launch_count - launches0)
     ctx.synchronize()  # raises on any pending validation error
-    phase_ms, phase_calls = ctx.phase_times(reset=True)
-    ctx.set_profiling(False)
+    if graph is None:
+        phase_ms, phase_calls = ctx.phase_times(reset=True)
+        ctx.set_profiling(False)
     caches.clear()
     if world > 1:
         import torch.distributed as dist
@@ -500,6 +548,7 @@ def main():
                               "frac": round(max(h2d, d2h) / (pcie * 1e9) * 1e3 / e2e_ms, 4)}}
                 if e2e_ms else None),
         "gpu_launches": launches,
+        "cuda_graph": graph is not None if graph_note is None else graph_note,
         "clocks": clocks.summary(),
     }
     if not args.no_cpu_baseline and args.config == 3:

@@ -706,9 +706,7 @@ void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
         }
         off[b + 1] = off[b] + nb;
     }
-    int32_t* d_off = static_cast<int32_t*>(scratch(ctx, WS_BLKOFF, sizeof(int32_t) * (c->B + 1)));
-    GMI_CUDA(cudaMemcpyAsync(d_off, off.data(), sizeof(int32_t) * (c->B + 1),
-                             cudaMemcpyHostToDevice, st));
+    const int32_t* d_off = upload_table(ctx, WS_BLKOFF, off);
     BwdParams p{};
     p.geom = c->geom_d;
     p.bins = c->bins;

@@ -457,10 +457,22 @@ void dfree(gmi_ctx* ctx, void* p) {
     if (p) cudaFreeAsync(p, ctx->stream);
 }
 
+int32_t* upload_table(gmi_ctx* ctx, int slot, const std::vector<int32_t>& v) {
+    int32_t* d = static_cast<int32_t*>(scratch(ctx, slot, sizeof(int32_t) * v.size()));
+    if (ctx->ws_table_ptr[slot] != d || ctx->ws_table[slot] != v) {
+        GMI_CUDA(cudaMemcpyAsync(d, v.data(), sizeof(int32_t) * v.size(), cudaMemcpyHostToDevice,
+                                 ctx->stream));
+        ctx->ws_table[slot] = v;
+        ctx->ws_table_ptr[slot] = d;
+    }
+    return d;
+}
+
 void* scratch(gmi_ctx* ctx, int slot, size_t bytes) {
     bytes = std::max<size_t>(bytes, 256);
     if (ctx->ws_cap[slot] < bytes) {
         if (ctx->ws_ptr[slot]) cudaFreeAsync(ctx->ws_ptr[slot], ctx->stream);
+        ctx->ws_table_ptr[slot] = nullptr;  // an uploaded table must be re-sent
         const size_t cap = bytes + bytes / 4;  // headroom for slowly growing sizes
         GMI_CUDA(cudaMallocAsync(&ctx->ws_ptr[slot], cap, ctx->stream));
         ctx->ws_cap[slot] = cap;

@@ -75,6 +75,9 @@ struct gmi_ctx {
     // grow-only per-call scratch (stream-ordered reuse on the ctx stream)
     void* ws_ptr[16] = {nullptr};
     size_t ws_cap[16] = {0};
+    // host copies of small tables uploaded into scratch slots (upload_table)
+    std::vector<int32_t> ws_table[16];
+    void* ws_table_ptr[16] = {nullptr};
     // scan tiles of the equal-segment (device geometry) binning, cached per
     // (batch, stride) so the hot path issues no host->device copy
     int eq_B = -1;
@@ -187,6 +190,10 @@ void dfree(gmi_ctx* ctx, void* p);
 // ctx scratch slot of at least `bytes` (contents undefined)
 void* scratch(gmi_ctx* ctx, int slot, size_t bytes);
 void* cache_alloc(gmi_cache* c, size_t bytes);
+// Device copy of a small host table in a ctx scratch slot, uploaded only
+// when its contents (or the slot's buffer) change: repeated calls issue no
+// host->device copy, so the hot path stays capturable in a CUDA graph.
+int32_t* upload_table(gmi_ctx* ctx, int slot, const std::vector<int32_t>& v);
 
 // ---- binning (gmi_bin.cu) ----
 // Validates positions, computes bbox, geometry (cap) and fills c->geom_*,

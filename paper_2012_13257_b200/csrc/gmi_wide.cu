@@ -962,9 +962,7 @@ bool launch_backward_wide(gmi_ctx* ctx, const gmi_cache* c, const float* upstrea
         const int ncols = c->geom_h.empty() ? c->grid_cap : c->geom_h[b].n_cols;
         off[b + 1] = off[b] + ncols * nseg_cap;
     }
-    int32_t* d_off = static_cast<int32_t*>(scratch(ctx, WS_BLKOFF, sizeof(int32_t) * (c->B + 1)));
-    GMI_CUDA(cudaMemcpyAsync(d_off, off.data(), sizeof(int32_t) * (c->B + 1),
-                             cudaMemcpyHostToDevice, st));
+    const int32_t* d_off = upload_table(ctx, WS_BLKOFF, off);
     BwdWideParams p{};
     p.geom = c->geom_d;
     p.bins = c->bins;

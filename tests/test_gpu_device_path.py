@@ -59,3 +59,43 @@ def test_device_path_validation(gmi, ctx):
         gmi.forward_cuda(torch.zeros(1, 4, 2, device="cuda"), torch.zeros(1, 5, 1, device="cuda"),
                          8, 8, 1.0, ctx=ctx)
     assert e.value.code == 4
+
+
+def test_cuda_graph_capture_replays_the_step(gmi, orc):
+    # a whole forward + backward (binning, gather, special pixels, backward,
+    # the cache's stream-ordered allocations and frees) captured once as a
+    # CUDA graph and replayed gives the eager results bit for bit
+    torch = pytest.importorskip("torch")
+    pos, col, up = orc.synth_batch(43, 2, 3000, 3, 80, 60)
+    dev = torch.device("cuda", 0)
+    s = torch.cuda.Stream(dev)
+    tpos, tcol, tup = (torch.from_numpy(a).to(dev) for a in (pos, col, up))
+    img = torch.empty(2, 60, 80, 3, device=dev)
+    dc = torch.empty(2, 3000, 3, device=dev)
+    dp = torch.empty(2, 3000, 2, device=dev)
+    gctx = gmi.Context(0)
+    gctx.set_stream(s.cuda_stream)
+    gctx.set_flags(1)
+    torch.cuda.synchronize()
+
+    def step():
+        cache = gctx.forward_device(tpos, tcol, 2, 3000, 3, 80, 60, 1.0, 3.0, 0, img)
+        gctx.backward_device(tpos, tcol, 2, 3000, 3, 80, 60, 1.0, 3.0, 0, cache, tup, dc, dp)
+        del cache
+
+    for _ in range(3):
+        step()
+    gctx.synchronize()
+    want = (img.cpu().numpy(), dc.cpu().numpy(), dp.cpu().numpy())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        step()
+    for t in (img, dc, dp):
+        t.zero_()
+    with torch.cuda.stream(s):
+        g.replay()
+        g.replay()
+    torch.cuda.synchronize()
+    gctx.synchronize()
+    assert np.array_equal(img.cpu().numpy(), want[0])
+    assert np.array_equal(dc.cpu().numpy(), want[1]) and np.array_equal(dp.cpu().numpy(), want[2])
