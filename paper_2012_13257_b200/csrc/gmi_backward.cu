@@ -611,55 +611,67 @@ struct SpecBwdParams {
 };
 
 // engine.cpp:200-211: fallback pixels route their upstream to the nearest
-// point's colour only (no position gradient).
-__global__ void k_special_backward(SpecBwdParams p) {
+// point's colour only (no position gradient).  Sparse inputs route hundreds
+// of O(1) upstream values into one point, so the sum is formed in f64 and
+// added to the point's fp32 d_col with ONE rounding (fp32 atomics would carry
+// their rounding — and their nondeterministic order — into a cancellation of
+// ~1e-2).  Three passes with fixed grids that read the special count on the
+// device (no host round trip, capturable in a CUDA graph), touching only the
+// routed points: zero their f64 slots and owner marks, accumulate, then the
+// entry that won the owner mark (the largest list position, unique whatever
+// the arrival order) adds the point's sum once.  f64 sums of fp32 upstream
+// values are exact in practice, so the result does not depend on the order.
+__device__ __forceinline__ bool special_route(const SpecBwdParams& p, int si, size_t& pixb,
+                                              size_t& pt) {
+    const Special sp = p.special[si];
+    if (sp.kind != 1 || sp.nearest < 0) return false;
+    pixb = static_cast<size_t>(sp.b) * p.H * p.W + sp.pix;
+    pt = static_cast<size_t>(sp.b) * p.N + sp.nearest;
+    return true;
+}
+
+__global__ void k_special_zero(SpecBwdParams p, double* __restrict__ acc, int* __restrict__ own) {
+    const int n = min(*p.special_count, p.special_cap);
+    for (int si = blockIdx.x * blockDim.x + threadIdx.x; si < n; si += gridDim.x * blockDim.x) {
+        size_t pixb, pt;
+        if (!special_route(p, si, pixb, pt)) continue;
+        own[pt] = -1;
+        for (int c = 0; c < p.C; ++c) acc[pt * p.C + c] = 0.0;
+    }
+}
+
+__global__ void k_special_accumulate(SpecBwdParams p, double* __restrict__ acc, int* __restrict__ own) {
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
     const int n = min(*p.special_count, p.special_cap);
-    if (p.fallback != GMI_FALLBACK_NEAREST) return;
     for (int si = warp; si < n; si += nwarps) {
-        const Special sp = p.special[si];
-        if (sp.kind != 1 || sp.nearest < 0) continue;
-        const size_t pixb = static_cast<size_t>(sp.b) * p.H * p.W + sp.pix;
-        const size_t base = static_cast<size_t>(sp.b) * p.N;
+        size_t pixb, pt;
+        if (!special_route(p, si, pixb, pt)) continue;
+        if (lane == 0) atomicMax(own + pt, si);
         for (int c = lane; c < p.C; c += 32)
-            atomicAdd(p.d_col + (base + sp.nearest) * p.C + c, p.upstream[pixb * p.C + c]);
+            atomicAdd(acc + pt * p.C + c, static_cast<double>(p.upstream[pixb * p.C + c]));
+    }
+}
+
+__global__ void k_special_merge(SpecBwdParams p, const double* __restrict__ acc,
+                                const int* __restrict__ own) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int n = min(*p.special_count, p.special_cap);
+    for (int si = warp; si < n; si += nwarps) {
+        size_t pixb, pt;
+        if (!special_route(p, si, pixb, pt) || own[pt] != si) continue;
+        for (int c = lane; c < p.C; c += 32) {
+            float* d = p.d_col + pt * p.C + c;
+            *d = static_cast<float>(static_cast<double>(*d) + acc[pt * p.C + c]);
+        }
     }
 }
 
 // float4 slots of one staged pixel pair (PairLayout<CG>::kF4)
 inline int pair_f4(int cg) { return (cg + 2) / 2; }
-
-// Precise fallback routing (special count known on the host, i.e. the
-// synchronous API): the upstream of every fallback pixel is summed per
-// (point, channel) in f64 and added to the point's fp32 d_col with ONE
-// rounding.  Sparse inputs route hundreds of O(1) upstream values into a
-// single point; fp32 atomics would carry their rounding (and their
-// nondeterministic order) into a cancellation to ~1e-2.
-__global__ void k_special_backward64(SpecBwdParams p, double* __restrict__ acc) {
-    const int lane = threadIdx.x & 31;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    const int n = min(*p.special_count, p.special_cap);
-    for (int si = warp; si < n; si += nwarps) {
-        const Special sp = p.special[si];
-        if (sp.kind != 1 || sp.nearest < 0) continue;
-        const size_t pixb = static_cast<size_t>(sp.b) * p.H * p.W + sp.pix;
-        const size_t base = static_cast<size_t>(sp.b) * p.N;
-        for (int c = lane; c < p.C; c += 32)
-            atomicAdd(acc + (base + sp.nearest) * p.C + c,
-                      static_cast<double>(p.upstream[pixb * p.C + c]));
-    }
-}
-
-__global__ void k_merge_special(const double* __restrict__ acc, float* __restrict__ d_col,
-                                size_t n) {
-    const size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    if (k >= n) return;
-    const double a = acc[k];
-    if (a != 0.0) d_col[k] = static_cast<float>(static_cast<double>(d_col[k]) + a);
-}
 
 template <int CG, int LPP>
 void launch_points_lpp(gmi_ctx* ctx, const BwdParams& p, int nblocks, int groups) {
@@ -786,19 +798,18 @@ void launch_special_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upst
     p.H = c->H;
     p.fallback = c->fallback;
     p.d_col = d_colors;
+    // count 0 known on the host (synchronous API): nothing to route
     if (c->special_count == 0 || c->fallback != GMI_FALLBACK_NEAREST) return;
-    if (c->special_count > 0) {
-        const size_t n = static_cast<size_t>(c->B) * c->N * c->C;
-        double* acc = static_cast<double*>(scratch(ctx, WS_PART, sizeof(double) * n));
-        GMI_CUDA(cudaMemsetAsync(acc, 0, sizeof(double) * n, ctx->stream));
-        k_special_backward64<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(p, acc);
-        GMI_LAUNCHED(ctx);
-        k_merge_special<<<static_cast<unsigned>((n + 255) / 256), 256, 0, ctx->stream>>>(acc, d_colors, n);
-        GMI_LAUNCHED(ctx);
-        return;
-    }
-    // count unknown (asynchronous API): fp32 atomics
-    k_special_backward<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(p);
+    const size_t npt = static_cast<size_t>(c->B) * c->N;
+    // slots touched only for routed points (never cleared wholesale)
+    double* acc = static_cast<double*>(scratch(ctx, WS_PART, sizeof(double) * npt * c->C));
+    int* own = static_cast<int*>(scratch(ctx, WS_TMP, sizeof(int) * npt));
+    const int grid = 2 * ctx->num_sms;
+    k_special_zero<<<grid, 256, 0, ctx->stream>>>(p, acc, own);
+    GMI_LAUNCHED(ctx);
+    k_special_accumulate<<<grid, 256, 0, ctx->stream>>>(p, acc, own);
+    GMI_LAUNCHED(ctx);
+    k_special_merge<<<grid, 256, 0, ctx->stream>>>(p, acc, own);
     GMI_LAUNCHED(ctx);
 }
 

@@ -61,26 +61,29 @@ def test_device_path_validation(gmi, ctx):
     assert e.value.code == 4
 
 
-def test_cuda_graph_capture_replays_the_step(gmi, orc):
+@pytest.mark.parametrize("n", [3000, 250])  # 250: many fallback pixels (K3 / K5 in the graph)
+def test_cuda_graph_capture_replays_the_step(gmi, orc, n):
     # a whole forward + backward (binning, gather, special pixels, backward,
     # the cache's stream-ordered allocations and frees) captured once as a
     # CUDA graph and replayed gives the eager results bit for bit
     torch = pytest.importorskip("torch")
-    pos, col, up = orc.synth_batch(43, 2, 3000, 3, 80, 60)
+    pos, col, up = orc.synth_batch(43, 2, n, 3, 80, 60)
+    if n < 1000:
+        assert gmi.forward_batch(pos, col, 80, 60, 1.0, 3.0)[1].fallback_count > 0
     dev = torch.device("cuda", 0)
     s = torch.cuda.Stream(dev)
     tpos, tcol, tup = (torch.from_numpy(a).to(dev) for a in (pos, col, up))
     img = torch.empty(2, 60, 80, 3, device=dev)
-    dc = torch.empty(2, 3000, 3, device=dev)
-    dp = torch.empty(2, 3000, 2, device=dev)
+    dc = torch.empty(2, n, 3, device=dev)
+    dp = torch.empty(2, n, 2, device=dev)
     gctx = gmi.Context(0)
     gctx.set_stream(s.cuda_stream)
     gctx.set_flags(1)
     torch.cuda.synchronize()
 
     def step():
-        cache = gctx.forward_device(tpos, tcol, 2, 3000, 3, 80, 60, 1.0, 3.0, 0, img)
-        gctx.backward_device(tpos, tcol, 2, 3000, 3, 80, 60, 1.0, 3.0, 0, cache, tup, dc, dp)
+        cache = gctx.forward_device(tpos, tcol, 2, n, 3, 80, 60, 1.0, 3.0, 0, img)
+        gctx.backward_device(tpos, tcol, 2, n, 3, 80, 60, 1.0, 3.0, 0, cache, tup, dc, dp)
         del cache
 
     for _ in range(3):
