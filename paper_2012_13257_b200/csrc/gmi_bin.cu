@@ -448,8 +448,6 @@ struct ScatterEmitParams {
     const float* col;
     const Geom* geom;
     int32_t* bins;          // k_scatter_emit: cell ends, decremented to starts
-    const int32_t* cellid;
-    const int32_t* rank;
     float4* rec;
     float* ccol;   // C > 4: [B][N][C] colours in bin order
     unsigned long long* issue;
