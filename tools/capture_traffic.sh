@@ -5,5 +5,5 @@
 O=gpurun_out/traffic
 mkdir -p $O
 python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > $O/plain.json 2> $O/plain.err && \
-ncu --set full --clock-control none --import-source on -k regex:"k_backward_points|k_gather|k_scatter_emit" \
-    -s 3 -c 3 -o $O/cfg3 python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > $O/ncu.log 2>&1
+ncu --set full --clock-control none --import-source on --graph-profiling node -k regex:"k_backward_points|k_gather|k_scatter_emit" \
+    -s 3 -c 3 -o $O/cfg3 python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline --graph off > $O/ncu.log 2>&1
