@@ -804,7 +804,7 @@ void launch_special_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upst
     // slots touched only for routed points (never cleared wholesale)
     double* acc = static_cast<double*>(scratch(ctx, WS_PART, sizeof(double) * npt * c->C));
     int* own = static_cast<int*>(scratch(ctx, WS_TMP, sizeof(int) * npt));
-    const int grid = 2 * ctx->num_sms;
+    const int grid = 8 * ctx->num_sms;  // many routed pixels in flight (dependent loads)
     k_special_zero<<<grid, 256, 0, ctx->stream>>>(p, acc, own);
     GMI_LAUNCHED(ctx);
     k_special_accumulate<<<grid, 256, 0, ctx->stream>>>(p, acc, own);

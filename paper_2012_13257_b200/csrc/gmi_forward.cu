@@ -474,7 +474,9 @@ void launch_special_forward(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* c
     p.special = c->special;
     p.special_count = c->special_count_d;
     p.special_cap = c->special_cap;
-    k_special<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(p);
+    // one warp per fallback pixel, up to 64 per SM in flight: the ring
+    // search is a chain of dependent loads, hidden by many pixels at once
+    k_special<<<8 * ctx->num_sms, 256, 0, ctx->stream>>>(p);
     GMI_LAUNCHED(ctx);
 }
 
