@@ -100,6 +100,8 @@ int collect_issue(gmi_ctx* ctx, int B) {
                                   (B > 1 ? " (image " + std::to_string(b) + ")" : "");
         if (code == GMI_ERR_COLOR_OUT_OF_RANGE)
             return fail(code, "color out of [0,1]" + where);
+        if (code == GMI_ERR_OUT_OF_MEMORY)
+            return fail(code, "more than " + std::to_string(idx) + " fallback pixels in one call");
         return fail(code, "non-finite value" + where);
     }
     return GMI_OK;
@@ -115,6 +117,11 @@ void join_copy_streams(gmi_ctx* ctx) {
         cudaStreamWaitEvent(ctx->stream, ev, 0);
         cudaEventDestroy(ev);
     }
+}
+
+__global__ void k_check_special(const int32_t* count, int cap, unsigned long long* issue) {
+    if (*count > cap)
+        atomicMin(issue, (static_cast<unsigned long long>(cap) << 8) | GMI_ERR_OUT_OF_MEMORY);
 }
 
 void free_cache_buffers(gmi_cache* c) {
@@ -230,6 +237,12 @@ int do_forward(gmi_ctx* ctx, const float* pos, const float* col, int B, int N,
         gmi_host::launch_special_forward(ctx, c, image, counts);
     }
     host_trace("fwd: gather+special launched");
+    if ((ctx->flags & GMI_CTX_ASYNC_ERRORS) && counts == nullptr) {
+        // no host check below: a fallback list overflow becomes a pending
+        // error reported by gmi_ctx_synchronize
+        k_check_special<<<1, 1, 0, ctx->stream>>>(c->special_count_d, c->special_cap, d_issue);
+        GMI_LAUNCHED(ctx);
+    }
     if (!(ctx->flags & GMI_CTX_ASYNC_ERRORS) || counts != nullptr) {
         int32_t nspec = 0;
         GMI_CUDA(cudaMemcpyAsync(&nspec, c->special_count_d, sizeof(int32_t),
