@@ -1,0 +1,91 @@
+"""Randomised parity sweep of the CUDA path against the C oracle (the
+restatement pinned to the reference): random frames, batch sizes, point
+counts, channel counts, sigma / cutoff, clusters, points outside the frame,
+integer lattices, fallback modes, synchronous and asynchronous contexts.
+Exits non-zero on the first mismatch (bit-exact fallback sets / nearest
+indices / counts; image and gradients within the north-star tolerance).
+
+    python tools/fuzz_parity.py [--seconds 300] [--seed 0]
+"""
+import argparse, os, sys, time
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def close(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return np.all(np.abs(a - b) <= 1e-6 + 1e-5 * np.maximum(np.abs(a), np.abs(b)))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--seconds", type=float, default=300)
+    ap.add_argument("--seed", type=int, default=0)
+    a = ap.parse_args()
+    import oracle
+    import paper_2012_13257_b200 as gmi
+    orc = oracle.Oracle()
+    rng = np.random.default_rng(a.seed)
+    sync_ctx, async_ctx = gmi.Context(0), gmi.Context(0)
+    async_ctx.set_flags(1)
+    t_end = time.time() + a.seconds
+    n_cases = 0
+    while time.time() < t_end:
+        W = int(rng.integers(1, 200))
+        H = int(rng.integers(1, 160))
+        B = int(rng.integers(1, 4))
+        C = int(rng.choice([1, 2, 3, 4, 3, 3, 5, 8, 16, 33]))
+        sigma = float(rng.choice([0.5, 0.8, 1.0, 1.5, 2.0, 3.0, rng.uniform(0.3, 4.0)]))
+        k = float(rng.choice([3.0, 3.0, 2.0, 2.5, 4.0, rng.uniform(1.0, 5.0)]))
+        cutoff = k * sigma
+        dens = float(rng.choice([0.02, 0.1, 0.3, 1.0, 3.0]))
+        N = max(1, int(dens * W * H))
+        N = min(N, 60000)
+        cluster = float(rng.choice([0.0, 0.0, 0.3, 0.8]))
+        # fp32 accumulation stays inside 1e-5 up to ~2e4 contributors per
+        # pixel; keep clusters below that
+        if cluster > 0:
+            N = min(N, int(15000 / cluster))
+        pos, col, up = orc.synth_batch(int(rng.integers(1 << 30)), B, N, C, W, H,
+                                       cluster_frac=cluster, cluster_px=int(rng.choice([1, 3, 16])))
+        mode = rng.integers(0, 4)
+        if mode == 1:  # some points far outside the frame
+            m = max(1, N // 10)
+            pos[:, :m] = rng.uniform(-3 * max(W, H), 4 * max(W, H), (B, m, 2)).astype(np.float32)
+        elif mode == 2:  # integer / half-integer lattice (boundary ties)
+            step = float(rng.choice([1.0, 2.0, 3.0]))
+            xs, ys = np.meshgrid(np.arange(0, W, step), np.arange(0, H, step))
+            lat = np.stack([xs.ravel(), ys.ravel()], 1).astype(np.float32)
+            lat += np.float32(rng.choice([0.0, 0.5]))
+            n2 = min(N, lat.shape[0])
+            pos[:, :n2] = lat[:n2]
+        fb = "nearest" if rng.random() < 0.8 else "zero"
+        ctx = async_ctx if rng.random() < 0.5 else sync_ctx
+        img, cache = gmi.forward_batch(pos, col, W, H, sigma, cutoff, fb, ctx=ctx)
+        dc, dp = gmi.backward_batch(pos, col, cache, up, sigma, cutoff, fb, ctx=ctx)
+        ctx.synchronize()
+        _, flag, near = cache.pixels()
+        desc = f"case {n_cases}: B={B} N={N} C={C} {W}x{H} sigma={sigma:.3f} r={cutoff:.3f} cluster={cluster} mode={mode} fb={fb}"
+        for b in range(B):
+            p64, c64, u64 = (x[b].astype(np.float64) for x in (pos, col, up))
+            r = orc.forward(p64, c64, W, H, sigma, cutoff, 0 if fb == "nearest" else 1)
+            rdc, rdp = orc.backward(p64, c64, r, u64, sigma, cutoff, 0 if fb == "nearest" else 1)
+            ok = np.array_equal(flag[b], r["fallback_flag"])
+            if fb == "nearest":
+                ok &= np.array_equal(near[b], np.where(r["fallback_flag"] == 1, r["nearest_index"], -1))
+            ok &= close(img[b], r["image"]) and close(dc[b], rdc) and close(dp[b], rdp)
+            if not ok:
+                print("MISMATCH", desc, "image", b, flush=True)
+                np.savez("gpurun_out/fuzz_fail.npz", pos=pos, col=col, up=up, W=W, H=H, sigma=sigma,
+                         cutoff=cutoff, fb=fb)
+                sys.exit(1)
+        n_cases += 1
+        if n_cases % 25 == 0:
+            print(f"{n_cases} cases ok ({desc})", flush=True)
+    print(f"fuzz ok: {n_cases} cases, {a.seconds:.0f} s")
+
+
+if __name__ == "__main__":
+    main()
