@@ -414,8 +414,9 @@ k_backward_points(BwdParams p) {
         float2 dcol[CG];
 #pragma unroll
         for (int c = 0; c < CG; ++c) dcol[c] = f2(0.f, 0.f);
-        float2 gx2 = f2(0.f, 0.f);
-        float gy = 0.f;
+        // d_pos: fp32 sums inside a row, f64 across rows (the row sums
+        // cancel; an fp32 total would carry their rounding)
+        double gx = 0.0, gy = 0.0;
         const float tx = truncf(mx);
         const float fmu = mx - tx;  // exact
         const int bx = static_cast<int>(tx);
@@ -467,7 +468,7 @@ k_backward_points(BwdParams p) {
             // pair's weight is bit-identical to the one summed into W
             const float ey = (dy * nk) * dy;
             if (!staged) {
-                float gyr = 0.f;
+                float gyr = 0.f, gxr = 0.f;
                 for (int x = xl; x <= xr; ++x) {
                     const float dx = static_cast<float>(x) - mx;
                     const float w = ex2(fmaf(dx * nk, dx, ey));
@@ -479,10 +480,11 @@ k_backward_points(BwdParams p) {
                     const float a = w * t;
 #pragma unroll
                     for (int c = 0; c < CG; ++c) dcol[c].x = fmaf(w, u[c], dcol[c].x);
-                    gx2.x = fmaf(a, dx, gx2.x);
+                    gxr = fmaf(a, dx, gxr);
                     gyr += a;
                 }
-                gy = fmaf(gyr, dy, gy);
+                gx += static_cast<double>(gxr);
+                gy = fma(static_cast<double>(gyr), static_cast<double>(dy), gy);
                 continue;
             }
             // pair-aligned span (rx0 is even): pairs xs..xs+2(np-1); the end
@@ -493,7 +495,7 @@ k_backward_points(BwdParams p) {
             const float ml = ((xr - rx0) & 1) ? 1.f : 0.f;
             float2 X = f2(static_cast<float>(xs), static_cast<float>(xs + 1));
             const float2 ey2 = f2(ey, ey), mmx = f2(-mx, -mx);
-            float2 gyr2 = f2(0.f, 0.f);
+            float2 gyr2 = f2(0.f, 0.f), gx2 = f2(0.f, 0.f);
             const float4* pr = s_pair + (y - ry0) * npairs + ((xs - rx0) >> 1);
 #pragma unroll 1
             for (int j = 0; j < np; ++j) {
@@ -518,9 +520,10 @@ k_backward_points(BwdParams p) {
                 X = __fadd2_rn(X, two);
                 ++pr;
             }
-            gy = fmaf(gyr2.x + gyr2.y, dy, gy);
+            gx += static_cast<double>(gx2.x + gx2.y);
+            gy = fma(static_cast<double>(gyr2.x + gyr2.y), static_cast<double>(dy), gy);
         }
-        float gxs = gx2.x + gx2.y;
+        double gxs = gx;
         float dcs[CG];
 #pragma unroll
         for (int c = 0; c < CG; ++c) dcs[c] = dcol[c].x + dcol[c].y;
@@ -533,8 +536,8 @@ k_backward_points(BwdParams p) {
         if (!live || sub != 0) continue;
         for (int c = 0; c < nch; ++c) p.d_col[(base + i) * p.C + ch0 + c] = dcs[c];
         float* dp = p.d_pos + (static_cast<size_t>(cg) * p.B * p.N + base + i) * 2;
-        dp[0] = gxs * inv_s2;
-        dp[1] = gy * inv_s2;
+        dp[0] = static_cast<float>(gxs * static_cast<double>(inv_s2));
+        dp[1] = static_cast<float>(gy * static_cast<double>(inv_s2));
     }
 }
 
