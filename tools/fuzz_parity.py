@@ -27,6 +27,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=300)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--large", action="store_true",
+                    help="fewer, larger cases (frames up to 640 px, up to 250k points)")
     a = ap.parse_args()
     import oracle
     import paper_2012_13257_b200 as gmi
@@ -37,8 +39,8 @@ def main():
     t_end = time.time() + a.seconds
     n_cases, marginal, worst = 0, 0, 0.0
     while time.time() < t_end:
-        W = int(rng.integers(1, 200))
-        H = int(rng.integers(1, 160))
+        W = int(rng.integers(1, 640 if a.large else 200))
+        H = int(rng.integers(1, 640 if a.large else 160))
         B = int(rng.integers(1, 4))
         C = int(rng.choice([1, 2, 3, 4, 3, 3, 5, 8, 16, 33]))
         sigma = float(rng.choice([0.5, 0.8, 1.0, 1.5, 2.0, 3.0, rng.uniform(0.3, 4.0)]))
@@ -46,7 +48,7 @@ def main():
         cutoff = k * sigma
         dens = float(rng.choice([0.02, 0.1, 0.3, 1.0, 3.0]))
         N = max(1, int(dens * W * H))
-        N = min(N, 60000)
+        N = min(N, 250000 if a.large else 60000)
         cluster = float(rng.choice([0.0, 0.0, 0.3, 0.8]))
         # fp32 accumulation stays inside 1e-5 up to ~2e4 contributors per
         # pixel; keep clusters below that
