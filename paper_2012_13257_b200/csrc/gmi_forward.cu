@@ -282,21 +282,6 @@ __device__ int nearest_exact(const SpecParams& p, const Geom& g, int b,
     const size_t base = static_cast<size_t>(b) * p.N;
     double best = INFINITY;
     int bi = INT32_MAX;
-    auto scan_cell = [&](int gx, int gy) {
-        if (gx < 0 || gx >= g.n_cols || gy < 0 || gy >= g.n_rows) return;
-        const int64_t bin = g.bin_off + static_cast<int64_t>(gy) * g.n_cols + gx;
-        const int s = p.bins[bin], e = p.bins[bin + 1];
-        for (int k = s + lane; k < e; k += 32) {
-            float px, py;
-            int i;
-            point_at(p, base + k, px, py, i);
-            const double d2 = d2_ref(qx, qy, static_cast<double>(px), static_cast<double>(py));
-            if (d2 < best || (d2 == best && i < bi)) {
-                best = d2;
-                bi = i;
-            }
-        }
-    };
     if (g.capped) {
         // clamped edge cells break ring pruning: brute force
         for (int k = lane; k < p.N; k += 32) {
@@ -336,17 +321,20 @@ __device__ int nearest_exact(const SpecParams& p, const Geom& g, int b,
             }
         }
     };
-    for (int ring = 0; ring <= ring_cap; ++ring) {
+    // rings 0..kR0 at once (a fallback pixel's nearest point is usually 1-2
+    // cells away): one round of dependent loads instead of kR0 + 1; the
+    // argmin over a superset of the rings the reference visits is the same
+    // point, and the ring bound then resumes at ring kR0 + 1
+    constexpr int kR0 = 2, kSide0 = 2 * kR0 + 1;
+    for (int c = lane; c < kSide0 * kSide0; c += 32)
+        scan_cell_serial(qcx - kR0 + c % kSide0, qcy - kR0 + c / kSide0);
+    for (int ring = kR0 + 1; ring <= ring_cap; ++ring) {
         double wb = best;
         int wi = bi;
         warp_argmin(wb, wi);
-        if (wi != INT32_MAX && ring >= 1) {
+        if (wi != INT32_MAX) {
             const double lb = (ring - 1) * g.cell;
             if (lb * lb > wb) break;
-        }
-        if (ring == 0) {
-            scan_cell(qcx, qcy);
-            continue;
         }
         const int side = 2 * ring + 1;
         for (int c = lane; c < 8 * ring; c += 32) {
