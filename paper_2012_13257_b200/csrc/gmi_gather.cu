@@ -7,8 +7,10 @@
 // whose normaliser W and numerators live in f32x2 registers.
 //
 //  stage  The candidate points of the tile (reference cells overlapping the
-//         tile grown by r, one run per cell row) are counting-sorted in shared
-//         memory by (1-px column, row-pair) bin.  Bin geometry is exact (f64
+//         tile grown by r: one contiguous run of 32-byte records per cell
+//         row) arrive in shared memory by TMA — one cp.async.bulk per run,
+//         completing on an mbarrier — and are counting-sorted there by
+//         (1-px column, row-pair) bin into dense record arrays.  Bin geometry is exact (f64
 //         differences of fp32 positions against integer / f64 anchors), so a
 //         point that can reach the tile lands in the bins its pixels read.
 //         Within a bin the order is canonicalised by original index, so the
