@@ -374,7 +374,9 @@ def main():
         torch.cuda.synchronize(dev)
         n0 = ctx.launch_count
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
+        # thread-local capture: CUDA calls from other threads (the NCCL
+        # watchdog under torchrun, the clock sampler) are not disturbed
+        with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
             c = step()
             del c
         n = ctx.launch_count - n0
