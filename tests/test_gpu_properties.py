@@ -1,0 +1,130 @@
+"""Property tests of the device path, restating the reference's engine
+invariants (proj/tests/test_engine.cpp) and adding size-independent checks at
+the BASELINE frame size, where the oracle would take minutes.
+
+Reference pins restated (the reference asserts them in f64 at 1e-12; the
+device computes in fp32, so the north-star tolerance |a-b| <= 1e-6 + 1e-5
+max(|a|,|b|) applies unless the arithmetic is exact):
+  - shared weights across channels          test_engine.cpp:72-88
+  - convex-combination bound                test_engine.cpp:122-139
+  - constant colours reconstruct            test_engine.cpp:141-156
+  - translation equivariance (bit-exact)    test_engine.cpp:158-187
+  - sigma-scaling consistency               test_engine.cpp:189-215
+  - constant colours -> d_pos = 0           test_engine.cpp:313-330
+At scale (configs[2] geometry, 1024^2, N = 262,144, sigma = 1.5):
+  - partition of unity of the backward: sum_i d_col[i] = sum_p upstream[p]
+    (every pixel's ratios sum to 1; fallback pixels route to their nearest
+    point under NearestPoint, engine.cpp:200-211), per image and channel.
+"""
+import numpy as np
+import pytest
+
+from conftest import ABS_TOL, REL_TOL, assert_close
+
+pytestmark = pytest.mark.gpu
+
+
+def random_points(rng, n, c, extent):
+    """gmi_test::random_points (test_support.hpp): positions U[-1, extent)."""
+    pos = rng.uniform(-1.0, extent, size=(1, n, 2)).astype(np.float32)
+    col = rng.uniform(0.0, 1.0, size=(1, n, c)).astype(np.float32)
+    return pos, col
+
+
+def test_shared_weights_flat_channel(gmi, ctx):
+    rng = np.random.default_rng(5)
+    pos, col = random_points(rng, 12, 3, 8.0)
+    col[..., 1] = 0.25
+    img, _ = gmi.forward_batch(pos, col, 8, 8, 1.5, ctx=ctx)
+    assert_close(img[..., 1], np.full_like(img[..., 1], 0.25), what="flat channel")
+
+
+def test_convex_bound(gmi, ctx):
+    rng = np.random.default_rng(7)
+    pos, col = random_points(rng, 30, 1, 10.0)
+    img, cache = gmi.forward_batch(pos, col, 10, 10, 0.8, ctx=ctx)
+    _, flag, _ = cache.pixels()
+    ok = flag[0] == 0
+    lo, hi = float(col.min()), float(col.max())
+    v = img[0, ..., 0][ok].astype(np.float64)
+    assert (v >= lo - ABS_TOL - REL_TOL * lo).all() and (v <= hi + ABS_TOL + REL_TOL * hi).all()
+
+
+@pytest.mark.parametrize("sigma", [0.5, 1.0, 3.0])
+def test_constant_colours_reconstruct(gmi, ctx, sigma):
+    rng = np.random.default_rng(8)
+    pos, col = random_points(rng, 20, 1, 10.0)
+    col[:] = 0.37
+    img, _ = gmi.forward_batch(pos, col, 10, 10, sigma, ctx=ctx)
+    assert_close(img, np.full_like(img, np.float32(0.37)), what=f"constant sigma={sigma}")
+
+
+@pytest.mark.parametrize("cutoff", [100.0, 3.0])
+def test_translation_equivariance_dyadic(gmi, ctx, cutoff):
+    """Dyadic positions + integer shifts are exact in fp32 too, so every
+    weight is bit-identical.  With the reference's 100-sigma cutoff (the
+    precise path, ascending-index sums) the shifted render is bit-identical;
+    with 3 sigma the tiles of the fast gather move against the points, so
+    the summation order may change: tolerance."""
+    rng = np.random.default_rng(9)
+    pos = (rng.integers(0, 97, size=(1, 15, 2)) / 8.0).astype(np.float32)
+    col = rng.uniform(0.0, 1.0, size=(1, 15, 1)).astype(np.float32)
+    dx, dy = 3, 2
+    moved = pos + np.array([dx, dy], np.float32)
+    base, _ = gmi.forward_batch(pos, col, 12, 12, 1.0, cutoff, ctx=ctx)
+    shifted, _ = gmi.forward_batch(moved, col, 12 + dx, 12 + dy, 1.0, cutoff, ctx=ctx)
+    win = shifted[0, dy:dy + 12, dx:dx + 12]
+    if cutoff == 100.0:
+        assert np.array_equal(base[0], win)
+    else:
+        assert_close(win, base[0], what="shifted window")
+
+
+def test_sigma_scaling(gmi, ctx):
+    rng = np.random.default_rng(10)
+    pos = rng.integers(0, 6, size=(1, 10, 2)).astype(np.float32)
+    col = rng.uniform(0.0, 1.0, size=(1, 10, 1)).astype(np.float32)
+    s = 2.0
+    base, _ = gmi.forward_batch(pos, col, 6, 6, 0.9, 1000.0, ctx=ctx)
+    big, _ = gmi.forward_batch(pos * s, col, 11, 11, 0.9 * s, 1000.0, ctx=ctx)
+    # nk = -log2(e) / (2 sigma^2) rounds differently for the two sigmas: the
+    # exponents (|e| <= ~100) agree to a few fp32 ulps, weights to ~1e-5 rel
+    assert_close(big[0, ::2, ::2], base[0], rel=5e-5, abs_=1e-6, what="sigma scaling")
+
+
+def test_constant_colours_zero_position_gradient(gmi, ctx):
+    rng = np.random.default_rng(11)
+    pos, col = random_points(rng, 40, 3, 16.0)
+    col[:] = np.array([0.2, 0.5, 0.9], np.float32)
+    sigma = 1.2
+    r = 3 * sigma
+    img, cache = gmi.forward_batch(pos, col, 16, 16, sigma, ctx=ctx)
+    up = np.ones_like(img)
+    dc, dp = gmi.backward_batch(pos, col, cache, up, sigma, ctx=ctx)
+    # exact zero in f64; in fp32 out_p = c (1 + O(1e-7)), so
+    # |d_pos_i| <= r / sigma^2 * sum_c c_c d_col_ic * O(1e-7)
+    scale = (r / sigma ** 2) * (dc[0] * col[0]).sum(axis=1, keepdims=True)
+    assert (np.abs(dp[0]) <= ABS_TOL + REL_TOL * scale).all(), np.abs(dp[0]).max()
+
+
+def test_backward_partition_of_unity_at_scale(gmi, ctx):
+    """configs[2] frame and density (2 images): sum_i d_col = sum_p upstream."""
+    rng = np.random.default_rng(2026)
+    B, N, C, W, H, sigma = 2, 262144, 3, 1024, 1024, 1.5
+    pos = np.empty((B, N, 2), np.float32)
+    pos[..., 0] = rng.uniform(-0.5, W - 0.5, size=(B, N))
+    pos[..., 1] = rng.uniform(-0.5, H - 0.5, size=(B, N))
+    col = rng.uniform(0.0, 1.0, size=(B, N, C)).astype(np.float32)
+    img, cache = gmi.forward_batch(pos, col, W, H, sigma, ctx=ctx)
+    up = rng.uniform(-1.0, 1.0, size=img.shape).astype(np.float32)
+    dc, dp = gmi.backward_batch(pos, col, cache, up, sigma, ctx=ctx)
+    assert np.isfinite(dc).all() and np.isfinite(dp).all()
+    got = dc.astype(np.float64).sum(axis=1)                     # [B, C]
+    want = up.astype(np.float64).sum(axis=(1, 2))               # [B, C]
+    # each d_col entry carries ~1e-6 relative fp32 error
+    bound = ABS_TOL + REL_TOL * np.abs(dc.astype(np.float64)).sum(axis=1)
+    assert (np.abs(got - want) <= bound).all(), (got, want, bound)
+    # and the image is a convex combination wherever W > 0
+    _, flag, _ = cache.pixels()
+    v = img[flag == 0]
+    assert v.min() >= -ABS_TOL and v.max() <= 1.0 + ABS_TOL + REL_TOL
