@@ -11,10 +11,13 @@ max(|a|,|b|) applies unless the arithmetic is exact):
   - translation equivariance (bit-exact)    test_engine.cpp:158-187
   - sigma-scaling consistency               test_engine.cpp:189-215
   - constant colours -> d_pos = 0           test_engine.cpp:313-330
-At scale (configs[2] geometry, 1024^2, N = 262,144, sigma = 1.5):
+At the BASELINE sizes (configs[2] through the host API; configs[3], one
+8192^2 image with 16.7M points, and one configs[4] image, C = 64 with a 5%
+cluster, through the zero-copy device path):
   - partition of unity of the backward: sum_i d_col[i] = sum_p upstream[p]
     (every pixel's ratios sum to 1; fallback pixels route to their nearest
-    point under NearestPoint, engine.cpp:200-211), per image and channel.
+    point under NearestPoint, engine.cpp:200-211), per image and channel;
+  - the image is a convex combination of colours in [0, 1].
 """
 import numpy as np
 import pytest
@@ -128,3 +131,49 @@ def test_backward_partition_of_unity_at_scale(gmi, ctx):
     _, flag, _ = cache.pixels()
     v = img[flag == 0]
     assert v.min() >= -ABS_TOL and v.max() <= 1.0 + ABS_TOL + REL_TOL
+
+
+def _device_scale_case(gmi, ctx, B, N, C, W, H, sigma, cluster, seed):
+    """Forward + backward at a full BASELINE size through the zero-copy
+    device path (inputs generated on the device with torch, as bench.py
+    does), checked by partition of unity and the convex bound."""
+    torch = pytest.importorskip("torch")
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    pos = torch.empty(B, N, 2, device="cuda")
+    pos[..., 0].uniform_(-0.5, W - 0.5, generator=g)
+    pos[..., 1].uniform_(-0.5, H - 0.5, generator=g)
+    nc = int(cluster * N)
+    if nc:
+        corner = torch.rand(B, 1, 2, device="cuda", generator=g) * torch.tensor([W - 32.0, H - 32.0],
+                                                                                device="cuda")
+        pos[:, :nc] = corner + torch.rand(B, nc, 2, device="cuda", generator=g) * 32.0
+    col = torch.rand(B, N, C, device="cuda", generator=g)
+    img = torch.empty(B, H, W, C, device="cuda")
+    torch.cuda.synchronize()
+    _, cache = gmi.forward_cuda(pos, col, W, H, sigma, image=img, ctx=ctx)
+    torch.cuda.synchronize()
+    up = torch.empty_like(img).uniform_(-1.0, 1.0, generator=g)
+    dc = torch.empty(B, N, C, device="cuda")
+    dp = torch.empty(B, N, 2, device="cuda")
+    torch.cuda.synchronize()
+    gmi.backward_cuda(pos, col, cache, up, sigma, d_colors=dc, d_positions=dp, ctx=ctx)
+    torch.cuda.synchronize()
+    assert bool(torch.isfinite(img).all()) and bool(torch.isfinite(dc).all())
+    assert bool(torch.isfinite(dp).all())
+    got = dc.double().sum(dim=1)
+    want = up.double().sum(dim=(1, 2))
+    bound = ABS_TOL + REL_TOL * dc.double().abs().sum(dim=1)
+    assert bool(((got - want).abs() <= bound).all()), (got - want).abs().max().item()
+    assert float(img.min()) >= -ABS_TOL and float(img.max()) <= 1.0 + ABS_TOL + REL_TOL
+
+
+def test_partition_of_unity_configs3_single_huge_image(gmi, ctx):
+    """configs[3]: one 8192^2 image, N = 16,777,216, sigma = 1 (one GPU)."""
+    _device_scale_case(gmi, ctx, 1, 16777216, 3, 8192, 8192, 1.0, 0.0, 33)
+
+
+def test_partition_of_unity_configs4_wide_clustered(gmi, ctx):
+    """configs[4] per image: 2048^2, N = 1,048,576 with 5% in one 32^2
+    square, C = 64 (wide kernels), sigma = 4."""
+    _device_scale_case(gmi, ctx, 1, 1048576, 64, 2048, 2048, 4.0, 0.05, 44)
