@@ -177,3 +177,48 @@ def test_partition_of_unity_configs4_wide_clustered(gmi, ctx):
     """configs[4] per image: 2048^2, N = 1,048,576 with 5% in one 32^2
     square, C = 64 (wide kernels), sigma = 4."""
     _device_scale_case(gmi, ctx, 1, 1048576, 64, 2048, 2048, 4.0, 0.05, 44)
+
+
+def test_backward_linear_in_upstream_configs2_full_batch(gmi, ctx):
+    """configs[2] at its full size (B = 64 x 1024^2, N = 262,144, sigma =
+    1.5): the backward is linear in the upstream image, so
+    bwd(2 u1 + u2) = 2 bwd(u1) + bwd(u2) to fp32 rounding, and a zero
+    upstream gives exactly zero gradients."""
+    torch = pytest.importorskip("torch")
+    B, N, C, W, H, sigma = 64, 262144, 3, 1024, 1024, 1.5
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7)
+    pos = torch.empty(B, N, 2, device="cuda")
+    pos[..., 0].uniform_(-0.5, W - 0.5, generator=g)
+    pos[..., 1].uniform_(-0.5, H - 0.5, generator=g)
+    col = torch.rand(B, N, C, device="cuda", generator=g)
+    img = torch.empty(B, H, W, C, device="cuda")
+    torch.cuda.synchronize()
+    _, cache = gmi.forward_cuda(pos, col, W, H, sigma, image=img, ctx=ctx)
+    torch.cuda.synchronize()
+    u1 = torch.empty_like(img).uniform_(-1.0, 1.0, generator=g)
+    u2 = torch.empty_like(img).uniform_(-1.0, 1.0, generator=g)
+    u3 = 2.0 * u1 + u2
+    torch.cuda.synchronize()
+
+    def bwd(u):
+        dc = torch.empty(B, N, C, device="cuda")
+        dp = torch.empty(B, N, 2, device="cuda")
+        gmi.backward_cuda(pos, col, cache, u, sigma, d_colors=dc, d_positions=dp, ctx=ctx)
+        torch.cuda.synchronize()
+        return dc.double(), dp.double()
+
+    c1, p1 = bwd(u1)
+    c2, p2 = bwd(u2)
+    c3, p3 = bwd(u3)
+    for got, want, mag, what in ((c3, 2 * c1 + c2, 2 * c1.abs() + c2.abs(), "d_colors"),
+                                 (p3, 2 * p1 + p2, 2 * p1.abs() + p2.abs(), "d_positions")):
+        # north-star form on the magnitudes of the combined results, plus a
+        # floor of 1e-9 x the largest magnitude: an entry whose terms cancel
+        # (d_positions under a random-sign upstream) keeps the fp32 rounding
+        # of its terms, not of its small total
+        bound = ABS_TOL + REL_TOL * mag + 1e-4 * REL_TOL * float(mag.max())
+        bad = (got - want).abs() > bound
+        assert not bool(bad.any()), f"{what}: {int(bad.sum())} entries off"
+    zc, zp = bwd(torch.zeros_like(u1))
+    assert bool((zc == 0).all()) and bool((zp == 0).all())
