@@ -202,11 +202,17 @@ def test_backward_linear_in_upstream_configs2_full_batch(gmi, ctx):
     torch.cuda.synchronize()
 
     def bwd(u):
+        # the library runs on its context's stream, torch on its own: every
+        # hand-over between them is a device synchronisation (including the
+        # f64 copies below, whose float sources go back to torch's allocator)
         dc = torch.empty(B, N, C, device="cuda")
         dp = torch.empty(B, N, 2, device="cuda")
+        torch.cuda.synchronize()
         gmi.backward_cuda(pos, col, cache, u, sigma, d_colors=dc, d_positions=dp, ctx=ctx)
         torch.cuda.synchronize()
-        return dc.double(), dp.double()
+        out = dc.double(), dp.double()
+        torch.cuda.synchronize()
+        return out
 
     c1, p1 = bwd(u1)
     c2, p2 = bwd(u2)
