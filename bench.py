@@ -244,6 +244,34 @@ def run_reference_arm(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def self_launch(args) -> bool:
+    """`--gpus N` without a launcher: re-run this script as N ranks (torchrun,
+    one process per GPU, rendezvous on 127.0.0.1).  True when it did."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return False
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")        # communicator lines on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    sys.exit(subprocess.call(cmd, env=env))
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+# roofline peaks of the non-tensor pipes (B200: 148 SMs; FP32 128 lanes and
+# MUFU 16 lanes per SM per clock at the max SM clock — the nominal rates, a
+# harder bar than the measured FFMA 122 / EX2 15.9, profiles/ubench_pipes_b200.txt)
+def pipe_peaks(sm_mhz: float):
+    return 148 * 128 * sm_mhz * 1e6, 148 * 16 * sm_mhz * 1e6
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -260,8 +288,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     args = ap.parse_args()
-    world, rank, local = dist_setup(args)
+    self_launch(args)
     if args.impl == "reference":
+        world, rank, local = dist_setup(args)
         run_reference_arm(args, world, rank)
         return
 
@@ -269,8 +298,11 @@ def main():
     import torch
 
     import paper_2012_13257_b200 as gmi
+    from paper_2012_13257_b200 import multi
 
     assert args.warmup >= 3, "contract: at least 3 warm-up steps"
+    group = multi.Group("nccl")
+    world, rank, local = group.world, group.rank, group.local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cfg = dict(CONFIGS[args.config])
@@ -280,9 +312,8 @@ def main():
     B, N, C, W, H = cfg["B"], cfg["N"], cfg["C"], cfg["W"], cfg["H"]
     sigma, cutoff = cfg["sigma"], cfg["cutoff"]
 
-    stream = torch.cuda.Stream(device=dev)
-    ctx = gmi.Context(local)
-    ctx.set_stream(stream.cuda_stream)
+    stream = group.stream
+    ctx = group.ctx
     ctx.set_flags(1)  # asynchronous validation errors; checked after the loop
 
     # configs[3] on N > 1 GPUs: ONE image split into row bands (strong
@@ -303,44 +334,31 @@ def main():
         up = torch.rand(B, H, W, C, device=dev, generator=g) * 2 - 1
     stream.synchronize()
     H_full = H
-    shared_local = None
     if band:
-        # row band of this rank + the points whose balls reach it (cutoff
-        # halo), y shifted to the band (exact); shared points' partial
-        # gradients are SUM-reduced over NCCL inside the step
-        from paper_2012_13257_b200 import dist as gdist
-
-        plan = gdist.BandPlan(pos[0].cpu().numpy(), H, world, rank, cutoff)
+        # the product's band driver: plan (halo certified for far nearest-
+        # point fallbacks), band-local points on the device, NCCL SUM of the
+        # shared points' partial gradients inside every step
+        splitter = multi.BandSplit(group, pos[0].cpu().numpy(), col[0].cpu().numpy(), W, H,
+                                   sigma, cutoff)
+        r0, r1 = splitter.rows
         with torch.cuda.stream(stream):
-            idx = torch.from_numpy(plan.idx).to(dev)
-            bpos = pos[0].index_select(0, idx)
-            bpos[:, 1] -= float(plan.r0)
-            pos = bpos.unsqueeze(0).contiguous()
-            col = col[0].index_select(0, idx).unsqueeze(0).contiguous()
-            up = up[:, plan.r0:plan.r1].contiguous()
-            sl = torch.from_numpy(plan.shared_local).to(dev)
-            shared_local = (sl.clamp(min=0), (sl >= 0).float().unsqueeze(1))
-            halo_buf = torch.zeros(plan.shared.size, C + 2, device=dev)
-        N, H = int(plan.idx.size), plan.rows
+            up = up[:, r0:r1].contiguous()
         stream.synchronize()
-    with torch.cuda.stream(stream):
-        img = torch.empty(B, H, W, C, device=dev)
-        dcol = torch.empty(B, N, C, device=dev)
-        dpos = torch.empty(B, N, 2, device=dev)
-    stream.synchronize()
+        N, H = splitter.N, r1 - r0
 
-    def step():
-        cache = ctx.forward_device(pos, col, B, N, C, W, H, sigma, cutoff, 0, img)
-        if not fwd_only:
-            ctx.backward_device(pos, col, B, N, C, W, H, sigma, cutoff, 0, cache, up, dcol, dpos)
-        if shared_local is not None:
-            import torch.distributed as dist
-            with torch.cuda.stream(stream):
-                li, have = shared_local
-                halo_buf[:, :C] = dcol[0].index_select(0, li) * have
-                halo_buf[:, C:] = dpos[0].index_select(0, li) * have
-                dist.all_reduce(halo_buf, op=dist.ReduceOp.SUM)
-        return cache
+        def step():
+            return splitter.step(up)
+        img = splitter.image
+    else:
+        shards = multi.BatchShards(group, W, H, sigma, cutoff)
+        with torch.cuda.stream(stream):
+            img = torch.empty(B, H, W, C, device=dev)
+            dcol = torch.empty(B, N, C, device=dev)
+            dpos = torch.empty(B, N, 2, device=dev)
+        stream.synchronize()
+
+        def step():
+            return shards.step(pos, col, up, img, dcol, dpos, forward_only=fwd_only)
 
     # warm-up mirrors the timed loop (two caches kept alive) so the
     # stream-ordered memory pool reaches its steady state before timing
@@ -350,11 +368,6 @@ def main():
         if len(warm) > 2:
             warm.pop(0)
     ctx.synchronize()
-
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
 
     # ---- device-resident timed region ----
     # Each timed step replays ONE captured CUDA graph of the whole step
@@ -373,18 +386,18 @@ def main():
         ctx.set_profiling(False)
         torch.cuda.synchronize(dev)
         n0 = ctx.launch_count
-        g = torch.cuda.CUDAGraph()
+        gr = torch.cuda.CUDAGraph()
         # thread-local capture: CUDA calls from other threads (the NCCL
         # watchdog under torchrun, the clock sampler) are not disturbed
-        with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
+        with torch.cuda.graph(gr, stream=stream, capture_error_mode="thread_local"):
             c = step()
             del c
         n = ctx.launch_count - n0
         with torch.cuda.stream(stream):  # replay() launches on the current stream
             for _ in range(2):
-                g.replay()
+                gr.replay()
         torch.cuda.synchronize(dev)
-        return g, n, pm, pc
+        return gr, n, pm, pc
 
     use_graph = args.graph == "on" or (args.graph == "auto" and not band)
     graph, graph_note = None, None
@@ -400,26 +413,26 @@ def main():
     if graph is None:
         ctx.set_profiling(True)
         ctx.phase_times(reset=True)
-    barrier()
+    group.barrier()
     torch.cuda.synchronize(dev)
     launches0 = ctx.launch_count
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     caches = warm
     with ClockSampler(local) as clocks:
-        ev0.record(stream)
-        for _ in range(args.steps):
+        evs[0].record(stream)
+        for k in range(args.steps):
             if graph is not None:
                 with torch.cuda.stream(stream):  # replay() launches on the current stream
                     graph.replay()
-                continue
-            caches.append(step())
-            if len(caches) > 2:
-                caches.pop(0)
-        ev1.record(stream)
+            else:
+                caches.append(step())
+                if len(caches) > 2:
+                    caches.pop(0)
+            evs[k + 1].record(stream)
         torch.cuda.synchronize(dev)
-    ms = ev0.elapsed_time(ev1)
-    barrier()
+    ms = evs[0].elapsed_time(evs[-1])
+    per_step = sorted(evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps))
+    group.barrier()
     launches = (per_step_launches * args.steps if graph is not None
                 else ctx.launch_count - launches0)
     ctx.synchronize()  # raises on any pending validation error
@@ -427,37 +440,72 @@ def main():
         phase_ms, phase_calls = ctx.phase_times(reset=True)
         ctx.set_profiling(False)
     caches.clear()
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = group.max_over_ranks(ms)
+    med = group.max_over_ranks(per_step[len(per_step) // 2])
     ms_step = ms / args.steps
     # band mode: the job renders one full image per step (strong scaling)
-    value = (W * H_full if band else world * B * W * H) / (ms_step * 1e-3) / 1e6
+    units = W * H_full if band else world * B * W * H
+    value = units / (ms_step * 1e-3) / 1e6
 
     # ---- pair count P (exact, counting instantiation of the same kernel) ----
-    cache = ctx.forward_device(pos[:1], col[:1], 1, N, C, W, H, sigma, cutoff, 0, img[:1])
+    with torch.cuda.stream(stream):
+        img1 = torch.empty(1, H, W, C, device=dev)
+    p1 = splitter.pos if band else pos[:1]
+    c1 = splitter.col if band else col[:1]
+    cache = ctx.forward_device(p1, c1, 1, N, C, W, H, sigma, cutoff, 0, img1)
     P_img = int(gmi.forward_counts(cache).astype(np.int64).sum())
     del cache
 
-    # ---- roofline of the dominant kernel (per launch = whole batch) ----
+    # ---- rooflines: the binding pipe (FP32 for the C <= 4 configs), MUFU
+    # and HBM beside it; per launch of the dominant kernel and per step ----
     hbm_peak, sm_mhz, peak_kind = peaks()
+    fp32_peak, mufu_peak = pipe_peaks(sm_mhz)
     per_call = {name: phase_ms[k] / max(1, phase_calls[k]) for k, name in enumerate(gmi.Context.PHASES)}
     dom = "gather" if fwd_only else max(("gather", "points_bwd"), key=lambda k: per_call[k])
+    Bk = 1 if band else B
     pts_bytes = 4 * N * (2 + C)
     img_bytes = 4 * H * W * C
-    alg_bytes = {"gather": B * (pts_bytes + img_bytes),            # points in, image out
-                 "points_bwd": B * (2 * pts_bytes + img_bytes)}   # points in, grads out, upstream in
-    alg_fp32 = {"gather": B * P_img * (6 + C), "points_bwd": B * P_img * (11 + 2 * C)}
+    alg_bytes = {"gather": Bk * (pts_bytes + img_bytes),            # points in, image out
+                 "points_bwd": Bk * (2 * pts_bytes + img_bytes)}   # points in, grads out, upstream in
+    alg_fp32 = {"gather": Bk * P_img * (6 + C), "points_bwd": Bk * P_img * (11 + 2 * C)}
+    alg_mufu = {"gather": Bk * (P_img + H * W), "points_bwd": Bk * (P_img + H * W)}
     t_dom = per_call[dom] * 1e-3
-    achieved = alg_bytes[dom] / t_dom / 1e9
-    fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # T FP32-instr/s
-    fp32_ach = alg_fp32[dom] / t_dom / 1e12
-    total_fp32 = B * P_img * ((6 + C) if fwd_only else (17 + 3 * C))
-    step_fp32_frac = total_fp32 / (ms_step * 1e-3) / 1e12 / fp32_peak
+    step_fp32 = Bk * P_img * ((6 + C) if fwd_only else (17 + 3 * C))
+    step_mufu = Bk * ((P_img + H * W) if fwd_only else 2 * (P_img + H * W))
+    step_bytes = Bk * ((pts_bytes + img_bytes + 12 * N) if fwd_only
+                       else (3 * pts_bytes + 2 * img_bytes + 12 * N))
+    t_roof = {"fp32": step_fp32 / fp32_peak, "mufu": step_mufu / mufu_peak,
+              "hbm": step_bytes / (hbm_peak * 1e9)}
+    binding = max(t_roof, key=t_roof.get)
+    t_step = ms_step * 1e-3
 
-    e2e_ms = None
+    def roof(kind):
+        if kind == "fp32":
+            a, pk, unit = alg_fp32[dom] / t_dom / 1e12, fp32_peak / 1e12, "T FP32-instr/s"
+            counts = "fwd 6+C, bwd 11+2C FP32 instr per (pixel, point) pair (SURVEY §8d)"
+        elif kind == "mufu":
+            a, pk, unit = alg_mufu[dom] / t_dom / 1e12, mufu_peak / 1e12, "T MUFU-op/s"
+            counts = "1 ex2 per pair + 1 rcp per pixel per pass (SURVEY §8d)"
+        else:
+            a, pk, unit = alg_bytes[dom] / t_dom / 1e9, hbm_peak, "GB/s"
+            counts = "4[N(2+C)+HWC] fwd, 4[2N(2+C)+HWC] bwd per image (SURVEY §8d)"
+        return {"bound": {"fp32": "fp32_pipe", "mufu": "mufu_pipe", "hbm": "hbm"}[kind],
+                "kernel": dom, "achieved": round(a, 3), "peak": round(pk, 2), "unit": unit,
+                "frac": round(a / pk, 4), "step_frac": round(t_roof[kind] / t_step, 4),
+                "step_roof_ms": round(t_roof[kind] * 1e3, 4), "counts": counts,
+                "peak_kind": peak_kind if kind == "hbm" else "nominal (148 SMs x lanes x sm_max_mhz)"}
+
+    roofline = roof(binding)
+    roofline["traffic"] = traffic_of(dom, args.config, B)
+    roofline["note"] = ("binding roof = max(FP32, MUFU, HBM) of the step's algorithmic counts; "
+                        "frac = the dominant kernel per launch, step_frac = the whole step")
+    others = {f"roofline_{k}": roof(k) for k in ("fp32", "mufu", "hbm") if k != binding}
+
+    # forward_host uploads positions+colours and downloads the image;
+    # backward_host uploads upstream and downloads both gradients
+    h2d = B * N * 4 * (2 + C) + (0 if fwd_only else B * H * W * C * 4)
+    d2h = B * H * W * C * 4 + (0 if fwd_only else B * N * 4 * (C + 2))
+    e2e_ms = e2e_np_ms = None
     if args.e2e_steps > 0 and not band:
         pinned = [pos.cpu().pin_memory(), col.cpu().pin_memory(), up.cpu().pin_memory(),
                   torch.empty(B, H, W, C).pin_memory(), torch.empty(B, N, C).pin_memory(),
@@ -482,45 +530,45 @@ def main():
             # forward's download inside the step)
             ctx.synchronize()
 
-        # W untimed warm-up steps here too: the first host-buffer steps grow
-        # the stream-ordered memory pool (pinned staging of ~2.3 GB per step)
-        diag = os.environ.get("GMI_E2E_DIAG") is not None
-        for _ in range(max(2, args.warmup)):
-            t0 = time.perf_counter()
-            e2e_step()
-            if diag:
-                print(f"e2e warm-up step {1e3 * (time.perf_counter() - t0):.1f} ms", file=sys.stderr)
-        barrier()
-        torch.cuda.synchronize(dev)
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.e2e_steps):
-            t0 = time.perf_counter()
-            e2e_step()
-            if diag:
-                print(f"e2e timed step {1e3 * (time.perf_counter() - t0):.1f} ms", file=sys.stderr)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
-        if world > 1:
-            import torch.distributed as dist
-            t = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        def timed(fn, n):
+            for _ in range(max(2, args.warmup)):  # grows the memory pool
+                fn()
+            group.barrier()
+            torch.cuda.synchronize(dev)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(n):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            return group.max_over_ranks(e0.elapsed_time(e1) / n)
+
+        e2e_ms = timed(e2e_step, args.e2e_steps)
         e2e_value = world * B * W * H / (e2e_ms * 1e-3) / 1e6
         pcie = pcie_duplex_gbps(dev)
-    # forward_host uploads positions+colours and downloads the image;
-    # backward_host uploads upstream and downloads both gradients
-    h2d = B * N * 4 * (2 + C) + (0 if fwd_only else B * H * W * C * 4)
-    d2h = B * H * W * C * 4 + (0 if fwd_only else B * N * 4 * (C + 2))
+
+        # the reference-shaped numpy shim (forward_batch / backward_batch) on
+        # plain pageable numpy arrays, as a user of gmi._core would call it
+        npos, ncol, nup = (np.array(t) for t in (hpos, hcol, hup))
+
+        def e2e_numpy_step():
+            im, cc = gmi.forward_batch(npos, ncol, W, H, sigma, cutoff, ctx=ctx)
+            if not fwd_only:
+                gmi.backward_batch(npos, ncol, cc, nup, sigma, cutoff, ctx=ctx)
+            ctx.synchronize()
+            cc.close()
+
+        e2e_np_ms = timed(e2e_numpy_step, max(1, min(args.e2e_steps, 2)))
 
     if rank != 0:
+        group.close()
         return
     line = {
         "metric": METRIC if args.config == 3 else METRIC.replace("1024^2, N=262k pts, C=3", cfg["workload"]),
         "value": round(value, 2), "unit": "Mpix/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "ms_per_step_median": round(med, 4), "ms_per_step_min": round(per_step[0], 4),
         "higher_is_better": True, "scaling": "strong" if band else "weak", "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic",
@@ -528,26 +576,23 @@ def main():
                    "points": N, "channels": C, "frame": [H, W], "sigma": sigma,
                    "cutoff": cutoff, "pairs_per_image": P_img,
                    "l2": "inputs > L2 (126 MB): no flush needed",
-                   "parallelism": (f"row bands x{world} (rows {H} + r halo per rank), NCCL SUM of "
-                                   f"{int(shared_local[0].numel())} shared points' gradients per step")
+                   "parallelism": (f"row bands x{world} (rows {H} + halo {splitter.plan.halo:g} per rank), "
+                                   f"NCCL SUM of {int(splitter.plan.shared.size)} shared points' gradients per step")
                                   if band else f"batch-sharded x{world}, no collective"},
         "phases_ms_per_step": {k: round(v, 4) for k, v in per_call.items()},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
-                     "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
-                     "traffic": traffic_of(dom, args.config, B), "peak_kind": peak_kind,
-                     "note": "algorithmic bytes per launch / CUDA-event time; the path is FP32-pipe bound, see roofline_fp32"},
-        "roofline_fp32": {"bound": "fp32_pipe", "kernel": dom, "achieved": round(fp32_ach, 3),
-                          "peak": round(fp32_peak, 2), "unit": "T FP32-instr/s",
-                          "frac": round(fp32_ach / fp32_peak, 4),
-                          "step_frac": round(step_fp32_frac, 4),
-                          "counts": "fwd 6+C, bwd 11+2C FP32 instr per (pixel,point) pair (SURVEY §8d)"},
+        "roofline": roofline,
+        **others,
         "e2e": ({"value": round(e2e_value, 2), "unit": "Mpix/s", "h2d_bytes_per_step": h2d,
                  "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3),
+                 "api": "gmi_forward_host / gmi_backward_host, pinned host buffers",
                  # the e2e bound: both directions' bytes at the measured
                  # pinned full-duplex PCIe rate of this box
                  "roofline": {"bound": "pcie_duplex", "peak_GBps_each_way": round(pcie, 1),
                               "bound_ms": round(max(h2d, d2h) / (pcie * 1e9) * 1e3, 3),
-                              "frac": round(max(h2d, d2h) / (pcie * 1e9) * 1e3 / e2e_ms, 4)}}
+                              "frac": round(max(h2d, d2h) / (pcie * 1e9) * 1e3 / e2e_ms, 4)},
+                 "numpy_shim": {"value": round(world * B * W * H / (e2e_np_ms * 1e-3) / 1e6, 2),
+                                "ms_per_step": round(e2e_np_ms, 3),
+                                "api": "forward_batch / backward_batch on pageable numpy arrays"}}
                 if e2e_ms else None),
         "gpu_launches": launches,
         "cuda_graph": graph is not None if graph_note is None else graph_note,
@@ -559,6 +604,7 @@ def main():
                                 "kind": kind,
                                 "sample": f"{imgs} image(s) of the workload, fwd+bwd, {secs:.1f} s"}
     print(json.dumps(line), flush=True)
+    group.close()
 
 
 if __name__ == "__main__":

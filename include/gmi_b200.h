@@ -81,9 +81,13 @@ enum {
      * complete, and their host inputs may be reused, after
      * gmi_ctx_synchronize() — so a backward's upload overlaps the preceding
      * forward's download.  Default (0): every call synchronises and returns
-     * the reference's error synchronously. */
+     * the reference's error synchronously.  The pending error is the first
+     * failing call's first failing image (smallest index there); it stays
+     * pending until gmi_ctx_synchronize() reports and clears it. */
     GMI_CTX_ASYNC_ERRORS = 1u << 0,
-    /* Bit-deterministic fallback-gradient routing (default on). */
+    /* Reserved, ignored: every path (forward, backward, fallback routing) is
+     * bit-deterministic run to run; there is no faster non-deterministic
+     * mode. */
     GMI_CTX_NONDETERMINISTIC = 1u << 1
 };
 
@@ -92,6 +96,8 @@ typedef struct gmi_cache gmi_cache; /* ForwardCache (engine.hpp:20-41) */
 
 /* ---- context ------------------------------------------------------------ */
 int gmi_ctx_create(int device, gmi_ctx** out);
+/* Drops the caller's handle.  Caches made on the ctx keep it alive (its
+ * stream and device state) until the last of them is freed. */
 int gmi_ctx_destroy(gmi_ctx* ctx);
 /* Use an external cudaStream_t (passed as void*); NULL = the ctx's own. */
 int gmi_ctx_set_stream(gmi_ctx* ctx, void* cuda_stream);

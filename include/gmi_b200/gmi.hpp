@@ -17,6 +17,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -140,6 +141,30 @@ struct GradientSet {  // core.hpp:119-131
 
 double gaussian_weight(const Vec2& q, const Vec2& mu, double sigma);  // core.cpp:49-53
 
+struct ValidationIssue {  // core.hpp:138-142
+    ErrorCode code;
+    int index;  // offending point, -1 when not point-specific
+    std::string message;
+};
+
+// core.hpp:144-149 (core.cpp:55-120), with C >= 1 channels accepted (the
+// device path's contract) instead of C in {1, 3}
+std::optional<ValidationIssue> validate_point_set(const PointSet& ps);
+void require_valid(const PointSet& ps);  // throws Error on violation
+void require_valid(const InterpConfig& cfg);
+void require_frame(const CoordinateFrame& frame);
+
+// The device path computes on fp32 inputs.  Positions / colours that are not
+// exactly representable in fp32 are rounded to nearest (the reference would
+// see the unrounded f64 values).  Allow (default) rounds and records the
+// number of rounded values in ForwardCache::inexact_inputs; Reject throws
+// DeviceError(GMI_ERR_INVALID_ARGUMENT) naming the first such value, for
+// callers that need the reference's bit-exact binning / neighbour decisions.
+enum class Fp32Inputs { Allow, Reject };
+void set_fp32_inputs(Fp32Inputs policy);  // this thread's calls
+// Number of positions + colours of `ps` that fp32 cannot hold exactly.
+std::int64_t count_inexact_fp32(const PointSet& ps);
+
 // ForwardCache (engine.hpp:20-41): metadata + per-pixel normaliser, fallback
 // flags and nearest indices, output copy; the device state (binned points,
 // W) backs backward().
@@ -161,6 +186,8 @@ struct ForwardCache {
     int fallback_count() const;
     // pixel_start deltas (engine.hpp:29-31), recomputed on the device
     std::vector<std::int32_t> contribution_counts() const;
+    // positions + colours rounded to fp32 by this forward (Fp32Inputs)
+    std::int64_t inexact_inputs = 0;
 
     std::shared_ptr<gmi_cache> device;  // owned device state
 };

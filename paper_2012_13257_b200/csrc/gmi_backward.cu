@@ -274,7 +274,11 @@ k_backward_points(BwdParams p) {
 
     if (staged) {
         // 8-byte alignment of a pixel pair in W / upstream / image rows
-        const bool vec = (p.W % 2 == 0) && (CG == p.C);
+        // (64-bit loads: the caller's upstream / image may be any float
+        // pointer, e.g. a view at an odd element offset)
+        const bool vec = (p.W % 2 == 0) && (CG == p.C) &&
+                         ((reinterpret_cast<uintptr_t>(p.upstream) |
+                           reinterpret_cast<uintptr_t>(p.image)) & 7) == 0;
         const bool vec4 = CG == 4 && (p.C % 4) == 0 && (p.W % 2) == 0 &&
                           (reinterpret_cast<uintptr_t>(p.upstream) & 15) == 0 &&
                           (reinterpret_cast<uintptr_t>(p.image) & 15) == 0;
@@ -474,9 +478,12 @@ k_backward_points(BwdParams p) {
                     const float w = ex2(fmaf(dx * nk, dx, ey));
                     float u[CG], v;
                     pixel_terms<CG>(p, img_base, ch0, nch, x, y, u, v);
-                    float t = -v;
+                    // t = sum_c c_ic u_c - v with the sum formed by the same
+                    // chain as v (pixel_terms): exactly 0 where c_i == out
+                    float t = u[0] * cc[0];
 #pragma unroll
-                    for (int c = 0; c < CG; ++c) t = fmaf(u[c], cc[c], t);
+                    for (int c = 1; c < CG; ++c) t = fmaf(u[c], cc[c], t);
+                    t -= v;
                     const float a = w * t;
 #pragma unroll
                     for (int c = 0; c < CG; ++c) dcol[c].x = fmaf(w, u[c], dcol[c].x);
@@ -508,10 +515,15 @@ k_backward_points(BwdParams p) {
                 float2 w = f2(ex2(arg.x), ex2(arg.y));
                 if (j == 0) w.x *= mf;
                 if (j == np - 1) w.y *= ml;
-                // t = sum_c c_ic u_c - v  (= dot / W, engine.cpp:219-221)
-                float2 t = q[CG];
+                // t = sum_c c_ic u_c - v  (= dot / W, engine.cpp:219-221);
+                // the sum is formed by the same operation chain as the staged
+                // v = sum_c u_c out_c, so t is exactly 0 where the pixel's
+                // output equals the point's colour (a sole contributor): the
+                // reference's dot is 0 there up to f64 rounding
+                float2 t = __fmul2_rn(q[0], f2(cc[0], cc[0]));
 #pragma unroll
-                for (int c = 0; c < CG; ++c) t = __ffma2_rn(q[c], f2(cc[c], cc[c]), t);
+                for (int c = 1; c < CG; ++c) t = __ffma2_rn(q[c], f2(cc[c], cc[c]), t);
+                t = __fadd2_rn(t, q[CG]);
                 const float2 a = __fmul2_rn(w, t);
 #pragma unroll
                 for (int c = 0; c < CG; ++c) dcol[c] = __ffma2_rn(w, q[c], dcol[c]);

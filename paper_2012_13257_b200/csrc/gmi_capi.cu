@@ -124,6 +124,62 @@ __global__ void k_check_special(const int32_t* count, int cap, unsigned long lon
         atomicMin(issue, (static_cast<unsigned long long>(cap) << 8) | GMI_ERR_OUT_OF_MEMORY);
 }
 
+// GMI_CTX_ASYNC_ERRORS: the call's first failing image (slots in image order)
+// becomes the ctx's pending error unless an earlier call already left one —
+// stream order makes "earlier" the call order, so gmi_ctx_synchronize reports
+// the first error since it last ran.
+__global__ void k_merge_issue(const unsigned long long* issue, int B, int b0,
+                              unsigned long long* pending) {
+    if (pending[0] != gmi_dev::kNoIssue) return;
+    for (int b = 0; b < B; ++b) {
+        if (issue[b] != gmi_dev::kNoIssue) {
+            pending[0] = issue[b];
+            pending[1] = static_cast<unsigned long long>(b0 + b);
+            return;
+        }
+    }
+}
+
+// Reads and clears the pending asynchronous error (stream drained).
+int collect_pending(gmi_ctx* ctx) {
+    unsigned long long h[2];
+    GMI_CUDA(cudaMemcpyAsync(h, ctx->d_pending, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    GMI_CUDA(cudaMemsetAsync(ctx->d_pending, 0xFF, sizeof(h), ctx->stream));
+    GMI_CUDA(cudaStreamSynchronize(ctx->stream));
+    const unsigned long long k = h[0];
+    if (k == gmi_dev::kNoIssue) return GMI_OK;
+    const long idx = static_cast<long>(k >> 8);
+    const int code = static_cast<int>(k & 0xff);
+    const std::string where = " at index " + std::to_string(idx) + " (image " +
+                              std::to_string(static_cast<long>(h[1])) + ")";
+    if (code == GMI_ERR_COLOR_OUT_OF_RANGE) return fail(code, "color out of [0,1]" + where);
+    if (code == GMI_ERR_OUT_OF_MEMORY)
+        return fail(code, "more than " + std::to_string(idx) + " fallback pixels in one call");
+    return fail(code, "non-finite value" + where);
+}
+
+void ctx_retain(gmi_ctx* ctx) { ctx->refs.fetch_add(1, std::memory_order_relaxed); }
+
+void ctx_teardown(gmi_ctx* ctx) {
+    cudaSetDevice(ctx->device);
+    // the grow-only scratch slots go back to the pool with the context
+    for (int s = 0; s < WS_COUNT; ++s)
+        if (ctx->ws_ptr[s]) cudaFreeAsync(ctx->ws_ptr[s], ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->d_issue) cudaFree(ctx->d_issue);
+    if (ctx->h_issue) cudaFreeHost(ctx->h_issue);
+    if (ctx->d_pending) cudaFree(ctx->d_pending);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
+    if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
+    delete ctx;
+}
+
+// Drops one reference; the last one (creator or cache) tears the ctx down.
+void ctx_release(gmi_ctx* ctx) {
+    if (ctx->refs.fetch_sub(1, std::memory_order_acq_rel) == 1) ctx_teardown(ctx);
+}
+
 void free_cache_buffers(gmi_cache* c) {
     if (c->d2h_done != nullptr) {
         // an asynchronous gmi_forward_host may still be downloading the image
@@ -242,6 +298,12 @@ int do_forward(gmi_ctx* ctx, const float* pos, const float* col, int B, int N,
         // error reported by gmi_ctx_synchronize
         k_check_special<<<1, 1, 0, ctx->stream>>>(c->special_count_d, c->special_cap, d_issue);
         GMI_LAUNCHED(ctx);
+        if (!ctx->collect_now) {
+            k_merge_issue<<<1, 1, 0, ctx->stream>>>(d_issue, B,
+                                                    static_cast<int>(d_issue - ctx->d_issue),
+                                                    ctx->d_pending);
+            GMI_LAUNCHED(ctx);
+        }
     }
     if (!(ctx->flags & GMI_CTX_ASYNC_ERRORS) || counts != nullptr) {
         int32_t nspec = 0;
@@ -553,6 +615,8 @@ int gmi_ctx_create(int device, gmi_ctx** out) {
         GMI_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
         GMI_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         ctx->own_stream = true;
+        GMI_CUDA(cudaMalloc(&ctx->d_pending, 2 * sizeof(unsigned long long)));
+        GMI_CUDA(cudaMemset(ctx->d_pending, 0xFF, 2 * sizeof(unsigned long long)));
         // keep freed stream-ordered memory cached between calls
         cudaMemPool_t pool;
         GMI_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -566,17 +630,9 @@ int gmi_ctx_create(int device, gmi_ctx** out) {
 int gmi_ctx_destroy(gmi_ctx* ctx) {
     if (ctx == nullptr) return GMI_OK;
     return guarded([&]() -> int {
-        cudaSetDevice(ctx->device);
-        // the grow-only scratch slots go back to the pool with the context
-        for (int s = 0; s < WS_COUNT; ++s)
-            if (ctx->ws_ptr[s]) cudaFreeAsync(ctx->ws_ptr[s], ctx->stream);
-        cudaStreamSynchronize(ctx->stream);
-        if (ctx->d_issue) cudaFree(ctx->d_issue);
-        if (ctx->h_issue) cudaFreeHost(ctx->h_issue);
-        if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
-        if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
-        if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
-        delete ctx;
+        // caches still alive keep the context (their stream and device) until
+        // the last of them is freed
+        ctx_release(ctx);
         return GMI_OK;
     });
 }
@@ -615,8 +671,7 @@ int gmi_ctx_synchronize(gmi_ctx* ctx) {
         // host-buffer downloads queued by asynchronous host-API calls
         if (ctx->s_in) GMI_CUDA(cudaStreamSynchronize(ctx->s_in));
         if (ctx->s_out) GMI_CUDA(cudaStreamSynchronize(ctx->s_out));
-        if (ctx->d_issue_cap > 0) return collect_issue(ctx, ctx->d_issue_cap);
-        return GMI_OK;
+        return collect_pending(ctx);
     });
 }
 
@@ -676,17 +731,21 @@ int gmi_forward(gmi_ctx* ctx, const float* positions, const float* colors, int32
         GMI_CUDA(cudaSetDevice(ctx->device));
         auto* c = new gmi_cache();
         c->ctx = ctx;
+        c->holds_ctx = true;
+        ctx_retain(ctx);
         try {
             rc = do_forward(ctx, positions, colors, batch, num_points, channels, cfg, image, c,
                             nullptr);
         } catch (...) {
             free_cache_buffers(c);
             delete c;
+            ctx_release(ctx);
             throw;
         }
         if (rc != GMI_OK) {
             free_cache_buffers(c);
             delete c;
+            ctx_release(ctx);
             return rc;
         }
         *cache_out = c;
@@ -730,6 +789,8 @@ int gmi_forward_host(gmi_ctx* ctx, const float* positions, const float* colors, 
         ensure_issue(ctx, batch);
         auto* c = new gmi_cache();
         c->ctx = ctx;
+        c->holds_ctx = true;
+        ctx_retain(ctx);
         c->B = batch;
         c->N = num_points;
         c->C = channels;
@@ -766,6 +827,8 @@ int gmi_forward_host(gmi_ctx* ctx, const float* positions, const float* colors, 
                 GMI_CUDA(cudaEventRecord(in[k], ctx->s_in));
             }
             ctx->flags |= GMI_CTX_ASYNC_ERRORS;
+            // a synchronous call collects its parts' errors itself below
+            ctx->collect_now = (saved & GMI_CTX_ASYNC_ERRORS) == 0;
             for (int k = 0; k < nk; ++k) {
                 const size_t o = b0[k];
                 const int n = b0[k + 1] - b0[k];
@@ -784,6 +847,7 @@ int gmi_forward_host(gmi_ctx* ctx, const float* positions, const float* colors, 
                                          cudaMemcpyDeviceToHost, ctx->s_out));
             }
             ctx->flags = saved;
+            ctx->collect_now = false;
             GMI_CUDA(cudaEventCreateWithFlags(&c->d2h_done, cudaEventDisableTiming));
             GMI_CUDA(cudaEventRecord(c->d2h_done, ctx->s_out));
             // GMI_CTX_ASYNC_ERRORS: return with the image download still
@@ -812,15 +876,18 @@ int gmi_forward_host(gmi_ctx* ctx, const float* positions, const float* colors, 
             }
         } catch (...) {
             ctx->flags = saved;
+            ctx->collect_now = false;
             cudaStreamSynchronize(ctx->s_in);
             cudaStreamSynchronize(ctx->s_out);
             free_cache_buffers(c);
             delete c;
+            ctx_release(ctx);
             throw;
         }
         if (rc != GMI_OK) {
             free_cache_buffers(c);
             delete c;
+            ctx_release(ctx);
             return rc;
         }
         *cache_out = c;
@@ -902,9 +969,12 @@ int gmi_backward_host(gmi_ctx* ctx, const float* positions, const float* colors,
 
 void gmi_cache_free(gmi_cache* c) {
     if (c == nullptr) return;
-    cudaSetDevice(c->ctx->device);
+    gmi_ctx* ctx = c->ctx;
+    cudaSetDevice(ctx->device);
     free_cache_buffers(c);
+    const bool held = c->holds_ctx;
     delete c;
+    if (held) ctx_release(ctx);
 }
 
 int gmi_cache_shape(const gmi_cache* c, int32_t* batch, int32_t* num_points, int32_t* channels,

@@ -3,7 +3,9 @@
 // the reference's ErrorCode on every validation failure.
 #include "gmi_b200/gmi.hpp"
 
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 
@@ -14,6 +16,7 @@ namespace gmi {
 namespace {
 
 thread_local int t_device = 0;
+thread_local Fp32Inputs t_fp32 = Fp32Inputs::Allow;
 
 struct CtxDeleter {
     void operator()(gmi_ctx* c) const { gmi_ctx_destroy(c); }
@@ -52,13 +55,38 @@ gmi_config to_cfg(const InterpConfig& cfg, const CoordinateFrame& frame) {
     return c;
 }
 
-void to_f32(const PointSet& ps, std::vector<float>& pos, std::vector<float>& col) {
+bool inexact(double v) {
+    // NaN / inf go to the device's own validation (the reference's codes)
+    return std::isfinite(v) && static_cast<double>(static_cast<float>(v)) != v;
+}
+
+// Rounds the f64 inputs to the device's fp32; returns how many changed value
+// (Fp32Inputs::Reject: throws on the first).
+std::int64_t to_f32(const PointSet& ps, std::vector<float>& pos, std::vector<float>& col) {
+    std::int64_t rounded = 0;
+    auto reject = [&](const char* what, std::size_t i, double v) {
+        if (t_fp32 == Fp32Inputs::Reject) {
+            char buf[160];
+            std::snprintf(buf, sizeof(buf), "%s %.17g at index %zu is not representable in fp32",
+                          what, v, i);
+            throw DeviceError(GMI_ERR_INVALID_ARGUMENT, buf);
+        }
+        ++rounded;
+    };
     pos.resize(static_cast<std::size_t>(ps.size()) * 2);
     for (int i = 0; i < ps.size(); ++i) {
-        pos[2 * i] = static_cast<float>(ps.positions[i].x);
-        pos[2 * i + 1] = static_cast<float>(ps.positions[i].y);
+        const Vec2 p = ps.positions[i];
+        if (inexact(p.x)) reject("position x", i, p.x);
+        if (inexact(p.y)) reject("position y", i, p.y);
+        pos[2 * i] = static_cast<float>(p.x);
+        pos[2 * i + 1] = static_cast<float>(p.y);
     }
-    col.assign(ps.colors.begin(), ps.colors.end());
+    col.resize(ps.colors.size());
+    for (std::size_t k = 0; k < ps.colors.size(); ++k) {
+        if (inexact(ps.colors[k])) reject("color", k / std::max(ps.channels, 1), ps.colors[k]);
+        col[k] = static_cast<float>(ps.colors[k]);
+    }
+    return rounded;
 }
 
 // core.cpp:55-66 shape checks (C relaxed to >= 1); value checks run on the
@@ -78,6 +106,63 @@ void check_shape(const PointSet& ps) {
 const char* error_code_name(ErrorCode code) { return gmi_error_name(static_cast<int>(code) + 1); }
 
 void set_device(int device) { t_device = device; }
+
+void set_fp32_inputs(Fp32Inputs policy) { t_fp32 = policy; }
+
+std::int64_t count_inexact_fp32(const PointSet& ps) {
+    std::int64_t n = 0;
+    for (const Vec2& p : ps.positions) n += inexact(p.x) + inexact(p.y);
+    for (double c : ps.colors) n += inexact(c);
+    return n;
+}
+
+// core.cpp:55-96 (C >= 1)
+std::optional<ValidationIssue> validate_point_set(const PointSet& ps) {
+    if (ps.positions.empty()) return ValidationIssue{ErrorCode::EmptyPointSet, -1, "point set is empty"};
+    if (ps.channels < 1)
+        return ValidationIssue{ErrorCode::ShapeMismatch, -1,
+                               "channels must be >= 1, got " + std::to_string(ps.channels)};
+    const std::size_t expected = ps.positions.size() * static_cast<std::size_t>(ps.channels);
+    if (ps.colors.size() != expected)
+        return ValidationIssue{ErrorCode::ShapeMismatch, -1,
+                               "colors holds " + std::to_string(ps.colors.size()) +
+                                   " values, expected " + std::to_string(expected)};
+    for (int i = 0; i < ps.size(); ++i) {
+        const Vec2 p = ps.positions[i];
+        if (!std::isfinite(p.x) || !std::isfinite(p.y))
+            return ValidationIssue{ErrorCode::NonFiniteValue, i,
+                                   "non-finite position at index " + std::to_string(i)};
+        for (int ch = 0; ch < ps.channels; ++ch) {
+            const double c = ps.color(i, ch);
+            if (!std::isfinite(c))
+                return ValidationIssue{ErrorCode::NonFiniteValue, i,
+                                       "non-finite color at index " + std::to_string(i)};
+            if (c < 0.0 || c > 1.0)
+                return ValidationIssue{ErrorCode::ColorOutOfRange, i,
+                                       "color " + std::to_string(c) + " out of [0,1] at index " +
+                                           std::to_string(i)};
+        }
+    }
+    return std::nullopt;
+}
+
+void require_valid(const PointSet& ps) {
+    if (auto issue = validate_point_set(ps)) throw Error(issue->code, issue->message);
+}
+
+// core.cpp:104-113
+void require_valid(const InterpConfig& cfg) {
+    if (!std::isfinite(cfg.sigma) || cfg.sigma <= 0.0)
+        throw Error(ErrorCode::ConfigInvalid, "sigma must be positive and finite");
+    if (!std::isfinite(cfg.cutoff_radius) || cfg.cutoff_radius <= 0.0)
+        throw Error(ErrorCode::ConfigInvalid, "cutoff_radius must be positive and finite");
+}
+
+// core.cpp:115-120
+void require_frame(const CoordinateFrame& frame) {
+    if (frame.width < 1 || frame.height < 1)
+        throw Error(ErrorCode::InvalidDimensions, "frame dimensions must be at least 1x1");
+}
 
 ImageBuffer ImageBuffer::zeros(int height, int width, int channels) {
     if (height < 1 || width < 1 || channels < 1)
@@ -119,7 +204,7 @@ ForwardResult forward(const PointSet& ps, const InterpConfig& cfg,
     check_shape(ps);
     const gmi_config c = to_cfg(cfg, out_frame);
     std::vector<float> pos, col;
-    to_f32(ps, pos, col);
+    const std::int64_t rounded = to_f32(ps, pos, col);
     std::vector<float> img(static_cast<std::size_t>(std::max(out_frame.width, 0)) *
                            std::max(out_frame.height, 0) * ps.channels);
     gmi_cache* h = nullptr;
@@ -137,6 +222,7 @@ ForwardResult forward(const PointSet& ps, const InterpConfig& cfg,
     fc.sigma = cfg.sigma;
     fc.cutoff_radius = cfg.cutoff_radius;
     fc.fallback = cfg.fallback;
+    fc.inexact_inputs = rounded;
     const std::size_t hw = static_cast<std::size_t>(fc.num_pixels());
     std::vector<float> norm(hw);
     fc.fallback_flag.resize(hw);

@@ -48,6 +48,10 @@ struct GmiFail {
     } while (0)
 
 struct gmi_ctx {
+    // one reference held by the creator (gmi_ctx_destroy drops it) and one
+    // by every live cache returned to a caller: a cache may outlive the
+    // handle it was made with (the C++ API's thread-local contexts)
+    std::atomic<int> refs{1};
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
@@ -60,9 +64,15 @@ struct gmi_ctx {
     std::vector<int> pending_codes;
     std::string pending_msg;
     int pending_code = 0;
-    // device scratch for validation keys
+    // device scratch for validation keys (per image of the current call)
     unsigned long long* d_issue = nullptr;
     int d_issue_cap = 0;
+    // first asynchronous error since the last gmi_ctx_synchronize:
+    // [0] = key (index << 8 | code), [1] = image; sticky until read
+    unsigned long long* d_pending = nullptr;
+    // set while a synchronous host-buffer call runs its parts asynchronously
+    // (their errors are collected by that call, not left pending)
+    bool collect_now = false;
     // optional per-phase CUDA-event timing (gmi_ctx_set_profiling)
     bool profiling = false;
     struct PhaseMark {
@@ -135,6 +145,7 @@ struct Special {
 
 struct gmi_cache {
     gmi_ctx* ctx = nullptr;
+    bool holds_ctx = false;   // a caller-owned cache: one reference on ctx
     int B = 0, N = 0, C = 0, W = 0, H = 0;
     double sigma = 0, cutoff = 0;
     int fallback = 0;

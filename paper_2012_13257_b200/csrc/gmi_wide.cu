@@ -456,16 +456,32 @@ __device__ __forceinline__ void load_px16(const BwdWideParams& p, size_t pix, in
     }
 }
 
+// sum_c u_c x_c over the group's 16 channels as four chains (c mod 4) in
+// f32x2, combined in a fixed order.  The backward forms both v = sum u out
+// and sum u c_i with it, so t = sum u c_i - v is exactly 0 where a pixel's
+// output equals the point's colour (a sole contributor).
+__device__ __forceinline__ float chain16(const float2* uu, const float2* xx) {
+    float2 ta = make_float2(0.f, 0.f), tb = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < kBG / 2; k += 2) {
+        ta = __ffma2_rn(uu[k], xx[k], ta);
+        tb = __ffma2_rn(uu[k + 1], xx[k + 1], tb);
+    }
+    return (ta.x + ta.y) + (tb.x + tb.y);
+}
+
 // u_c = up_c / W and v = sum_c u_c out_c (zeros for W == 0: fallback pixel)
 __device__ __forceinline__ float pixel_uv(float w, float* u, const float* im) {
     const float inv = w > 0.f ? 1.0f / w : 0.f;
-    float v = 0.f;
+    float2 uu[kBG / 2], oo[kBG / 2];
 #pragma unroll
-    for (int c = 0; c < kBG; ++c) {
-        u[c] *= inv;
-        v = fmaf(u[c], im[c], v);
+    for (int k = 0; k < kBG / 2; ++k) {
+        u[2 * k] *= inv;
+        u[2 * k + 1] *= inv;
+        uu[k] = make_float2(u[2 * k], u[2 * k + 1]);
+        oo[k] = make_float2(im[2 * k], im[2 * k + 1]);
     }
-    return v;
+    return chain16(uu, oo);
 }
 
 // Column walk: CTA = (image, cell column, segment of kBSeg cell rows, group).
@@ -747,14 +763,9 @@ k_backward_wide(BwdWideParams p) {
                         const float dx = xf - mx;
                         const float w = ex2(fmaf(dx * nk, dx, ey));
                         // t = sum_c c_ic u_c - v  (= dot / W, engine.cpp:219-221):
-                        // four partial sums (chains c mod 4) as two f32x2
-                        float2 ta = f2(-v, 0.f), tb = f2(0.f, 0.f);
-#pragma unroll
-                        for (int k = 0; k < kBG / 2; k += 2) {
-                            ta = __ffma2_rn(uu[k], cc2[k], ta);
-                            tb = __ffma2_rn(uu[k + 1], cc2[k + 1], tb);
-                        }
-                        const float t = (ta.x + ta.y) + (tb.x + tb.y);
+                        // four partial sums (chains c mod 4) as two f32x2, the
+                        // chain of the staged v (chain16)
+                        const float t = chain16(uu, cc2) - v;
                         const float a = w * t;
                         gx = fmaf(a, dx, gx);
                         gy = fmaf(a, dy, gy);
@@ -769,13 +780,10 @@ k_backward_wide(BwdWideParams p) {
                         const float v = pixel_uv(w0, u, im);
                         const float dx = xf - mx;
                         const float w = ex2(fmaf(dx * nk, dx, ey));
-                        float2 ta = f2(-v, 0.f), tb = f2(0.f, 0.f);
+                        float2 uu[kBG / 2];
 #pragma unroll
-                        for (int k = 0; k < kBG / 2; k += 2) {
-                            ta = __ffma2_rn(f2(u[2 * k], u[2 * k + 1]), cc2[k], ta);
-                            tb = __ffma2_rn(f2(u[2 * k + 2], u[2 * k + 3]), cc2[k + 1], tb);
-                        }
-                        const float t = (ta.x + ta.y) + (tb.x + tb.y);
+                        for (int k = 0; k < kBG / 2; ++k) uu[k] = f2(u[2 * k], u[2 * k + 1]);
+                        const float t = chain16(uu, cc2) - v;
                         const float a = w * t;
                         gx = fmaf(a, dx, gx);
                         gy = fmaf(a, dy, gy);

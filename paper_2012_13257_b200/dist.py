@@ -30,35 +30,44 @@ def band_rows(height: int, world: int, rank: int) -> tuple[int, int]:
     return shard_range(height, world, rank)
 
 
-def band_point_mask(pos_y: np.ndarray, r0: int, r1: int, cutoff: float) -> np.ndarray:
-    """Points whose closed ball of radius `cutoff` can touch a pixel row in
-    [r0, r1): |mu_y - y| <= cutoff for some integer y in the band."""
-    lo = r0 - cutoff - 1.0
-    hi = (r1 - 1) + cutoff + 1.0
+def default_halo(cutoff: float) -> float:
+    """Rows beyond a band a point may sit and still reach it: the cutoff
+    (closed ball, bin_grid.cpp:98) plus one row of slack."""
+    return float(cutoff) + 1.0
+
+
+def band_point_mask(pos_y: np.ndarray, r0: int, r1: int, halo: float) -> np.ndarray:
+    """Points a band keeps: mu_y in [r0 - halo, r1 - 1 + halo].  With the
+    default halo (cutoff + 1) that is every point whose closed ball can touch
+    a pixel row in [r0, r1) (|mu_y - y| <= cutoff for an integer y there);
+    a wider halo also keeps the candidates of far nearest-point fallbacks."""
+    lo = r0 - halo
+    hi = (r1 - 1) + halo
     return (pos_y >= lo) & (pos_y <= hi)
 
 
-def halo_points(pos_y: np.ndarray, height: int, world: int, cutoff: float) -> np.ndarray:
-    """Number of bands each point contributes to (>1: its gradient is a sum of
+def halo_points(pos_y: np.ndarray, height: int, world: int, halo: float) -> np.ndarray:
+    """Number of bands each point belongs to (>1: its gradient is a sum of
     per-band partials and needs the cross-rank reduction)."""
     n = np.zeros(pos_y.shape[0], np.int32)
     for r in range(world):
         r0, r1 = band_rows(height, world, r)
-        n += band_point_mask(pos_y, r0, r1, cutoff)
+        n += band_point_mask(pos_y, r0, r1, halo)
     return n
 
 
-def band_points(pos_y: np.ndarray, r0: int, r1: int, cutoff: float) -> np.ndarray:
-    """Ascending indices of the points a rank needs for rows [r0, r1).  The
+def band_points(pos_y: np.ndarray, r0: int, r1: int, halo: float) -> np.ndarray:
+    """Ascending indices of the points a rank keeps for rows [r0, r1).  The
     ascending order keeps the reference's per-pixel summation order
-    (engine.cpp:59-72 sums in ascending point index)."""
-    return np.nonzero(band_point_mask(pos_y, r0, r1, cutoff))[0]
+    (engine.cpp:59-72 sums in ascending point index) and its nearest-point
+    tie rule (smallest index, bin_grid.cpp:114-164)."""
+    return np.nonzero(band_point_mask(pos_y, r0, r1, halo))[0]
 
 
-def shared_points(pos_y: np.ndarray, height: int, world: int, cutoff: float) -> np.ndarray:
-    """Ascending indices of the points whose balls reach two or more bands:
-    the only gradients that need a cross-rank reduction."""
-    return np.nonzero(halo_points(pos_y, height, world, cutoff) > 1)[0]
+def shared_points(pos_y: np.ndarray, height: int, world: int, halo: float) -> np.ndarray:
+    """Ascending indices of the points kept by two or more bands: the only
+    gradients that need a cross-rank reduction."""
+    return np.nonzero(halo_points(pos_y, height, world, halo) > 1)[0]
 
 
 class BandPlan:
@@ -67,10 +76,15 @@ class BandPlan:
     by -r0, exact in fp32 for integer r0 within the frame) and where the
     globally shared points sit in its local arrays."""
 
-    def __init__(self, pos: np.ndarray, height: int, world: int, rank: int, cutoff: float):
+    def __init__(self, pos: np.ndarray, height: int, world: int, rank: int, cutoff: float,
+                 halo: float | None = None):
         self.r0, self.r1 = band_rows(height, world, rank)
-        self.idx = band_points(pos[:, 1], self.r0, self.r1, cutoff)
-        self.shared = shared_points(pos[:, 1], height, world, cutoff)
+        self.cutoff = float(cutoff)
+        self.halo = default_halo(cutoff) if halo is None else float(halo)
+        if self.halo < default_halo(cutoff):
+            raise ValueError("halo must be >= cutoff + 1")
+        self.idx = band_points(pos[:, 1], self.r0, self.r1, self.halo)
+        self.shared = shared_points(pos[:, 1], height, world, self.halo)
         # local slot of each shared point on this rank (-1: not in this band)
         where = np.full(pos.shape[0], -1, np.int64)
         where[self.idx] = np.arange(self.idx.size)
@@ -83,6 +97,34 @@ class BandPlan:
     @property
     def rows(self) -> int:
         return self.r1 - self.r0
+
+    def halo_needed(self, pos: np.ndarray, fb_pixels: np.ndarray, fb_nearest: np.ndarray,
+                    width: int) -> float:
+        """The halo under which this band's nearest-point fallbacks are the
+        full frame's (bin_grid.cpp:114-164: argmin over ALL points, ties to
+        the smallest index).  `fb_pixels` are band-local pixel ids (r * W + c)
+        of the band's fallback pixels and `fb_nearest` the band-local point
+        each one chose.  A point the band does not keep lies more than
+        m = min(y - (r0 - halo), (r1 - 1 + halo) - y) rows from pixel row y,
+        so a local choice at distance d <= m is the global one (ties
+        included: every point at distance <= m is kept).  Returns the current
+        halo when every choice is certified, else the smallest halo that
+        certifies the worst one (plus one row)."""
+        if len(fb_pixels) == 0:
+            return self.halo
+        fb_pixels = np.asarray(fb_pixels, np.int64)
+        near = self.idx[np.asarray(fb_nearest, np.int64)]
+        qx = (fb_pixels % width).astype(np.float64)
+        qy = (fb_pixels // width + self.r0).astype(np.float64)
+        p = np.asarray(pos, np.float64)[near]
+        d = np.sqrt((qx - p[:, 0]) ** 2 + (qy - p[:, 1]) ** 2)
+        inner = np.minimum(qy - self.r0, (self.r1 - 1) - qy)  # rows to the band edge
+        m = inner + self.halo
+        # certified with a relative guard for the f64 distance itself
+        bad = d * (1.0 + 1e-12) + 1e-9 > m
+        if not bad.any():
+            return self.halo
+        return float(np.ceil(np.max(d[bad] - inner[bad])) + 1.0)
 
     def local_positions(self, pos: np.ndarray) -> np.ndarray:
         p = np.array(pos[self.idx], dtype=pos.dtype, copy=True)
@@ -111,6 +153,30 @@ class BandPlan:
         g_col[self.shared] = reduced[:, :C]
         g_pos[self.shared] = reduced[:, C:]
         return g_col, g_pos
+
+
+def resolve_band_plan(pos: np.ndarray, width: int, height: int, world: int, rank: int,
+                      cutoff: float, probe, reduce_max=None, max_rounds: int = 4) -> "BandPlan":
+    """The band plan whose nearest-point fallbacks equal the full frame's.
+
+    `probe(plan)` renders the band (the device forward on the plan's local
+    points) and returns (band-local fallback pixel ids, band-local nearest
+    point of each).  Every rank certifies its fallbacks (BandPlan.halo_needed);
+    the halo is the max over ranks (`reduce_max`, identity for one process) so
+    that all ranks agree on the kept and shared point sets.  One widening
+    certifies every fallback: the widened halo keeps the previous choice and
+    puts the band edge beyond it, and a closer point found there is closer
+    still."""
+    reduce_max = reduce_max or (lambda v: v)
+    halo = default_halo(cutoff)
+    for _ in range(max_rounds):
+        plan = BandPlan(pos, height, world, rank, cutoff, halo)
+        fb_pix, fb_near = probe(plan)
+        need = float(reduce_max(plan.halo_needed(pos, fb_pix, fb_near, width)))
+        if need <= halo:
+            return plan
+        halo = need
+    raise RuntimeError("band halo did not converge")
 
 
 def max_over_ranks(value: float, device=None) -> float:

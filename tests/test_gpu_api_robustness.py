@@ -1,0 +1,100 @@
+"""Host-API contracts that are not numerics: asynchronous error reporting,
+context lifetime against caches that outlive it, and device pointers at any
+element alignment.  (sticky async errors, cache-held contexts,
+misaligned 64-bit loads in the backward's staging.)"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _bad_colour(orc, seed, b, i):
+    pos, col, up = orc.synth_batch(seed, 2, 500, 3, 40, 30)
+    col[b, i, 1] = 1.5
+    return pos, col, up
+
+
+def test_async_error_survives_later_calls(gmi, orc):
+    # the first failing call's error stays pending across a later clean call
+    actx = gmi.Context(0)
+    actx.set_flags(1)
+    pos, col, _ = _bad_colour(orc, 5, 1, 77)
+    gmi.forward_batch(pos, col, 40, 30, 1.0, 3.0, ctx=actx)
+    good, gcol, _ = orc.synth_batch(6, 3, 500, 3, 40, 30)
+    gmi.forward_batch(good, gcol, 40, 30, 1.0, 3.0, ctx=actx)
+    with pytest.raises(gmi.GmiError) as e:
+        actx.synchronize()
+    assert e.value.name == "ColorOutOfRange"
+    assert "index 77" in str(e.value) and "image 1" in str(e.value)
+    # reported once: nothing pending afterwards (no stale slots re-reported)
+    actx.synchronize()
+    gmi.forward_batch(good, gcol, 40, 30, 1.0, 3.0, ctx=actx)
+    actx.synchronize()
+
+
+def test_async_error_is_the_first_of_several(gmi, orc):
+    actx = gmi.Context(0)
+    actx.set_flags(1)
+    good, gcol, _ = orc.synth_batch(8, 1, 500, 3, 40, 30)
+    gmi.forward_batch(good, gcol, 40, 30, 1.0, 3.0, ctx=actx)
+    pos, col, _ = _bad_colour(orc, 9, 0, 311)
+    gmi.forward_batch(pos, col, 40, 30, 1.0, 3.0, ctx=actx)
+    pos2, col2, _ = orc.synth_batch(10, 2, 500, 3, 40, 30)
+    pos2[1, 12, 0] = np.nan
+    gmi.forward_batch(pos2, col2, 40, 30, 1.0, 3.0, ctx=actx)
+    with pytest.raises(gmi.GmiError) as e:
+        actx.synchronize()
+    assert e.value.name == "ColorOutOfRange" and "index 311" in str(e.value)
+    actx.synchronize()
+
+
+def test_sync_context_reports_per_call_and_leaves_nothing_pending(gmi, orc):
+    sctx = gmi.Context(0)
+    pos, col, _ = _bad_colour(orc, 12, 0, 3)
+    with pytest.raises(gmi.GmiError):
+        gmi.forward_batch(pos, col, 40, 30, 1.0, 3.0, ctx=sctx)
+    sctx.synchronize()  # already reported by the call itself
+
+
+def test_cache_outlives_its_context(gmi, orc):
+    # a cache keeps its context (stream, device) alive: querying and freeing
+    # it after the caller dropped the context handle is valid
+    pos, col, up = orc.synth_batch(13, 1, 2000, 3, 64, 48)
+    c1 = gmi.Context(0)
+    img, cache = gmi.forward_batch(pos, col, 64, 48, 1.0, 3.0, ctx=c1)
+    norm0, flag0, _ = cache.pixels()
+    c1.close()
+    norm1, flag1, _ = cache.pixels()
+    assert np.array_equal(norm0, norm1) and np.array_equal(flag0, flag1)
+    assert cache.fallback_count == int(flag0.sum())
+    cache.close()
+    # the device is still usable by a fresh context
+    c2 = gmi.Context(0)
+    img2, cache2 = gmi.forward_batch(pos, col, 64, 48, 1.0, 3.0, ctx=c2)
+    assert np.array_equal(img, img2)
+
+
+@pytest.mark.parametrize("offset", [1, 3])
+def test_device_pointers_at_odd_element_offsets(gmi, ctx, orc, offset):
+    # upstream / image views at an odd float offset: results equal the
+    # aligned call bit for bit (no misaligned 64-bit loads)
+    torch = pytest.importorskip("torch")
+    w, h = 64, 40
+    pos, col, up = orc.synth_batch(14, 1, 1500, 3, w, h)
+    img, cache = gmi.forward_batch(pos, col, w, h, 1.0, 3.0, ctx=ctx)
+    dc, dp = gmi.backward_batch(pos, col, cache, up, 1.0, 3.0, ctx=ctx)
+    n = h * w * 3
+    tpos = torch.from_numpy(pos).cuda()
+    tcol = torch.from_numpy(col).cuda()
+    img_store = torch.zeros(n + offset, device="cuda")
+    up_store = torch.zeros(n + offset, device="cuda")
+    timg = img_store[offset:].view(1, h, w, 3)
+    tup = up_store[offset:].view(1, h, w, 3)
+    tup.copy_(torch.from_numpy(up).cuda())
+    torch.cuda.synchronize()
+    out, dcache = gmi.forward_cuda(tpos, tcol, w, h, 1.0, radius=3.0, image=timg, ctx=ctx)
+    ctx.synchronize()
+    assert np.array_equal(timg.cpu().numpy(), img)
+    ddc, ddp = gmi.backward_cuda(tpos, tcol, dcache, tup, 1.0, radius=3.0, ctx=ctx)
+    ctx.synchronize()
+    assert np.array_equal(ddc.numpy(), dc) and np.array_equal(ddp.numpy(), dp)

@@ -19,3 +19,24 @@ def test_cxx_api_program(gmi, tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "cxx api ok" in r.stdout
+
+
+def test_reference_callers_on_the_dropin():
+    """The reference's own callers of the hot path (oracle.cpp, validate.cpp,
+    optimize.cpp, imaging.cpp — unmodified) compiled against
+    include/gmi_dropin and linked with libgmi_b200_cxx.so instead of the
+    reference's core/bin_grid/engine.cpp (oracle/Makefile `dropin`), running
+    acceptance.cpp's criteria 1, 3, 4, 5 with the reference's seeds at the
+    fp32 tolerance, and the reference's optimize_points loop."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "gmi_acceptance_dropin")
+    if not os.path.exists(exe):
+        if os.path.isdir("/root/reference/proj/src"):
+            subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "dropin"], check=True)
+        else:
+            pytest.skip("drop-in acceptance binary not built (needs the reference sources)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    for k in (1, 3, 4, 5):
+        assert f"[PASS] criterion {k}:" in r.stdout
+    assert "[PASS] caller 8:" in r.stdout

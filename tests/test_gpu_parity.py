@@ -285,6 +285,52 @@ def test_band_split_matches_full_frame(gmi, ctx, orc):
     assert_close(g_pos, rdp, what="band d_positions")
 
 
+def test_band_fallbacks_match_full_frame(gmi, ctx, orc):
+    """Row bands at configs[3]'s density (0.25) and r = 3 with fallback
+    pixels whose nearest point lies beyond the default halo (the instance of
+    tests/test_multirank.py): the certified halo (dist.resolve_band_plan,
+    max over the bands) reproduces the full frame's nearest indices bit for
+    bit on the real kernels, and the routed gradients."""
+    from paper_2012_13257_b200 import dist as gdist
+    from test_multirank import _hole_instance
+
+    pos, col, up, W, H, sigma, cutoff = _hole_instance()
+    up = f32(up)
+    world = 2
+    r = orc.forward(pos, col, W, H, sigma, cutoff)
+    rdc, rdp = orc.backward(pos, col, r, up, sigma, cutoff)
+    want_near = np.where(r["fallback_flag"] == 1, r["nearest_index"], -1)
+
+    def probe(plan):
+        _, c = gmi.forward_batch(plan.local_positions(pos)[None], col[plan.idx][None], W,
+                                 plan.rows, sigma, cutoff, ctx=ctx)
+        _, flag, near = c.pixels()
+        fb = np.nonzero(flag[0].ravel())[0]
+        return fb, near[0].ravel()[fb]
+
+    halo = max(gdist.resolve_band_plan(pos, W, H, world, k, cutoff, probe).halo
+               for k in range(world))
+    assert halo > gdist.default_halo(cutoff)
+    g_col = np.zeros_like(rdc)
+    g_pos = np.zeros_like(rdp)
+    for k in range(world):
+        plan = gdist.BandPlan(pos, H, world, k, cutoff, halo)
+        bpos = plan.local_positions(pos)
+        bimg, bc = gmi.forward_batch(bpos[None], col[plan.idx][None], W, plan.rows, sigma, cutoff,
+                                     ctx=ctx)
+        _, flag, near = bc.pixels()
+        got = np.where(flag[0] == 1, plan.idx[np.maximum(near[0], 0)], -1)
+        assert np.array_equal(got, want_near[plan.r0:plan.r1]), f"band {k} nearest indices"
+        assert_close(bimg[0], r["image"][plan.r0:plan.r1], what=f"band {k} image")
+        dc, dp = gmi.backward_batch(bpos[None], col[plan.idx][None], bc,
+                                    up[plan.r0:plan.r1][None].astype(np.float32), sigma, cutoff,
+                                    ctx=ctx)
+        g_col[plan.idx] += dc[0]
+        g_pos[plan.idx] += dp[0]
+    assert_close(g_col, rdc, what="band d_colors")
+    assert_close(g_pos, rdp, what="band d_positions")
+
+
 @pytest.mark.parametrize("opt", [(True, False), (False, True), (True, True)])
 def test_optimize_points_matches_reference(gmi, ctx, opt):
     """optimize_points (optimize.cpp:47-98) on the device against the
