@@ -88,7 +88,14 @@ enum {
     /* Reserved, ignored: every path (forward, backward, fallback routing) is
      * bit-deterministic run to run; there is no faster non-deterministic
      * mode. */
-    GMI_CTX_NONDETERMINISTIC = 1u << 1
+    GMI_CTX_NONDETERMINISTIC = 1u << 1,
+    /* Reference-grade precision: weights, sums and the normalised image of
+     * the gradient in f64 (the path cutoff > 6 sigma always takes), for
+     * inputs where the fp32 hot path's d_positions / d_colors can exceed the
+     * 1e-6 absolute floor — isolated points at sigma < 1, disks of thousands
+     * of pixels, > ~10^4 contributors per pixel.  Slower
+     * (generic kernels); the image itself is returned in fp32. */
+    GMI_CTX_PRECISE = 1u << 2
 };
 
 typedef struct gmi_ctx gmi_ctx;     /* one device + one stream */

@@ -40,10 +40,14 @@ __all__ = [
     "forward_batch", "backward_batch", "Context", "bin_grid", "forward_counts",
     "default_context", "optimize_points", "gmm_benchmark", "ERROR_NAMES", "__version__",
     "load_point_set", "save_point_set", "load_image", "save_image",
-    "DeviceArray", "forward_cuda", "backward_cuda",
+    "DeviceArray", "forward_cuda", "backward_cuda", "CTX_ASYNC_ERRORS", "CTX_PRECISE",
 ]
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"
+
+# context flags (include/gmi_b200.h)
+CTX_ASYNC_ERRORS = 1   # errors reported by Context.synchronize()
+CTX_PRECISE = 4        # f64 weights, sums and image (reference-grade precision)
 
 # gmi::ErrorCode names (core.hpp:35-50), index = code - 1
 ERROR_NAMES = ["NonFiniteValue", "ColorOutOfRange", "EmptyPointSet", "ShapeMismatch",

@@ -47,6 +47,7 @@ struct BwdParams {
     int lpp;                // lanes per point (1, 2, 4, 8): rows split over lanes
     const float* wsum;      // [B][H][W]
     const float* image;     // [B][H][W][C]
+    const double* image64;  // [B][H][W][C] f64 image (precise mode) or null
     const float* upstream;  // [B][H][W][C]
     int B, N, C, W, H;
     int bs;                 // cells per block side
@@ -600,7 +601,9 @@ __global__ void k_backward_points_f64(BwdParams p, const double* __restrict__ ws
                 for (int c = 0; c < nch; ++c) {
                     const double u = p.upstream[pix * p.C + ch0 + c];
                     dcol[c] += u * ratio;
-                    dot += u * (cc[c] - static_cast<double>(p.image[pix * p.C + ch0 + c]));
+                    const double o = p.image64 ? p.image64[pix * p.C + ch0 + c]
+                                               : static_cast<double>(p.image[pix * p.C + ch0 + c]);
+                    dot += u * (cc[c] - o);
                 }
                 const double coef = ratio * dot;
                 gx += coef * (x - mx);
@@ -749,6 +752,7 @@ void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
     p.lpp = c->cutoff >= 6.0 ? 8 : 1;
     p.wsum = c->wsum;
     p.image = c->image;
+    p.image64 = c->image64;
     p.upstream = upstream;
     p.B = c->B;
     p.N = c->N;

@@ -255,8 +255,10 @@ int do_forward(gmi_ctx* ctx, const float* pos, const float* col, int B, int N,
     const size_t BHW = static_cast<size_t>(B) * c->H * c->W;
     c->wsum = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * BHW));
     // f64 weight mode beyond 6 sigma (see gmi_forward.cu)
-    if (cfg->cutoff_radius > 6.0 * cfg->sigma)
+    if (cfg->cutoff_radius > 6.0 * cfg->sigma || (ctx->flags & GMI_CTX_PRECISE)) {
         c->wsum64 = static_cast<double*>(gmi_host::cache_alloc(c, sizeof(double) * BHW));
+        c->image64 = static_cast<double*>(gmi_host::cache_alloc(c, sizeof(double) * BHW * C));
+    }
     c->special_cap = static_cast<int>(std::min<size_t>(BHW, size_t(1) << 22));
     c->special = static_cast<Special*>(gmi_host::cache_alloc(c, sizeof(Special) * c->special_cap));
     c->special_count_d = static_cast<int32_t*>(gmi_host::cache_alloc(c, sizeof(int32_t)));

@@ -42,6 +42,7 @@ struct FwdParams {
     float* image;       // [B][H][W][C]
     float* wsum;        // [B][H][W]
     double* wsum64;     // [B][H][W] (f64 weight mode only)
+    double* image64;    // [B][H][W][C] (f64 weight mode only)
     int32_t* counts;    // [B][H][W] or null
     Special* special;
     int32_t* special_count;
@@ -190,7 +191,11 @@ k_forward_tile(FwdParams p) {
     float* out = p.image + bp * p.C + ch0;
     if constexpr (kF64) {
         if (wsum64 > 0.0) {
-            for (int c = 0; c < nch; ++c) out[c] = static_cast<float>(num64[c] / wsum64);
+            for (int c = 0; c < nch; ++c) {
+                const double o64 = num64[c] / wsum64;
+                out[c] = static_cast<float>(o64);
+                if (p.image64) p.image64[bp * p.C + ch0 + c] = o64;
+            }
             if (cg == 0) {
                 p.wsum64[bp] = wsum64;
                 p.wsum[bp] = 1.0f;
@@ -412,6 +417,7 @@ static FwdParams fwd_params(const gmi_cache* c, float* image, int32_t* counts) {
     p.image = image;
     p.wsum = c->wsum;
     p.wsum64 = c->wsum64;
+    p.image64 = c->image64;
     p.counts = counts;
     p.special = c->special;
     p.special_count = c->special_count_d;

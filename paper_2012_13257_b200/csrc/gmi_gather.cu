@@ -68,6 +68,7 @@ struct SmemGather {
     int scan_w[kNW];
     int n_multi;
     int n_runs, cur_cy, cur_off, done, pre;
+    int fold_slot;                         // multi-chunk tiles: f64 fold slot (-1: none)
     int cx0, cx1, cy1;
     unsigned long long mbar;               // TMA completion barrier
 };
@@ -87,7 +88,14 @@ struct GatherParams {
     Special* special;
     int32_t* special_count;
     int special_cap;
+    // multi-chunk (clustered) tiles fold their fp32 sums into private f64
+    // totals at every chunk end: [slot][16][thread], slots from fold_count
+    double* fold;
+    int32_t* fold_count;
+    int fold_cap;
 };
+
+constexpr int kFoldVals = 16;  // W and up to 3 numerators x 4 pixels (C <= 3)
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
@@ -192,9 +200,28 @@ k_gather(GatherParams p) {
             S.cur_off = 0;
             S.done = one ? 1 : 0;
             if (!one) S.pre = 0;
+            int fs = -1;
+            if (!one && CC <= 3 && p.fold != nullptr) {
+                fs = atomicAdd(p.fold_count, 1);
+                if (fs >= p.fold_cap) fs = -1;
+            }
+            S.fold_slot = fs;
         }
     }
     __syncthreads();
+    // Clustered tiles (several chunks) sum thousands of candidates per pixel:
+    // a plain fp32 running sum drifts by ~sqrt(n/3) ulp.  Their threads fold
+    // the chunk's fp32 sums into private f64 totals at every chunk end, in
+    // chunk order (deterministic), and normalise in f64.
+    double* const fold = S.fold_slot >= 0
+                             ? p.fold + static_cast<size_t>(S.fold_slot) * kFoldVals * kNT + tid
+                             : nullptr;
+    bool folded = false;
+    auto fold_acc = [&](float& a, int k) {
+        double* f = fold + static_cast<size_t>(k) * kNT;
+        *f = (folded ? *f : 0.0) + static_cast<double>(a);
+        a = 0.f;
+    };
     while (true) {
         // ---- next chunk of runs (<= kRsMax runs, <= kCap candidates) ----
         if (tid == 0 && S.pre) {
@@ -499,6 +526,20 @@ k_gather(GatherParams p) {
                 }
             }
         }
+        if (fold != nullptr) {
+            fold_acc(Wa.x, 0);
+            fold_acc(Wa.y, 1);
+            fold_acc(Wb.x, 2);
+            fold_acc(Wb.y, 3);
+#pragma unroll
+            for (int c = 0; c < CC && c < 3; ++c) {
+                fold_acc(Na[c].x, 4 + 4 * c);
+                fold_acc(Na[c].y, 5 + 4 * c);
+                fold_acc(Nb[c].x, 6 + 4 * c);
+                fold_acc(Nb[c].y, 7 + 4 * c);
+            }
+            folded = true;
+        }
         // the last chunk needs no barrier: a warp that is done goes straight
         // to its epilogue instead of waiting for the CTA's longest window
         // (S.done was published before this chunk's first barrier)
@@ -512,6 +553,32 @@ k_gather(GatherParams p) {
         const float q0 = num * inv;
         return fmaf(fmaf(-q0, w, num), inv, q0);
     };
+    if (fold != nullptr && folded) {
+        // folded tile: W and out = num / W from the f64 totals
+#pragma unroll
+        for (int pk = 0; pk < 4; ++pk) {
+            const int py = pk >> 1, px = pk & 1;
+            const int qx = xa + px, qy = ya + py;
+            if (qx >= p.W || qy >= p.H) continue;
+            const double w64 = fold[static_cast<size_t>(pk) * kNT];
+            const size_t bp = (static_cast<size_t>(b) * p.H + qy) * p.W + qx;
+            float* out = p.image + bp * p.C;
+            if (w64 > 0.0) {
+#pragma unroll
+                for (int c = 0; c < CC; ++c)
+                    out[c] = static_cast<float>(fold[static_cast<size_t>(4 + 4 * c + pk) * kNT] / w64);
+                p.wsum[bp] = static_cast<float>(w64);
+                if (kCount) p.counts[bp] = py ? (px ? cnt11 : cnt10) : (px ? cnt01 : cnt00);
+            } else {
+                p.wsum[bp] = 0.f;
+                if (kCount) p.counts[bp] = 0;
+                const int slot = atomicAdd(p.special_count, 1);
+                if (slot < p.special_cap)
+                    p.special[slot] = Special{b, static_cast<int32_t>(qy * p.W + qx), -1, 1};
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int py = 0; py < 2; ++py) {
         const int qy = ya + py;
@@ -631,6 +698,15 @@ bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* count
     p.special_cap = c->special_cap;
     const dim3 grid((c->W + kTW - 1) / kTW, (c->H + kTH - 1) / kTH, c->B);
     GMI_CUDA(cudaMemsetAsync(c->special_count_d, 0, sizeof(int32_t), ctx->stream));
+    if (c->C <= 3) {
+        // f64 folds of multi-chunk (clustered) tiles: up to 1024 per call
+        // (128 KB each), slots handed out on the device
+        p.fold_cap = 1024;
+        char* f = static_cast<char*>(scratch(ctx, WS_FOLD, 256 + sizeof(double) * kFoldVals * kNT * p.fold_cap));
+        p.fold_count = reinterpret_cast<int32_t*>(f);
+        p.fold = reinterpret_cast<double*>(f + 256);
+        GMI_CUDA(cudaMemsetAsync(p.fold_count, 0, sizeof(int32_t), ctx->stream));
+    }
     const bool cnt = counts != nullptr;
     switch (c->C) {
         case 1: cnt ? launch_cc<1, true>(ctx, p, grid) : launch_cc<1, false>(ctx, p, grid); break;

@@ -83,11 +83,11 @@ struct gmi_ctx {
     double phase_ms[GMI_NUM_PHASES] = {0};
     uint64_t phase_calls[GMI_NUM_PHASES] = {0};
     // grow-only per-call scratch (stream-ordered reuse on the ctx stream)
-    void* ws_ptr[16] = {nullptr};
-    size_t ws_cap[16] = {0};
+    void* ws_ptr[24] = {nullptr};
+    size_t ws_cap[24] = {0};
     // host copies of small tables uploaded into scratch slots (upload_table)
-    std::vector<int32_t> ws_table[16];
-    void* ws_table_ptr[16] = {nullptr};
+    std::vector<int32_t> ws_table[24];
+    void* ws_table_ptr[24] = {nullptr};
     // scan tiles of the equal-segment (device geometry) binning, cached per
     // (batch, stride) so the hot path issues no host->device copy
     int eq_B = -1;
@@ -102,7 +102,7 @@ struct gmi_ctx {
 enum WsSlot {
     WS_BBOX = 0, WS_CELLID, WS_RANK, WS_TMP, WS_BIG, WS_BIGCOUNT, WS_TILES, WS_TSUM,
     WS_SEGOFF, WS_BLKOFF, WS_PART, WS_HOST_IN0, WS_HOST_IN1, WS_HOST_IN2,
-    WS_TILES_EQ, WS_SEGOFF_EQ, WS_COUNT
+    WS_TILES_EQ, WS_SEGOFF_EQ, WS_FOLD, WS_COUNT
 };
 
 // RAII phase marker: records an event pair on the ctx stream when profiling.
@@ -177,6 +177,7 @@ struct gmi_cache {
     // per pixel
     float* wsum = nullptr;    // [B][H][W]; 0 => special pixel
     double* wsum64 = nullptr; // [B][H][W] f64 normaliser (precise mode only)
+    double* image64 = nullptr;// [B][H][W][C] f64 image (precise mode: the backward's out)
     // special pixels
     Special* special = nullptr;
     int32_t* special_count_d = nullptr;

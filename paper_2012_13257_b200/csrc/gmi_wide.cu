@@ -78,6 +78,10 @@ struct GatherWideParams {
     const int32_t* heavy_list;   // heavy tiles (linear b * ty * tx index)
     const int32_t* heavy_count;
     const uint8_t* heavy_mark;   // per tile: 1 = processed from the heavy list
+    // f64 fold of the fp32 accumulators at every chunk end, for the first
+    // fold_cap heavy tiles: [heavy slot][pass][4 + 4 CB][thread]
+    double* fold;
+    int fold_cap;
     double r64, r2_64;
     float rhit2;         // (r + 1e-3)^2: conservative block test
     float nk, thr;
@@ -139,6 +143,22 @@ k_gather_wide(GatherWideParams p) {
         Nb[c] = f2(0.f, 0.f);
     }
     int cnt00 = 0, cnt01 = 0, cnt10 = 0, cnt11 = 0;
+    // Heavy (clustered) tiles sum tens of thousands of candidates per pixel:
+    // a plain fp32 running sum drifts by ~sqrt(n/3) ulp (configs[4]'s
+    // cluster: > 1e-5 relative).  Their lanes fold the fp32 accumulators of
+    // every chunk (<= kWCap candidates) into private f64 totals, in chunk
+    // order (deterministic), and normalise in f64.
+    double* const fold = (p.fold != nullptr && blockIdx.x < p.fold_cap &&
+                          static_cast<int>(blockIdx.x) < p.heavy_cap)
+                             ? p.fold + (static_cast<size_t>(blockIdx.x) * gridDim.y + sg) *
+                                            (4 + 4 * CB) * kWThreads + tid
+                             : nullptr;
+    bool folded = false;
+    auto fold_acc = [&](float& a, int k) {
+        double* f = fold + static_cast<size_t>(k) * kWThreads;
+        *f = (folded ? *f : 0.0) + static_cast<double>(a);
+        a = 0.f;
+    };
 
     // the tile's reference cell rectangle (bin_grid.cpp:88-91 for the tile)
     if (tid < 4) {
@@ -305,6 +325,20 @@ k_gather_wide(GatherWideParams p) {
                     }
                 }
             }
+            if (fold != nullptr) {
+                fold_acc(Wa.x, 0);
+                fold_acc(Wa.y, 1);
+                fold_acc(Wb.x, 2);
+                fold_acc(Wb.y, 3);
+#pragma unroll
+                for (int c = 0; c < CB; ++c) {
+                    fold_acc(Na[c].x, 4 + 4 * c);
+                    fold_acc(Na[c].y, 5 + 4 * c);
+                    fold_acc(Nb[c].x, 6 + 4 * c);
+                    fold_acc(Nb[c].y, 7 + 4 * c);
+                }
+                folded = true;
+            }
             __syncthreads();  // chunk consumed before the next staging
         }
     }
@@ -319,13 +353,24 @@ k_gather_wide(GatherWideParams p) {
         for (int px = 0; px < 2; ++px) {
             const int qx = xa + px, qy = ya + py;
             if (qx >= p.W || qy >= p.H) continue;
-            const float w = py ? (px ? Wb.y : Wb.x) : (px ? Wa.y : Wa.x);
+            float w = py ? (px ? Wb.y : Wb.x) : (px ? Wa.y : Wa.x);
             const size_t bp = (static_cast<size_t>(b) * p.H + qy) * p.W + qx;
+            const int pk = 2 * py + px;
+            double w64 = 0.0;
+            if (fold != nullptr && folded) {
+                w64 = fold[static_cast<size_t>(pk) * kWThreads];
+                w = static_cast<float>(w64);
+            }
             if (w > 0.f) {
                 const float inv = 1.0f / w;
                 float o[CB];
 #pragma unroll
                 for (int c = 0; c < CB; ++c) {
+                    if (fold != nullptr && folded) {
+                        o[c] = static_cast<float>(
+                            fold[static_cast<size_t>(4 + 4 * c + pk) * kWThreads] / w64);
+                        continue;
+                    }
                     const float num = py ? (px ? Nb[c].y : Nb[c].x) : (px ? Na[c].y : Na[c].x);
                     const float q0 = num * inv;
                     o[c] = fmaf(fmaf(-q0, w, num), inv, q0);
@@ -943,6 +988,10 @@ bool launch_gather_wide(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* count
         reinterpret_cast<uint8_t*>(ws + sizeof(int32_t) * (1 + p.heavy_cap)));
     GMI_LAUNCHED(ctx);
     const dim3 grid(p.heavy_cap + ntiles, p.nsg);
+    // f64 folds for up to 512 heavy tiles per call (~140 KB each at C = 64)
+    p.fold_cap = std::min(p.heavy_cap, 512);
+    p.fold = static_cast<double*>(scratch(ctx, WS_FOLD, sizeof(double) * p.fold_cap * p.nsg *
+                                                            (4 + 4 * cb) * kWThreads));
     GMI_CUDA(cudaMemsetAsync(c->special_count_d, 0, sizeof(int32_t), ctx->stream));
     const bool cnt = counts != nullptr;
     switch (cb) {

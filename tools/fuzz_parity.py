@@ -127,13 +127,17 @@ def main():
     ap.add_argument("--out", default="gpurun_out/fuzz_fail")
     ap.add_argument("--max-fail", type=int, default=400)
     ap.add_argument("--max-save", type=int, default=12)
+    ap.add_argument("--precise", action="store_true",
+                    help="contexts with GMI_CTX_PRECISE (f64 weights, sums and image)")
     a = ap.parse_args()
     import oracle
     import paper_2012_13257_b200 as gmi
     orc = oracle.Oracle()
     rng = np.random.default_rng(a.seed)
     sync_ctx, async_ctx = gmi.Context(0), gmi.Context(0)
-    async_ctx.set_flags(1)
+    extra = gmi.CTX_PRECISE if a.precise else 0
+    sync_ctx.set_flags(extra)
+    async_ctx.set_flags(gmi.CTX_ASYNC_ERRORS | extra)
     t_end = time.time() + a.seconds
     n_cases, n_images, worst, fails, saved = 0, 0, 0.0, 0, 0
     hist = {"image": 0, "d_colors": 0, "d_positions": 0, "exact": 0}
@@ -178,7 +182,8 @@ def main():
             print(f"{n_cases} cases, {n_images} images, {fails} failing, worst {worst:.2f}x "
                   f"({desc})", flush=True)
     verdict = "fuzz ok" if fails == 0 else "FUZZ FAILED"
-    print(f"{verdict} [{a.domain}{' large' if a.large else ''}, seed {a.seed}]: {n_cases} cases, "
+    mode = a.domain + (" large" if a.large else "") + (" precise" if a.precise else "")
+    print(f"{verdict} [{mode}, seed {a.seed}]: {n_cases} cases, "
           f"{n_images} images, {a.seconds:.0f} s, worst {worst:.2f}x tolerance, {fails} image(s) "
           f"over 1x (by output: {hist})")
     sys.exit(0 if fails == 0 else 1)
