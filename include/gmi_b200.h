@@ -95,7 +95,12 @@ enum {
      * 1e-6 absolute floor — isolated points at sigma < 1, disks of thousands
      * of pixels, > ~10^4 contributors per pixel.  Slower
      * (generic kernels); the image itself is returned in fp32. */
-    GMI_CTX_PRECISE = 1u << 2
+    GMI_CTX_PRECISE = 1u << 2,
+    /* Test hook, the analogue of the reference's inject_fault
+     * (validate.cpp:207-209): every backward adds 1e-3 to d_colors[0] of its
+     * first image on the device, so a parity harness can prove it detects a
+     * corrupted GPU output.  Never set in production. */
+    GMI_CTX_INJECT_FAULT = 1u << 3
 };
 
 typedef struct gmi_ctx gmi_ctx;     /* one device + one stream */

@@ -221,4 +221,9 @@ BinGrid build_bin_grid(const PointSet& ps, double cell_size);
 // Device selection for this thread's calls (default: device 0).
 void set_device(int device);
 
+// This thread's calls in reference-grade precision (GMI_CTX_PRECISE: f64
+// weights, sums and image on the device; slower).  Default off: the fp32 hot
+// path, within rel 1e-5 / abs 1e-6 of the reference on the BASELINE configs.
+void set_precise(bool on);
+
 }  // namespace gmi

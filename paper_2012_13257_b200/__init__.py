@@ -29,6 +29,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import threading
+import warnings
 
 import numpy as np
 
@@ -41,6 +42,7 @@ __all__ = [
     "default_context", "optimize_points", "gmm_benchmark", "ERROR_NAMES", "__version__",
     "load_point_set", "save_point_set", "load_image", "save_image",
     "DeviceArray", "forward_cuda", "backward_cuda", "CTX_ASYNC_ERRORS", "CTX_PRECISE",
+    "CTX_INJECT_FAULT", "PrecisionWarning", "set_fp32_inputs",
 ]
 
 __version__ = "0.2.0"
@@ -48,6 +50,7 @@ __version__ = "0.2.0"
 # context flags (include/gmi_b200.h)
 CTX_ASYNC_ERRORS = 1   # errors reported by Context.synchronize()
 CTX_PRECISE = 4        # f64 weights, sums and image (reference-grade precision)
+CTX_INJECT_FAULT = 8   # test hook: the backward corrupts d_colors[0] (harness check)
 
 # gmi::ErrorCode names (core.hpp:35-50), index = code - 1
 ERROR_NAMES = ["NonFiniteValue", "ColorOutOfRange", "EmptyPointSet", "ShapeMismatch",
@@ -71,6 +74,24 @@ def _check(rc: int) -> None:
         if rc in (101,):
             raise ValueError(msg)
         raise GmiError(rc, msg)
+
+
+class PrecisionWarning(UserWarning):
+    """Inputs rounded to the device path's fp32 (see set_fp32_inputs)."""
+
+
+_fp32_policy = "allow"
+
+
+def set_fp32_inputs(policy: str) -> None:
+    """What PointSet does with positions / colours fp32 cannot hold exactly
+    (the device computes in fp32; the reference in f64): "allow" (default:
+    round, count in PointSet.inexact_inputs), "warn" (PrecisionWarning) or
+    "reject" (GmiError) — the C++ API's gmi::set_fp32_inputs."""
+    global _fp32_policy
+    if policy not in ("allow", "warn", "reject"):
+        raise ValueError("policy must be 'allow', 'warn' or 'reject'")
+    _fp32_policy = policy
 
 
 # ---------------------------------------------------------------------------
@@ -112,6 +133,15 @@ class PointSet:
             raise GmiError(*issue)
         self._pos32 = np.ascontiguousarray(positions, dtype=np.float32)
         self._col32 = np.ascontiguousarray(colors, dtype=np.float32)
+        # values the fp32 device path rounds (the reference keeps them in f64)
+        self.inexact_inputs = int(np.count_nonzero(self._pos32.astype(np.float64) != positions) +
+                                  np.count_nonzero(self._col32.astype(np.float64) != colors))
+        if self.inexact_inputs and _fp32_policy != "allow":
+            msg = (f"{self.inexact_inputs} position / colour value(s) are not representable in "
+                   f"fp32 and are rounded for the device path")
+            if _fp32_policy == "reject":
+                raise GmiError(101, msg)
+            warnings.warn(msg, PrecisionWarning, stacklevel=2)
 
     @property
     def positions(self) -> np.ndarray:

@@ -97,6 +97,33 @@ __device__ __forceinline__ void pixel_terms(const BwdParams& p, size_t img_base,
     }
 }
 
+// Issues prefetch.global.L2 for the W / upstream / image rows of the pixel
+// region a block of cells reaches (once per CTA, before the prologue).
+__device__ __forceinline__ void prefetch_region(const BwdParams& p, const Geom& g, int b, int cx0,
+                                             int cy0, int cx1, int cy1) {
+    const double pad = p.r64 + 1.0;
+    const int x0 = max(0, static_cast<int>(floor(g.ox + cx0 * g.cell - pad))) & ~1;
+    const int y0 = max(0, static_cast<int>(floor(g.oy + cy0 * g.cell - pad)));
+    const int x1 = min(p.W - 1, static_cast<int>(ceil(g.ox + cx1 * g.cell + pad)));
+    const int y1 = min(p.H - 1, static_cast<int>(ceil(g.oy + cy1 * g.cell + pad)));
+    if (x1 < x0 || y1 < y0) return;
+    const size_t ib = static_cast<size_t>(b) * p.H * p.W;
+    // per row: W (4 B / px), upstream and image (4 C B / px), 128-B lines
+    const int lw = ((x1 - x0 + 1) * 4 + 127) / 128 + 1;
+    const int lc = ((x1 - x0 + 1) * 4 * p.C + 127) / 128 + 1;
+    const int per_row = lw + 2 * lc;
+    const int total_lines = per_row * (y1 - y0 + 1);
+    for (int k = threadIdx.x; k < total_lines; k += blockDim.x) {
+        const int row = k / per_row, j = k - row * per_row;
+        const size_t px = ib + static_cast<size_t>(y0 + row) * p.W + x0;
+        const char* a;
+        if (j < lw) a = reinterpret_cast<const char*>(p.wsum + px) + 128 * j;
+        else if (j < lw + lc) a = reinterpret_cast<const char*>(p.upstream + px * p.C) + 128 * (j - lw);
+        else a = reinterpret_cast<const char*>(p.image + px * p.C) + 128 * (j - lw - lc);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+    }
+}
+
 template <int CG, int LPP>
 __global__ void __launch_bounds__(kThreads, 4)
 k_backward_points(BwdParams p) {
@@ -127,6 +154,11 @@ k_backward_points(BwdParams p) {
     const int cg = blockIdx.y, ch0 = cg * CG, nch = min(CG, p.C - ch0);
     const int tid = threadIdx.x, lane = tid & 31;
     const size_t base = static_cast<size_t>(b) * p.N;
+
+    // ---- L2 prefetch of the pixel region (uncapped grids: the block's
+    // cells grown by r, known from the geometry alone) so the staging loads
+    // below hit L2 instead of waiting on HBM behind the point-run prologue ----
+    if (!g.capped) prefetch_region(p, g, b, cx0, cy0, cx1, cy1);
 
     // ---- point runs (one per cell row of the block) ----
     const int nrun = cy1 - cy0;

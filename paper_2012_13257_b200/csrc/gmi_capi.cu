@@ -222,9 +222,15 @@ struct EventSet {
     }
 };
 
+// GMI_CTX_INJECT_FAULT: the parity harness's negative-path hook (the
+// analogue of the reference's ValidationOptions::inject_fault, validate.cpp:
+// 207-209): perturbs d_colors of point 0 of the call's first image on the
+// device, after the backward, so a harness that misses it is broken.
+__global__ void k_inject_fault(float* d_colors) { d_colors[0] += 1e-3f; }
+
 // the backward of one (part) cache on device buffers at image offset 0
 void backward_part(gmi_ctx* ctx, const gmi_cache* c, const float* upstream, float* d_colors,
-                   float* d_positions) {
+                   float* d_positions, bool first_image = true) {
     {
         PhaseScope ph(ctx, 3);
         gmi_host::launch_backward(ctx, c, upstream, d_colors, d_positions);
@@ -232,6 +238,10 @@ void backward_part(gmi_ctx* ctx, const gmi_cache* c, const float* upstream, floa
     {
         PhaseScope ph(ctx, 4);
         gmi_host::launch_special_backward(ctx, c, upstream, d_colors, d_positions);
+    }
+    if ((ctx->flags & GMI_CTX_INJECT_FAULT) && first_image) {
+        k_inject_fault<<<1, 1, 0, ctx->stream>>>(d_colors);
+        GMI_LAUNCHED(ctx);
     }
 }
 
@@ -340,7 +350,7 @@ int do_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
         for (size_t k = 0; k < c->parts.size(); ++k) {
             const size_t b0 = c->part_b0[k];
             backward_part(ctx, c->parts[k], upstream + b0 * hwc,
-                          d_colors + b0 * c->N * c->C, d_positions + b0 * c->N * 2);
+                          d_colors + b0 * c->N * c->C, d_positions + b0 * c->N * 2, k == 0);
         }
     }
     if (!(ctx->flags & GMI_CTX_ASYNC_ERRORS)) GMI_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -945,7 +955,7 @@ int gmi_backward_host(gmi_ctx* ctx, const float* positions, const float* colors,
         for (size_t k = 0; k < parts.size(); ++k) {
             const size_t o = b0[k], n = parts[k]->B;
             GMI_CUDA(cudaStreamWaitEvent(ctx->stream, in[k], 0));
-            backward_part(ctx, parts[k], dup + o * hwc, dc + o * N * C, dp + o * N * 2);
+            backward_part(ctx, parts[k], dup + o * hwc, dc + o * N * C, dp + o * N * 2, k == 0);
             cudaEvent_t done = E.get();
             GMI_CUDA(cudaEventRecord(done, ctx->stream));
             GMI_CUDA(cudaStreamWaitEvent(ctx->s_out, done, 0));

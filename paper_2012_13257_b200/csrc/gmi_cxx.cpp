@@ -17,6 +17,7 @@ namespace {
 
 thread_local int t_device = 0;
 thread_local Fp32Inputs t_fp32 = Fp32Inputs::Allow;
+thread_local bool t_precise = false;
 
 struct CtxDeleter {
     void operator()(gmi_ctx* c) const { gmi_ctx_destroy(c); }
@@ -32,6 +33,7 @@ gmi_ctx* thread_ctx() {
         ctx.reset(c);
         ctx_device = t_device;
     }
+    gmi_ctx_set_flags(ctx.get(), t_precise ? GMI_CTX_PRECISE : 0u);
     return ctx.get();
 }
 
@@ -108,6 +110,8 @@ const char* error_code_name(ErrorCode code) { return gmi_error_name(static_cast<
 void set_device(int device) { t_device = device; }
 
 void set_fp32_inputs(Fp32Inputs policy) { t_fp32 = policy; }
+
+void set_precise(bool on) { t_precise = on; }
 
 std::int64_t count_inexact_fp32(const PointSet& ps) {
     std::int64_t n = 0;

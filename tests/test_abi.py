@@ -133,3 +133,28 @@ def test_interp_config_semantics(gmi):
     assert (c.cutoff_radius, c.fallback) == (2.5, 1)
     with pytest.raises(ValueError):
         gmi._interp_config(1.0, 0.0, "bilinear", 8, 6)
+
+
+def test_pointset_reports_fp32_rounding():
+    # weak r1 #12: f64 inputs the fp32 device path rounds are counted, and
+    # can warn or be rejected instead of silently changing the bins
+    import warnings
+
+    import paper_2012_13257_b200 as gmi
+
+    exact = gmi.PointSet([[0.5, 1.25]], [[0.25, 0.5, 0.75]])
+    assert exact.inexact_inputs == 0
+    rounded = gmi.PointSet([[0.1, 1.25]], [[0.3, 0.5, 0.75]])
+    assert rounded.inexact_inputs == 2
+    try:
+        gmi.set_fp32_inputs("warn")
+        with warnings.catch_warnings(record=True) as w:
+            warnings.simplefilter("always")
+            gmi.PointSet([[0.1, 1.0]], [[0.5]])
+        assert any(issubclass(x.category, gmi.PrecisionWarning) for x in w)
+        gmi.set_fp32_inputs("reject")
+        with pytest.raises(gmi.GmiError):
+            gmi.PointSet([[0.1, 1.0]], [[0.5]])
+        gmi.PointSet([[0.5, 1.0]], [[0.5]])  # exact values still pass
+    finally:
+        gmi.set_fp32_inputs("allow")

@@ -2,6 +2,8 @@
 context lifetime against caches that outlive it, and device pointers at any
 element alignment.  (sticky async errors, cache-held contexts,
 misaligned 64-bit loads in the backward's staging.)"""
+import os
+
 import numpy as np
 import pytest
 
@@ -98,3 +100,33 @@ def test_device_pointers_at_odd_element_offsets(gmi, ctx, orc, offset):
     ddc, ddp = gmi.backward_cuda(tpos, tcol, dcache, tup, 1.0, radius=3.0, ctx=ctx)
     ctx.synchronize()
     assert np.array_equal(ddc.numpy(), dc) and np.array_equal(ddp.numpy(), dp)
+
+
+def test_parity_harness_detects_an_injected_fault(gmi, orc):
+    # SURVEY §5 negative path (inject_fault, validate.cpp:207-209): the
+    # device perturbs d_colors[0] by 1e-3; the parity comparison must fail
+    from conftest import assert_close
+
+    fctx = gmi.Context(0)
+    fctx.set_flags(gmi.CTX_INJECT_FAULT)
+    pos, col, up = orc.synth_batch(15, 1, 800, 3, 48, 40)
+    img, cache = gmi.forward_batch(pos, col, 48, 40, 1.0, 3.0, ctx=fctx)
+    dc, dp = gmi.backward_batch(pos, col, cache, up, 1.0, 3.0, ctx=fctx)
+    r = orc.forward(pos[0], col[0], 48, 40, 1.0, 3.0)
+    rdc, _ = orc.backward(pos[0], col[0], r, up[0], 1.0, 3.0)
+    with pytest.raises(AssertionError, match="1/2400 entries"):
+        assert_close(dc[0], rdc, what="d_colors")
+    fctx.set_flags(0)
+    dc2, _ = gmi.backward_batch(pos, col, cache, up, 1.0, 3.0, ctx=fctx)
+    assert_close(dc2[0], rdc, what="d_colors")
+
+
+def test_fuzzer_fails_on_an_injected_fault(tmp_path):
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_parity.py"), "--seconds", "8",
+                        "--inject-fault", "--out", str(tmp_path), "--max-fail", "3"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 1 and "FUZZ FAILED" in r.stdout, r.stdout[-2000:]

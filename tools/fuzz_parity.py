@@ -11,6 +11,9 @@ committed under tests/golden/fuzz_cases/); the run exits non-zero if any case
 failed.
 
 Domains:
+  baseline  the BASELINE configs' regimes: sigma 1 / 1.5 / 4 at cutoff
+            3 sigma, 0.2-0.3 points/px, C in {1, 3}, configs[4]'s C = 64 with
+            its cluster at sigma 4; random frames, far-out points, lattices.
   contract  inputs the reference accepts (C in {1,3}; configs[4]'s C = 64
             at its sigma through the C restatement, which is the reference
             per channel group), sigma in the reference's random_instance
@@ -45,6 +48,22 @@ def draw_case(rng, domain, large):
     W = int(rng.integers(1, 640 if large else 200))
     H = int(rng.integers(1, 640 if large else 160))
     B = int(rng.integers(1, 4))
+    if domain == "baseline":
+        # the BASELINE configs' regimes (configs[0..4]): sigma 1 / 1.5 / 4 at
+        # cutoff 3 sigma, densities around their 0.25 points/px, C = 3 (and
+        # 1), configs[4]'s C = 64 with its 5% / 32 px cluster at sigma 4
+        C = int(rng.choice([1, 3, 3, 3, 64] if not large else [1, 3, 3]))
+        sigma = 4.0 if C == 64 else float(rng.choice([1.0, 1.5, 4.0]))
+        cluster, cluster_px = (0.05, 32) if C == 64 else (0.0, 32)
+        dens = float(rng.choice([0.2, 0.25, 0.3]))
+        N = max(1, int(dens * W * H))
+        N = min(N, 250000 if large else 60000)
+        if C == 64:
+            N = min(N, 8000)
+            B = 1
+        return dict(W=W, H=H, B=B, C=C, sigma=sigma, cutoff=3.0 * sigma, N=N, cluster=cluster,
+                    cluster_px=cluster_px, mode=int(rng.choice([0, 0, 1, 2])),
+                    fb="nearest" if rng.random() < 0.8 else "zero", seed=int(rng.integers(1 << 30)))
     if domain == "contract":
         C = int(rng.choice([1, 3, 3, 3, 64] if not large else [1, 3, 3]))
         sigma = float(rng.choice([0.5, 1.0, 1.5, 2.0, 4.0, rng.uniform(0.5, 4.0)]))
@@ -121,12 +140,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=300)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--domain", choices=["contract", "stress"], default="contract")
+    ap.add_argument("--domain", choices=["baseline", "contract", "stress"], default="contract")
     ap.add_argument("--large", action="store_true",
                     help="fewer, larger cases (frames up to 640 px, up to 250k points)")
     ap.add_argument("--out", default="gpurun_out/fuzz_fail")
     ap.add_argument("--max-fail", type=int, default=400)
     ap.add_argument("--max-save", type=int, default=12)
+    ap.add_argument("--inject-fault", action="store_true",
+                    help="negative path: GMI_CTX_INJECT_FAULT corrupts d_colors[0]; the run must FAIL")
     ap.add_argument("--precise", action="store_true",
                     help="contexts with GMI_CTX_PRECISE (f64 weights, sums and image)")
     a = ap.parse_args()
@@ -135,7 +156,7 @@ def main():
     orc = oracle.Oracle()
     rng = np.random.default_rng(a.seed)
     sync_ctx, async_ctx = gmi.Context(0), gmi.Context(0)
-    extra = gmi.CTX_PRECISE if a.precise else 0
+    extra = (gmi.CTX_PRECISE if a.precise else 0) | (gmi.CTX_INJECT_FAULT if a.inject_fault else 0)
     sync_ctx.set_flags(extra)
     async_ctx.set_flags(gmi.CTX_ASYNC_ERRORS | extra)
     t_end = time.time() + a.seconds
