@@ -56,5 +56,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB_SO
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """An experimental build of libgmi_b200.so with extra -D flags under
+    build/variants/<name>/ (loaded with GMI_LIBRARY=...; never the product)."""
+    out_dir = os.path.join(ROOT, "build", "variants", name)
+    os.makedirs(out_dir, exist_ok=True)
+    out = os.path.join(out_dir, "libgmi_b200.so")
+    srcs = [os.path.join(CSRC, s) for s in CU_SOURCES]
+    cmd = ["nvcc", *NVCC_FLAGS, *ARCH, "-shared", f"-I{INCLUDE}", f"-I{CSRC}",
+           *[f"-D{d}" for d in defines], *srcs, "-o", out]
+    subprocess.run(cmd, check=True)
+    return out
+
+
 if __name__ == "__main__":
     build(force=True, verbose=True)

@@ -10,12 +10,15 @@ import os
 
 from ._build import LIB_SO
 
-if not os.path.exists(LIB_SO):
+# GMI_LIBRARY: an alternative build of the same library (kernel variants
+# measured side by side, tools/ab_variants.sh); default the in-tree build
+_PATH = os.environ.get("GMI_LIBRARY") or LIB_SO
+if not os.path.exists(_PATH):
     raise ImportError(
-        f"{LIB_SO} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        f"{_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
         "(paper_2012_13257_b200 has no CPU fallback)")
 
-lib = C.CDLL(LIB_SO, mode=C.RTLD_GLOBAL)
+lib = C.CDLL(_PATH, mode=C.RTLD_GLOBAL)
 
 _vp = C.c_void_p
 _fp = C.POINTER(C.c_float)

@@ -37,7 +37,6 @@ constexpr int kRunMax = 64;             // cell rows per block
 struct BwdParams {
     const Geom* geom;
     const int32_t* bins;
-    const int32_t* blk_off;  // [B+1] CTA offsets per image
     const float* sx;
     const float* sy;
     const int32_t* sidx;
@@ -50,6 +49,7 @@ struct BwdParams {
     const double* image64;  // [B][H][W][C] f64 image (precise mode) or null
     const float* upstream;  // [B][H][W][C]
     int B, N, C, W, H;
+    int b0;                 // first image of this launch (grid z <= 65535)
     int bs;                 // cells per block side
     double r64, r2_64;
     float nk;               // -log2(e) / (2 sigma^2)
@@ -134,22 +134,14 @@ k_backward_points(BwdParams p) {
     __shared__ float s_red[4][kThreads / 32];
     __shared__ int s_region[5];
 
-    // ---- image / cell block of this CTA ----
-    int b = 0;
-    {
-        int lo = 0, hi = p.B;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (p.blk_off[mid] <= static_cast<int>(blockIdx.x)) lo = mid;
-            else hi = mid;
-        }
-        b = lo;
-    }
+    // ---- image / cell block of this CTA (grid: blocks x groups x images;
+    // blocks past this image's own grid exit at once) ----
+    const int b = p.b0 + static_cast<int>(blockIdx.z);
     const Geom g = p.geom[b];
-    const int local = blockIdx.x - p.blk_off[b];
+    const int local = blockIdx.x;
     const int nbx = (g.n_cols + p.bs - 1) / p.bs;
     const int cx0 = (local % nbx) * p.bs, cy0 = (local / nbx) * p.bs;
-    if (cy0 >= g.n_rows) return;  // past this image's grid (device geometry)
+    if (cy0 >= g.n_rows) return;
     const int cx1 = min(cx0 + p.bs, g.n_cols), cy1 = min(cy0 + p.bs, g.n_rows);
     const int cg = blockIdx.y, ch0 = cg * CG, nch = min(CG, p.C - ch0);
     const int tid = threadIdx.x, lane = tid & 31;
@@ -158,7 +150,9 @@ k_backward_points(BwdParams p) {
     // ---- L2 prefetch of the pixel region (uncapped grids: the block's
     // cells grown by r, known from the geometry alone) so the staging loads
     // below hit L2 instead of waiting on HBM behind the point-run prologue ----
+#ifndef GMI_BWD_NO_PREFETCH
     if (!g.capped) prefetch_region(p, g, b, cx0, cy0, cx1, cy1);
+#endif
 
     // ---- point runs (one per cell row of the block) ----
     const int nrun = cy1 - cy0;
@@ -727,8 +721,13 @@ template <int CG, int LPP>
 void launch_points_lpp(gmi_ctx* ctx, const BwdParams& p, int nblocks, int groups) {
     const int smem = kSmemBudget;
     GMI_SMEM_ONCE(ctx, (k_backward_points<CG, LPP>), smem);
-    k_backward_points<CG, LPP><<<dim3(nblocks, groups), kThreads, smem, ctx->stream>>>(p);
-    GMI_LAUNCHED(ctx);
+    for (int b0 = 0; b0 < p.B; b0 += 65535) {
+        BwdParams q = p;
+        q.b0 = b0;
+        const unsigned nz = static_cast<unsigned>(std::min(p.B - b0, 65535));
+        k_backward_points<CG, LPP><<<dim3(nblocks, groups, nz), kThreads, smem, ctx->stream>>>(q);
+        GMI_LAUNCHED(ctx);
+    }
 }
 
 template <int CG>
@@ -754,25 +753,20 @@ void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
     const double side_px = std::sqrt(static_cast<double>(kSmemBudget) / pix_bytes);
     int bs = static_cast<int>(std::floor((side_px - 2.0 * cell - 8.0) / cell));
     bs = std::max(1, std::min(bs, kRunMax));
-    std::vector<int32_t> off(c->B + 1, 0);
-    for (int b = 0; b < c->B; ++b) {
-        int nb;
-        if (c->geom_h.empty()) {
-            // device geometry: a grid of at most grid_cap^2 cells per image;
-            // CTAs past the image's actual grid exit at once
-            const int side = (c->grid_cap + bs - 1) / bs;
-            nb = side * side;
-        } else {
-            const auto& g = c->geom_h[b];
-            nb = ((g.n_cols + bs - 1) / bs) * ((g.n_rows + bs - 1) / bs);
-        }
-        off[b + 1] = off[b] + nb;
+    // CTAs per image: device geometry = a grid of at most grid_cap^2 cells;
+    // host geometry = the largest image's grid (smaller images' extra CTAs
+    // exit at once)
+    int nb_max = 0;
+    if (c->geom_h.empty()) {
+        const int side = (c->grid_cap + bs - 1) / bs;
+        nb_max = side * side;
+    } else {
+        for (const auto& g : c->geom_h)
+            nb_max = std::max(nb_max, ((g.n_cols + bs - 1) / bs) * ((g.n_rows + bs - 1) / bs));
     }
-    const int32_t* d_off = upload_table(ctx, WS_BLKOFF, off);
     BwdParams p{};
     p.geom = c->geom_d;
     p.bins = c->bins;
-    p.blk_off = d_off;
     p.sx = c->sx;
     p.sy = c->sy;
     p.sidx = c->sidx;
@@ -822,12 +816,12 @@ void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
         }
         return;
     }
-    if (off[c->B] > 0) {
+    if (nb_max > 0) {
         switch (CG) {
-            case 1: launch_points<1>(ctx, p, off[c->B], groups); break;
-            case 2: launch_points<2>(ctx, p, off[c->B], groups); break;
-            case 3: launch_points<3>(ctx, p, off[c->B], groups); break;
-            default: launch_points<4>(ctx, p, off[c->B], groups); break;
+            case 1: launch_points<1>(ctx, p, nb_max, groups); break;
+            case 2: launch_points<2>(ctx, p, nb_max, groups); break;
+            case 3: launch_points<3>(ctx, p, nb_max, groups); break;
+            default: launch_points<4>(ctx, p, nb_max, groups); break;
         }
     }
     if (groups > 1) {

@@ -66,6 +66,82 @@ __global__ void k_bbox_validate(const float2* __restrict__ pos, int N,
     }
 }
 
+// The same bbox + finiteness pass with 16-byte loads (two points each) and
+// 8 points per thread in flight, one block-level reduction and 4 atomics per
+// CTA (N even, positions 16-byte aligned).
+constexpr int kBboxPer = 4;  // float4 per thread
+
+__global__ void __launch_bounds__(256) k_bbox_validate4(const float4* __restrict__ pos, int N,
+                                                        uint32_t* __restrict__ bbox,
+                                                        unsigned long long* __restrict__ issue) {
+    __shared__ float red[4][8];
+    __shared__ unsigned long long red_bad[8];
+    const int b = blockIdx.y;
+    const int n2 = N >> 1;  // float4 per image
+    const float4* p = pos + static_cast<size_t>(b) * n2;
+    float mnx = INFINITY, mny = INFINITY, mxx = -INFINITY, mxy = -INFINITY;
+    unsigned long long bad = kNoIssue;
+    const int k0 = blockIdx.x * (blockDim.x * kBboxPer) + threadIdx.x;
+    float4 v[kBboxPer];
+#pragma unroll
+    for (int u = 0; u < kBboxPer; ++u) {
+        const int k = k0 + u * blockDim.x;
+        v[u] = k < n2 ? p[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < kBboxPer; ++u) {
+        const int k = k0 + u * blockDim.x;
+        if (k >= n2) continue;
+        const bool f0 = is_finite_f(v[u].x) && is_finite_f(v[u].y);
+        const bool f1 = is_finite_f(v[u].z) && is_finite_f(v[u].w);
+        if (!f0) bad = min(bad, (static_cast<unsigned long long>(2 * k) << 8) | 1ull);
+        else if (!f1) bad = min(bad, (static_cast<unsigned long long>(2 * k + 1) << 8) | 1ull);
+        if (f0) {
+            mnx = fminf(mnx, v[u].x);
+            mny = fminf(mny, v[u].y);
+            mxx = fmaxf(mxx, v[u].x);
+            mxy = fmaxf(mxy, v[u].y);
+        }
+        if (f1) {
+            mnx = fminf(mnx, v[u].z);
+            mny = fminf(mny, v[u].w);
+            mxx = fmaxf(mxx, v[u].z);
+            mxy = fmaxf(mxy, v[u].w);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mnx = fminf(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+        mny = fminf(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+        mxx = fmaxf(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+        mxy = fmaxf(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+        bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, o));
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red[0][w] = mnx;
+        red[1][w] = mny;
+        red[2][w] = mxx;
+        red[3][w] = mxy;
+        red_bad[w] = bad;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k) {
+            mnx = fminf(mnx, red[0][k]);
+            mny = fminf(mny, red[1][k]);
+            mxx = fmaxf(mxx, red[2][k]);
+            mxy = fmaxf(mxy, red[3][k]);
+            bad = min(bad, red_bad[k]);
+        }
+        uint32_t* bb = bbox + 4 * b;
+        atomicMin(bb + 0, f2ord(mnx));
+        atomicMin(bb + 1, f2ord(mny));
+        atomicMax(bb + 2, f2ord(mxx));
+        atomicMax(bb + 3, f2ord(mxy));
+        if (bad != kNoIssue) atomicMin(issue + b, bad);
+    }
+}
+
 __global__ void k_bbox_init(uint32_t* bbox, unsigned long long* issue, int B) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b < B) {
@@ -805,6 +881,14 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
     uint32_t* d_bbox = static_cast<uint32_t*>(scratch(ctx, WS_BBOX, sizeof(uint32_t) * 4 * B));
     k_bbox_init<<<(B + 127) / 128, 128, 0, st>>>(d_bbox, d_issue, B);
     GMI_LAUNCHED(ctx);
+#ifndef GMI_K1_BBOX_SCALAR
+    if ((N % 2) == 0 && (reinterpret_cast<uintptr_t>(pos) & 15) == 0) {
+        const int per_img = (N / 2 + 256 * kBboxPer - 1) / (256 * kBboxPer);
+        k_bbox_validate4<<<dim3(per_img, B), 256, 0, st>>>(reinterpret_cast<const float4*>(pos), N,
+                                                          d_bbox, d_issue);
+        GMI_LAUNCHED(ctx);
+    } else
+#endif
     {
         const int per_img = std::max(1, std::min((N + 1023) / 1024,
                                                  (4 * ctx->num_sms + B - 1) / B));
