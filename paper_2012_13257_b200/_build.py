@@ -56,10 +56,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB_SO
 
 
-def build_variant(name: str, defines: list[str]) -> str:
+def build_variant(name: str, defines: list[str], kind: str = "variants") -> str:
     """An experimental build of libgmi_b200.so with extra -D flags under
-    build/variants/<name>/ (loaded with GMI_LIBRARY=...; never the product)."""
-    out_dir = os.path.join(ROOT, "build", "variants", name)
+    build/<kind>/<name>/ (loaded with GMI_LIBRARY=...; never the product):
+    kind "variants" for A/B timing (tools/ab_variants.sh), "debug" for the
+    bounds-checked build (tools/gpu_bounds.sh)."""
+    out_dir = os.path.join(ROOT, "build", kind, name)
     os.makedirs(out_dir, exist_ok=True)
     out = os.path.join(out_dir, "libgmi_b200.so")
     srcs = [os.path.join(CSRC, s) for s in CU_SOURCES]

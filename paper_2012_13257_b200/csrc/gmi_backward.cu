@@ -97,33 +97,6 @@ __device__ __forceinline__ void pixel_terms(const BwdParams& p, size_t img_base,
     }
 }
 
-// Issues prefetch.global.L2 for the W / upstream / image rows of the pixel
-// region a block of cells reaches (once per CTA, before the prologue).
-__device__ __forceinline__ void prefetch_region(const BwdParams& p, const Geom& g, int b, int cx0,
-                                             int cy0, int cx1, int cy1) {
-    const double pad = p.r64 + 1.0;
-    const int x0 = max(0, static_cast<int>(floor(g.ox + cx0 * g.cell - pad))) & ~1;
-    const int y0 = max(0, static_cast<int>(floor(g.oy + cy0 * g.cell - pad)));
-    const int x1 = min(p.W - 1, static_cast<int>(ceil(g.ox + cx1 * g.cell + pad)));
-    const int y1 = min(p.H - 1, static_cast<int>(ceil(g.oy + cy1 * g.cell + pad)));
-    if (x1 < x0 || y1 < y0) return;
-    const size_t ib = static_cast<size_t>(b) * p.H * p.W;
-    // per row: W (4 B / px), upstream and image (4 C B / px), 128-B lines
-    const int lw = ((x1 - x0 + 1) * 4 + 127) / 128 + 1;
-    const int lc = ((x1 - x0 + 1) * 4 * p.C + 127) / 128 + 1;
-    const int per_row = lw + 2 * lc;
-    const int total_lines = per_row * (y1 - y0 + 1);
-    for (int k = threadIdx.x; k < total_lines; k += blockDim.x) {
-        const int row = k / per_row, j = k - row * per_row;
-        const size_t px = ib + static_cast<size_t>(y0 + row) * p.W + x0;
-        const char* a;
-        if (j < lw) a = reinterpret_cast<const char*>(p.wsum + px) + 128 * j;
-        else if (j < lw + lc) a = reinterpret_cast<const char*>(p.upstream + px * p.C) + 128 * (j - lw);
-        else a = reinterpret_cast<const char*>(p.image + px * p.C) + 128 * (j - lw - lc);
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-    }
-}
-
 template <int CG, int LPP>
 __global__ void __launch_bounds__(kThreads, 4)
 k_backward_points(BwdParams p) {
@@ -146,13 +119,6 @@ k_backward_points(BwdParams p) {
     const int cg = blockIdx.y, ch0 = cg * CG, nch = min(CG, p.C - ch0);
     const int tid = threadIdx.x, lane = tid & 31;
     const size_t base = static_cast<size_t>(b) * p.N;
-
-    // ---- L2 prefetch of the pixel region (uncapped grids: the block's
-    // cells grown by r, known from the geometry alone) so the staging loads
-    // below hit L2 instead of waiting on HBM behind the point-run prologue ----
-#ifndef GMI_BWD_NO_PREFETCH
-    if (!g.capped) prefetch_region(p, g, b, cx0, cy0, cx1, cy1);
-#endif
 
     // ---- point runs (one per cell row of the block) ----
     const int nrun = cy1 - cy0;
@@ -190,7 +156,9 @@ k_backward_points(BwdParams p) {
             if (s_run[mid] <= k) lo = mid;
             else hi = mid;
         }
-        return s_rung[lo] + (k - s_run[lo]);
+        const int s = s_rung[lo] + (k - s_run[lo]);
+        GMI_CHECK(s >= 0 && s < p.N);
+        return s;
     };
 
     // ---- pixel region reached by the block's points ----
@@ -374,7 +342,10 @@ k_backward_points(BwdParams p) {
             // slot-major planes (16-byte stride: conflict-light LDS.128)
 #pragma unroll
             for (int j = 0; j < L::kF4; ++j)
+            {
+                GMI_CHECK(k >= 0 && k < area);
                 s_pair[j * area + k] = make_float4(e[2 * j].x, e[2 * j].y, e[2 * j + 1].x, e[2 * j + 1].y);
+            }
         }
         __syncthreads();
     }
@@ -531,6 +502,8 @@ k_backward_points(BwdParams p) {
             const float2 ey2 = f2(ey, ey), mmx = f2(-mx, -mx);
             float2 gyr2 = f2(0.f, 0.f), gx2 = f2(0.f, 0.f);
             const float4* pr = s_pair + (y - ry0) * npairs + ((xs - rx0) >> 1);
+            GMI_CHECK(y >= ry0 && xs >= rx0 && (y - ry0) * npairs + ((xs - rx0) >> 1) + np <= area &&
+                      area * L::kF4 * static_cast<int>(sizeof(float4)) <= kSmemBudget);
 #pragma unroll 1
             for (int j = 0; j < np; ++j) {
                 float4 q4[L::kF4];
@@ -573,6 +546,7 @@ k_backward_points(BwdParams p) {
             gy += __shfl_xor_sync(0xffffffffu, gy, o);
         }
         if (!live || sub != 0) continue;
+        GMI_CHECK(i >= 0 && i < p.N);
         for (int c = 0; c < nch; ++c) p.d_col[(base + i) * p.C + ch0 + c] = dcs[c];
         float* dp = p.d_pos + (static_cast<size_t>(cg) * p.B * p.N + base + i) * 2;
         dp[0] = static_cast<float>(gxs * static_cast<double>(inv_s2));

@@ -560,6 +560,7 @@ __global__ void __launch_bounds__(256) k_scatter_emit(ScatterEmitParams p) {
             const int cx = cell_of_fast(static_cast<double>(v[u].x), g.ox, g.cell, inv, g.n_cols);
             const int cy = cell_of_fast(static_cast<double>(v[u].y), g.oy, g.cell, inv, g.n_rows);
             dst[u] = atomicSub(p.bins + g.bin_off + cy * g.n_cols + cx, 1) - 1;  // bin_grid.cpp:67
+            GMI_CHECK(dst[u] >= 0 && dst[u] < p.N);
         }
     }
 #pragma unroll

@@ -11,6 +11,25 @@
 
 #define GMI_HD __host__ __device__ __forceinline__
 
+// Device-side bounds checks for a debug build (-DGMI_DEBUG_BOUNDS, built by
+// tools/gpu_bounds.sh as a variant library): every shared / global index of
+// the hot kernels' staging, lists and scatters is checked and a violation
+// traps with its location.  Compiled out of the product build.
+#ifdef GMI_DEBUG_BOUNDS
+#include <cstdio>
+#define GMI_CHECK(cond)                                                          \
+    do {                                                                         \
+        if (!(cond)) {                                                           \
+            printf("GMI_CHECK failed %s:%d: %s (block %d,%d,%d thread %d)\n",     \
+                   __FILE__, __LINE__, #cond, blockIdx.x, blockIdx.y, blockIdx.z, \
+                   threadIdx.x);                                                 \
+            __trap();                                                            \
+        }                                                                        \
+    } while (0)
+#else
+#define GMI_CHECK(cond) do { } while (0)
+#endif
+
 namespace gmi_dev {
 
 // ----------------------------------------------------------------------------

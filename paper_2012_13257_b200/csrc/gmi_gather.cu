@@ -289,6 +289,7 @@ k_gather(GatherParams p) {
             __syncwarp();
             if (lane < n_runs) {
                 const int rb = S.run_beg[lane], len = S.run_beg[lane + 1] - rb;
+                GMI_CHECK(rb >= 0 && len >= 0 && rb + len <= kCap);
                 if (len > 0)
                     asm volatile(
                         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -327,6 +328,7 @@ k_gather(GatherParams p) {
                        static_cast<double>(my) >= ylo - 1.0 && static_cast<double>(my) <= yhi + 1.0) {
                 key = nbins;  // the flag bin
             }
+            GMI_CHECK(key <= nbins && nbins + 1 < kBinMax + 2);
             if (key >= 0) atomicAdd(&S.bin[key], 1);
             S.key[k] = key;
         }
@@ -372,6 +374,7 @@ k_gather(GatherParams p) {
             const int key = S.key[k];
             if (key < 0) continue;
             const int pos = atomicSub(&S.bin[key], 1) - 1;
+            GMI_CHECK(pos >= 0 && pos < kCap);
             const float4 ra = S.u.R[2 * k];
             const float4 rb = S.u.R[2 * k + 1];
             S.A[pos] = ra;
@@ -434,6 +437,7 @@ k_gather(GatherParams p) {
 #pragma unroll
             for (int j = 0; j < kCpl; ++j) {
                 const int q = c0 + j;
+                GMI_CHECK(q >= c1 || (q <= kColMax && at + pl[j] <= kCap));
                 if (q < c1) S.v.wcs[warp][q] = static_cast<uint16_t>(at);
                 for (int e = 0; e < pl[j]; ++e) wl[at + e] = static_cast<uint16_t>(ps[j] + e);
                 at += pl[j];
@@ -451,6 +455,7 @@ k_gather(GatherParams p) {
 #pragma unroll 2
             for (int t = ts; t < te; ++t) {
                 const int kc = kn;
+                GMI_CHECK(kc >= 0 && kc < kCap && t < kCap);
                 kn = lst[t + 1 < te ? t + 1 : t];
                 const float4 a = S.A[kc];
                 const float2 bcur = CC > 2 ? S.Bc[kc] : f2(0.f, 0.f);

@@ -231,6 +231,7 @@ k_gather_wide(GatherWideParams p) {
                     blk += c;
                 }
                 const int pos = n + woff + __popc(bal & ((1u << lane) - 1u));
+                GMI_CHECK(!keep || pos >= 0);
                 if (keep && pos < kWCap) {
                     S.pt[pos] = pt;
                     S.slot[pos] = slot;
@@ -277,6 +278,7 @@ k_gather_wide(GatherWideParams p) {
                 unsigned m = __ballot_sync(0xffffffffu, hit);
                 while (m) {
                     const int k = kb + __ffs(m) - 1;
+                    GMI_CHECK(k >= 0 && k < n && n <= kWCap);
                     m &= m - 1;
                     const float4 t = S.pt[k];
                     const float2 dx = __fadd2_rn(X, f2(-t.x, -t.x));
