@@ -33,6 +33,10 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kSmemBudget = 52 * 1024;  // staged pixel bytes per CTA (4 CTAs/SM)
 constexpr int kRunMax = 64;             // cell rows per block
+#ifndef GMI_BWD_STAGE_UNROLL
+#define GMI_BWD_STAGE_UNROLL 2
+#endif
+constexpr int kStageUnroll = GMI_BWD_STAGE_UNROLL;  // staging pairs in flight per lane
 
 struct BwdParams {
     const Geom* geom;
@@ -280,7 +284,7 @@ k_backward_points(BwdParams p) {
         // rows by warps, pixel pairs by lanes (coalesced, no index division)
         const int nrows = ry1 - ry0 + 1;
         for (int row = tid >> 5; row < nrows; row += kThreads / 32)
-#pragma unroll 2
+#pragma unroll kStageUnroll
         for (int pp = lane; pp < npairs; pp += 32) {
             const int k = row * npairs + pp, yy = ry0 + row;
             const int xa = rx0 + 2 * pp;

@@ -532,7 +532,10 @@ struct ScatterEmitParams {
     float rf, r2f;
 };
 
-constexpr int kEmitPer = 4;
+#ifndef GMI_K1_EMIT_PER
+#define GMI_K1_EMIT_PER 4
+#endif
+constexpr int kEmitPer = GMI_K1_EMIT_PER;
 
 __global__ void __launch_bounds__(256) k_scatter_emit(ScatterEmitParams p) {
     const int b = blockIdx.y;

@@ -4,6 +4,7 @@
 // plus a thread-local message.
 #include <algorithm>
 #include <chrono>
+#include <thread>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
@@ -107,6 +108,90 @@ int collect_issue(gmi_ctx* ctx, int B) {
     return GMI_OK;
 }
 
+// ---- pageable host buffers ----------------------------------------------
+// cudaMemcpyAsync from / to pageable memory runs through the driver's own
+// bounce buffers one piece at a time (~6 GB/s here).  The host API instead
+// stages pageable buffers through two 64 MB pinned slots of the context:
+// host threads copy piece k+1 into one slot while the DMA of piece k runs
+// from the other.
+constexpr size_t kStageSlot = size_t(64) << 20;
+
+bool is_pageable(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+void parallel_memcpy(void* dst, const void* src, size_t n) {
+    const size_t kPer = size_t(8) << 20;
+    const int hw = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+    const int nt = static_cast<int>(std::min<size_t>(hw, (n + kPer - 1) / kPer));
+    if (nt <= 1) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    const size_t step = ((n + nt - 1) / nt + 63) & ~size_t(63);
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) {
+        const size_t a = std::min(n, t * step), b = std::min(n, (t + 1) * step);
+        if (b > a)
+            th.emplace_back([=] {
+                std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+            });
+    }
+    std::memcpy(dst, src, std::min(n, step));
+    for (auto& t : th) t.join();
+}
+
+void ensure_staging(gmi_ctx* ctx) {
+    for (int s = 0; s < 2; ++s) {
+        if (ctx->stg_slot[s] == nullptr) GMI_CUDA(cudaMallocHost(&ctx->stg_slot[s], kStageSlot));
+        if (ctx->stg_ev[s] == nullptr)
+            GMI_CUDA(cudaEventCreateWithFlags(&ctx->stg_ev[s], cudaEventDisableTiming));
+    }
+}
+
+// host (pageable) -> device, queued on `st`; returns with the last DMA queued
+void h2d_staged(gmi_ctx* ctx, void* dst, const void* src, size_t n, cudaStream_t st) {
+    ensure_staging(ctx);
+    int s = 0;
+    for (size_t off = 0; off < n; off += kStageSlot, s ^= 1) {
+        const size_t m = std::min(kStageSlot, n - off);
+        GMI_CUDA(cudaEventSynchronize(ctx->stg_ev[s]));  // the slot's previous DMA is done
+        parallel_memcpy(ctx->stg_slot[s], static_cast<const char*>(src) + off, m);
+        GMI_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, ctx->stg_slot[s], m,
+                                 cudaMemcpyHostToDevice, st));
+        GMI_CUDA(cudaEventRecord(ctx->stg_ev[s], st));
+    }
+}
+
+// device -> host (pageable) after the work queued on `st`; returns complete
+void d2h_staged(gmi_ctx* ctx, void* dst, const void* src, size_t n, cudaStream_t st) {
+    ensure_staging(ctx);
+    size_t prev_off = 0, prev_m = 0;
+    int s = 0;
+    for (size_t off = 0; off < n; off += kStageSlot, s ^= 1) {
+        const size_t m = std::min(kStageSlot, n - off);
+        GMI_CUDA(cudaEventSynchronize(ctx->stg_ev[s]));
+        GMI_CUDA(cudaMemcpyAsync(ctx->stg_slot[s], static_cast<const char*>(src) + off, m,
+                                 cudaMemcpyDeviceToHost, st));
+        GMI_CUDA(cudaEventRecord(ctx->stg_ev[s], st));
+        if (prev_m) {  // the other slot's piece is down: copy it out while this one comes
+            GMI_CUDA(cudaEventSynchronize(ctx->stg_ev[s ^ 1]));
+            parallel_memcpy(static_cast<char*>(dst) + prev_off, ctx->stg_slot[s ^ 1], prev_m);
+        }
+        prev_off = off;
+        prev_m = m;
+    }
+    if (prev_m) {
+        GMI_CUDA(cudaEventSynchronize(ctx->stg_ev[s ^ 1]));
+        parallel_memcpy(static_cast<char*>(dst) + prev_off, ctx->stg_slot[s ^ 1], prev_m);
+    }
+}
+
 // The ctx stream waits for the copy streams of the host-buffer API.
 void join_copy_streams(gmi_ctx* ctx) {
     for (cudaStream_t cs : {ctx->s_in, ctx->s_out}) {
@@ -172,6 +257,10 @@ void ctx_teardown(gmi_ctx* ctx) {
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
     if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
+    for (int s = 0; s < 2; ++s) {
+        if (ctx->stg_slot[s]) cudaFreeHost(ctx->stg_slot[s]);
+        if (ctx->stg_ev[s]) cudaEventDestroy(ctx->stg_ev[s]);
+    }
     delete ctx;
 }
 
@@ -783,6 +872,44 @@ int gmi_backward(gmi_ctx* ctx, const float* positions, const float* colors, int3
     });
 }
 
+// gmi_forward_host on PAGEABLE host buffers: inputs staged up through the
+// pinned slots, the whole batch in one device forward, the image staged
+// down; complete on return.
+int forward_host_pageable(gmi_ctx* ctx, const float* positions, const float* colors, int batch,
+                          int num_points, int channels, const gmi_config* cfg, float* image,
+                          gmi_cache** cache_out) {
+    auto* c = new gmi_cache();
+    c->ctx = ctx;
+    c->holds_ctx = true;
+    ctx_retain(ctx);
+    const size_t N = num_points, C = channels;
+    const size_t hwc = static_cast<size_t>(cfg->height) * cfg->width * C;
+    int rc = GMI_OK;
+    try {
+        float* dpos = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * batch * N * 2));
+        float* dcol = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * batch * N * C));
+        float* dimg = static_cast<float*>(gmi_host::cache_alloc(c, sizeof(float) * batch * hwc));
+        h2d_staged(ctx, dpos, positions, sizeof(float) * batch * N * 2, ctx->stream);
+        h2d_staged(ctx, dcol, colors, sizeof(float) * batch * N * C, ctx->stream);
+        rc = do_forward(ctx, dpos, dcol, batch, num_points, channels, cfg, dimg, c, nullptr);
+        if (rc == GMI_OK) d2h_staged(ctx, image, dimg, sizeof(float) * batch * hwc, ctx->stream);
+    } catch (...) {
+        cudaStreamSynchronize(ctx->stream);
+        free_cache_buffers(c);
+        delete c;
+        ctx_release(ctx);
+        throw;
+    }
+    if (rc != GMI_OK) {
+        free_cache_buffers(c);
+        delete c;
+        ctx_release(ctx);
+        return rc;
+    }
+    *cache_out = c;
+    return GMI_OK;
+}
+
 int gmi_forward_host(gmi_ctx* ctx, const float* positions, const float* colors, int32_t batch,
                      int32_t num_points, int32_t channels, const gmi_config* cfg, float* image,
                      gmi_cache** cache_out) {
@@ -797,6 +924,9 @@ int gmi_forward_host(gmi_ctx* ctx, const float* positions, const float* colors, 
         rc = check_config(cfg);
         if (rc) return rc;
         GMI_CUDA(cudaSetDevice(ctx->device));
+        if (is_pageable(positions) || is_pageable(colors) || is_pageable(image))
+            return forward_host_pageable(ctx, positions, colors, batch, num_points, channels, cfg,
+                                         image, cache_out);
         ensure_copy_streams(ctx);
         ensure_issue(ctx, batch);
         auto* c = new gmi_cache();
@@ -923,9 +1053,24 @@ int gmi_backward_host(gmi_ctx* ctx, const float* positions, const float* colors,
         rc = backward_checks(cache, batch, num_points, channels, cfg);
         if (rc) return rc;
         GMI_CUDA(cudaSetDevice(ctx->device));
-        ensure_copy_streams(ctx);
         const size_t N = num_points, C = channels;
         const size_t hwc = static_cast<size_t>(cfg->height) * cfg->width * C;
+        if (is_pageable(upstream) || is_pageable(d_colors) || is_pageable(d_positions)) {
+            // pageable buffers: staged through the pinned slots (the result
+            // is complete on return)
+            float* dup = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * batch * hwc));
+            float* dc = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * batch * N * C));
+            float* dp = static_cast<float*>(gmi_host::dalloc(ctx, sizeof(float) * batch * N * 2));
+            h2d_staged(ctx, dup, upstream, sizeof(float) * batch * hwc, ctx->stream);
+            do_backward(ctx, cache, dup, dc, dp);
+            d2h_staged(ctx, d_colors, dc, sizeof(float) * batch * N * C, ctx->stream);
+            d2h_staged(ctx, d_positions, dp, sizeof(float) * batch * N * 2, ctx->stream);
+            gmi_host::dfree(ctx, dup);
+            gmi_host::dfree(ctx, dc);
+            gmi_host::dfree(ctx, dp);
+            return GMI_OK;
+        }
+        ensure_copy_streams(ctx);
         std::vector<const gmi_cache*> parts;
         std::vector<int> b0;
         if (cache->parts.empty()) {

@@ -45,6 +45,10 @@ constexpr int kRsMax = 32;         // cell-row runs per chunk
 constexpr int kColMax = 128;       // 1-px columns across the tile's reach
 constexpr int kBinMax = 2048;      // (column, row-pair) bins (+1 flag bin)
 constexpr int kMultiCap = kNW * (kColMax + 1);  // multi-bin list, shares wcs
+#ifndef GMI_GATHER_UNROLL
+#define GMI_GATHER_UNROLL 2
+#endif
+constexpr int kLoopUnroll = GMI_GATHER_UNROLL;  // candidate loop unroll
 
 template <int CC>
 struct SmemGather {
@@ -452,7 +456,7 @@ k_gather(GatherParams p) {
             const uint16_t* lst = S.u.wl[warp];
             // list entry of the next candidate fetched one iteration ahead
             int kn = ts < te ? lst[ts] : 0;
-#pragma unroll 2
+#pragma unroll kLoopUnroll
             for (int t = ts; t < te; ++t) {
                 const int kc = kn;
                 GMI_CHECK(kc >= 0 && kc < kCap && t < kCap);

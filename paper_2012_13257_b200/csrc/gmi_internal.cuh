@@ -96,6 +96,10 @@ struct gmi_ctx {
     // copy streams of the pipelined host-buffer API (created on first use)
     cudaStream_t s_in = nullptr;
     cudaStream_t s_out = nullptr;
+    // pinned staging of PAGEABLE host buffers (host API): two slots copied
+    // by a few host threads while the other slot's DMA runs
+    void* stg_slot[2] = {nullptr, nullptr};
+    cudaEvent_t stg_ev[2] = {nullptr, nullptr};
 };
 
 // scratch slots

@@ -130,3 +130,44 @@ def test_fuzzer_fails_on_an_injected_fault(tmp_path):
                         "--inject-fault", "--out", str(tmp_path), "--max-fail", "3"],
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 1 and "FUZZ FAILED" in r.stdout, r.stdout[-2000:]
+
+
+def test_pinned_and_pageable_host_buffers_agree(gmi, orc):
+    # the host API takes two routes: all-pinned buffers run the chunked
+    # three-stream pipeline (composite cache), pageable ones are staged
+    # through the context's pinned slots; results are bit-identical, and a
+    # cache made by either route serves a backward on either route
+    import ctypes as C
+
+    torch = pytest.importorskip("torch")
+    B, N, Cc, W, H = 5, 3000, 3, 96, 80
+    pos, col, up = orc.synth_batch(16, B, N, Cc, W, H)
+    ctx = gmi.Context(0)
+    img_a, cache_a = gmi.forward_batch(pos, col, W, H, 1.5, 4.5, ctx=ctx)   # pageable
+    dc_a, dp_a = gmi.backward_batch(pos, col, cache_a, up, 1.5, 4.5, ctx=ctx)
+
+    def pinned(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+
+    ppos, pcol, pup = pinned(pos), pinned(col), pinned(up)
+    pimg, pdc, pdp = pinned(np.zeros_like(img_a)), pinned(np.zeros_like(dc_a)), pinned(np.zeros_like(dp_a))
+    fp = C.POINTER(C.c_float)
+    cfg = gmi._lib.GmiConfig(1.5, 4.5, 0, W, H)
+    h = C.c_void_p()
+    gmi._check(gmi.lib.gmi_forward_host(ctx.handle, ppos.ctypes.data_as(fp), pcol.ctypes.data_as(fp), B, N,
+                                        Cc, C.byref(cfg), pimg.ctypes.data_as(fp), C.byref(h)))
+    cache_b = gmi.ForwardCache(h, ctx)
+    gmi._check(gmi.lib.gmi_backward_host(ctx.handle, ppos.ctypes.data_as(fp), pcol.ctypes.data_as(fp), B, N,
+                                         Cc, C.byref(cfg), cache_b.handle, pup.ctypes.data_as(fp),
+                                         pdc.ctypes.data_as(fp), pdp.ctypes.data_as(fp)))
+    assert np.array_equal(img_a, pimg)
+    assert np.array_equal(dc_a, pdc) and np.array_equal(dp_a, pdp)
+    # the pinned route's composite cache with a pageable backward
+    dc_c, dp_c = gmi.backward_batch(pos, col, cache_b, up, 1.5, 4.5, ctx=ctx)
+    assert np.array_equal(dc_a, dc_c) and np.array_equal(dp_a, dp_c)
+    # the pageable route's cache with a pinned backward
+    pdc[:] = 0
+    gmi._check(gmi.lib.gmi_backward_host(ctx.handle, ppos.ctypes.data_as(fp), pcol.ctypes.data_as(fp), B, N,
+                                         Cc, C.byref(cfg), cache_a.handle, pup.ctypes.data_as(fp),
+                                         pdc.ctypes.data_as(fp), pdp.ctypes.data_as(fp)))
+    assert np.array_equal(dc_a, pdc)
