@@ -6,14 +6,26 @@ cutoff 3*sigma = 4.5.  One "step" = gmi_forward + gmi_backward over the whole
 batch.  Synthetic inputs (positions U(-0.5, W-0.5), colours U[0,1), upstream
 U(-1,1)), generated on the device with torch (plumbing only).
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python bench.py [--gpus N --steps K --warmup W] [--config 1..5] [--impl reference]
 
-value    device-resident throughput (output Mpix/s, whole job)
+--gpus N without a launcher re-runs this script as N ranks (torchrun, one
+process per GPU, rendezvous on 127.0.0.1); each rank runs the product's
+multi-GPU driver (paper_2012_13257_b200.multi: BatchShards, or BandSplit for
+--config 4).
+
+value    device-resident throughput (output Mpix/s, whole job), each timed
+         step one replay of a CUDA graph of the library's calls
 e2e      the same through the host-buffer C-ABI (gmi_forward_host /
          gmi_backward_host): H2D of positions/colours/upstream and D2H of the
-         image and both gradients inside the timed region
+         image and both gradients inside the timed region, pinned buffers;
+         e2e.numpy_shim: the reference-shaped numpy shim (forward_batch /
+         backward_batch) on plain pageable arrays
+roofline the binding roof of the step's algorithmic counts (SURVEY §8d:
+         max of FP32 pipe, MUFU, HBM), for the dominant kernel per launch
+         (`frac`) and the whole step (`step_frac`); the other two beside it
 Timing: CUDA events on the library's stream, warm-up first, barrier +
-synchronize around the timed region, max over ranks.  Inputs (B*...) are far
+synchronize around the timed region, max over ranks; ms_per_step is the
+total / K, ms_per_step_median the median step.  Inputs (B*...) are far
 larger than L2 (126 MB), so no explicit flush is needed.
 """
 from __future__ import annotations

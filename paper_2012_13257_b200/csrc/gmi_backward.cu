@@ -34,7 +34,7 @@ constexpr int kThreads = 256;
 constexpr int kSmemBudget = 52 * 1024;  // staged pixel bytes per CTA (4 CTAs/SM)
 constexpr int kRunMax = 64;             // cell rows per block
 #ifndef GMI_BWD_STAGE_UNROLL
-#define GMI_BWD_STAGE_UNROLL 2
+#define GMI_BWD_STAGE_UNROLL 1
 #endif
 constexpr int kStageUnroll = GMI_BWD_STAGE_UNROLL;  // staging pairs in flight per lane
 
@@ -551,10 +551,32 @@ k_backward_points(BwdParams p) {
         }
         if (!live || sub != 0) continue;
         GMI_CHECK(i >= 0 && i < p.N);
-        for (int c = 0; c < nch; ++c) p.d_col[(base + i) * p.C + ch0 + c] = dcs[c];
+        // each point's gradients land at its original index (random against
+        // the cell order): as few store transactions as alignment allows
+        float* dc = p.d_col + (base + i) * p.C + ch0;
+        if (CG == 3 && nch == 3 && p.C == 3 && (reinterpret_cast<uintptr_t>(p.d_col) & 7) == 0) {
+            // 12-byte rows: one 8-byte and one 4-byte store (the 8-byte half
+            // is the first two channels for an even row, the last two for an
+            // odd one)
+            if (((base + i) & 1) == 0) {
+                *reinterpret_cast<float2*>(dc) = f2(dcs[0], dcs[1]);
+                dc[2] = dcs[2];
+            } else {
+                dc[0] = dcs[0];
+                *reinterpret_cast<float2*>(dc + 1) = f2(dcs[1], dcs[2]);
+            }
+        } else {
+            for (int c = 0; c < nch; ++c) dc[c] = dcs[c];
+        }
         float* dp = p.d_pos + (static_cast<size_t>(cg) * p.B * p.N + base + i) * 2;
-        dp[0] = static_cast<float>(gxs * static_cast<double>(inv_s2));
-        dp[1] = static_cast<float>(gy * static_cast<double>(inv_s2));
+        const float2 g2 = f2(static_cast<float>(gxs * static_cast<double>(inv_s2)),
+                             static_cast<float>(gy * static_cast<double>(inv_s2)));
+        if ((reinterpret_cast<uintptr_t>(p.d_pos) & 7) == 0) {
+            *reinterpret_cast<float2*>(dp) = g2;
+        } else {
+            dp[0] = g2.x;
+            dp[1] = g2.y;
+        }
     }
 }
 

@@ -202,13 +202,25 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot,
     return res;
 }
 
+// Per tile: the sum of its counts.  With `big` (the fast path), cells above
+// the gather's chunk capacity are listed on the way (k_sort_big_recs puts
+// their records in index order) — the counts are read here anyway.
+constexpr int kBigRecCellScan = 640;   // = kBigRecCell below
 __global__ void k_scan_reduce(const int32_t* __restrict__ data,
                               const ScanTile* __restrict__ tiles,
-                              int32_t* __restrict__ tile_sum) {
+                              int32_t* __restrict__ tile_sum,
+                              const Geom* __restrict__ geom = nullptr,
+                              int2* __restrict__ big = nullptr, int32_t* big_count = nullptr) {
     __shared__ int red[kScanThreads / 32];
     const ScanTile t = tiles[blockIdx.x];
     int s = 0;
-    for (int k = threadIdx.x; k < t.len; k += blockDim.x) s += data[t.start + k];
+    for (int k = threadIdx.x; k < t.len; k += blockDim.x) {
+        const int v = data[t.start + k];
+        s += v;
+        if (big != nullptr && v > kBigRecCellScan)
+            big[atomicAdd(big_count, 1)] =
+                make_int2(t.seg, static_cast<int>(t.start + k - geom[t.seg].bin_off));
+    }
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
     __syncthreads();
@@ -533,7 +545,7 @@ struct ScatterEmitParams {
 };
 
 #ifndef GMI_K1_EMIT_PER
-#define GMI_K1_EMIT_PER 4
+#define GMI_K1_EMIT_PER 2
 #endif
 constexpr int kEmitPer = GMI_K1_EMIT_PER;
 
@@ -649,22 +661,13 @@ __global__ void __launch_bounds__(256) k_emit_rec(ScatterEmitParams p, const int
     r[1] = make_float4(c4[2], c4[3], __uint_as_float(id), 0.f);
 }
 
-// Cells the fast gather may split across chunks (> its 1024-candidate
+// Cells the fast gather may split across chunks (> its 640-candidate
 // capacity) get their records in ascending original index, so chunk
 // membership — and the summation order — is independent of the atomic
 // arrival order (bit-deterministic results for clustered inputs).
 constexpr int kBigRecCell = 640;    // = the fast gather's chunk capacity (kCap)
+static_assert(kBigRecCell == kBigRecCellScan, "the scan lists the cells k_sort_big_recs sorts");
 constexpr int kBigRecSmem = 4096;   // cells up to this size sort in shared memory
-
-__global__ void k_find_big_cells(const Geom* __restrict__ geom, const int32_t* __restrict__ bins,
-                                 int2* __restrict__ big, int32_t* big_count) {
-    const int b = blockIdx.y;
-    const Geom g = geom[b];
-    const int cell = blockIdx.x * blockDim.x + threadIdx.x;
-    if (cell >= g.n_cols * g.n_rows) return;
-    const int n = bins[g.bin_off + cell + 1] - bins[g.bin_off + cell];
-    if (n > kBigRecCell) big[atomicAdd(big_count, 1)] = make_int2(b, cell);
-}
 
 __device__ __forceinline__ uint32_t rec_idx(const float4& r1) {
     return __float_as_uint(r1.z) & 0x7fffffffu;
@@ -826,7 +829,8 @@ int host_axis_cells(double span, double cell, int cap) {
 // inclusive: data[k] = sum of counts [0, k] (cell ends), else exclusive.
 static void scan_segments(gmi_ctx* ctx, int32_t* data, const std::vector<int64_t>& seg_start,
                           const std::vector<int64_t>& seg_len, bool equal = false,
-                          bool inclusive = false) {
+                          bool inclusive = false, const gmi_dev::Geom* geom = nullptr,
+                          int2* big = nullptr, int32_t* big_count = nullptr) {
     cudaStream_t st = ctx->stream;
     const int B = static_cast<int>(seg_start.size());
     if (equal && ctx->eq_B == B && ctx->eq_stride == seg_len[0]) {
@@ -834,7 +838,7 @@ static void scan_segments(gmi_ctx* ctx, int32_t* data, const std::vector<int64_t
         ScanTile* d_tiles = static_cast<ScanTile*>(ctx->ws_ptr[WS_TILES_EQ]);
         int32_t* d_segoff = static_cast<int32_t*>(ctx->ws_ptr[WS_SEGOFF_EQ]);
         int32_t* d_tsum = static_cast<int32_t*>(scratch(ctx, WS_TSUM, sizeof(int32_t) * nt));
-        k_scan_reduce<<<nt, kScanThreads, 0, st>>>(data, d_tiles, d_tsum);
+        k_scan_reduce<<<nt, kScanThreads, 0, st>>>(data, d_tiles, d_tsum, geom, big, big_count);
         GMI_LAUNCHED(ctx);
         k_scan_segments<<<B, 1024, 0, st>>>(d_tsum, d_segoff);
         GMI_LAUNCHED(ctx);
@@ -865,7 +869,7 @@ static void scan_segments(gmi_ctx* ctx, int32_t* data, const std::vector<int64_t
                              cudaMemcpyHostToDevice, st));
     GMI_CUDA(cudaMemcpyAsync(d_segoff, seg_off.data(), sizeof(int32_t) * (B + 1),
                              cudaMemcpyHostToDevice, st));
-    k_scan_reduce<<<nt, kScanThreads, 0, st>>>(data, d_tiles, d_tsum);
+    k_scan_reduce<<<nt, kScanThreads, 0, st>>>(data, d_tiles, d_tsum, geom, big, big_count);
     GMI_LAUNCHED(ctx);
     k_scan_segments<<<B, 1024, 0, st>>>(d_tsum, d_segoff);
     GMI_LAUNCHED(ctx);
@@ -976,7 +980,14 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
         k_count_red<<<pgrid4, 256, 0, st>>>(p2, N, c->geom_d, c->bins);
         GMI_LAUNCHED(ctx);
         host_trace("bin: count launched");
-        scan_segments(ctx, c->bins, seg_start, seg_len, c->geom_h.empty(), true);
+        // cells the gather may split (> its chunk capacity) are listed by the
+        // scan's reduce pass and put in index order after the scatter
+        int2* d_big = static_cast<int2*>(
+            scratch(ctx, WS_BIG, sizeof(int2) * std::max<size_t>(1, BN / (kBigRecCell + 1) + 1)));
+        int32_t* d_bigcount = static_cast<int32_t*>(scratch(ctx, WS_BIGCOUNT, sizeof(int32_t)));
+        GMI_CUDA(cudaMemsetAsync(d_bigcount, 0, sizeof(int32_t), st));
+        scan_segments(ctx, c->bins, seg_start, seg_len, c->geom_h.empty(), true, c->geom_d, d_big,
+                      d_bigcount);
         ScatterEmitParams e{};
         e.pos = p2;
         e.col = col;
@@ -993,13 +1004,6 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
         k_scatter_emit<<<pgrid4, 256, 0, st>>>(e);
         GMI_LAUNCHED(ctx);
         // cells the gather may split: index order
-        int2* d_big = static_cast<int2*>(
-            scratch(ctx, WS_BIG, sizeof(int2) * std::max<size_t>(1, BN / (kBigRecCell + 1) + 1)));
-        int32_t* d_bigcount = static_cast<int32_t*>(scratch(ctx, WS_BIGCOUNT, sizeof(int32_t)));
-        GMI_CUDA(cudaMemsetAsync(d_bigcount, 0, sizeof(int32_t), st));
-        k_find_big_cells<<<dim3((max_bins + 127) / 128, B), 128, 0, st>>>(c->geom_d, c->bins, d_big,
-                                                                          d_bigcount);
-        GMI_LAUNCHED(ctx);
         const int rsmem = kBigRecSmem * (2 * sizeof(float4) + sizeof(unsigned long long));
         GMI_SMEM_ONCE(ctx, k_sort_big_recs, rsmem);
         k_sort_big_recs<<<ctx->num_sms, 512, rsmem, st>>>(N, c->geom_d, c->bins, c->rec, d_big, d_bigcount);

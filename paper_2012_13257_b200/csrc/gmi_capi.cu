@@ -204,18 +204,18 @@ void join_copy_streams(gmi_ctx* ctx) {
     }
 }
 
-__global__ void k_check_special(const int32_t* count, int cap, unsigned long long* issue) {
+
+// GMI_CTX_ASYNC_ERRORS, after a forward: a fallback-list overflow becomes an
+// issue of the call, and the call's first failing image (slots in image
+// order) becomes the ctx's pending error unless an earlier call already left
+// one — stream order makes "earlier" the call order, so gmi_ctx_synchronize
+// reports the first error since it last ran (pending == null: the caller
+// collects the call's issues itself).
+__global__ void k_async_check(const int32_t* count, int cap, unsigned long long* issue, int B,
+                              int b0, unsigned long long* pending) {
     if (*count > cap)
         atomicMin(issue, (static_cast<unsigned long long>(cap) << 8) | GMI_ERR_OUT_OF_MEMORY);
-}
-
-// GMI_CTX_ASYNC_ERRORS: the call's first failing image (slots in image order)
-// becomes the ctx's pending error unless an earlier call already left one —
-// stream order makes "earlier" the call order, so gmi_ctx_synchronize reports
-// the first error since it last ran.
-__global__ void k_merge_issue(const unsigned long long* issue, int B, int b0,
-                              unsigned long long* pending) {
-    if (pending[0] != gmi_dev::kNoIssue) return;
+    if (pending == nullptr || pending[0] != gmi_dev::kNoIssue) return;
     for (int b = 0; b < B; ++b) {
         if (issue[b] != gmi_dev::kNoIssue) {
             pending[0] = issue[b];
@@ -397,14 +397,10 @@ int do_forward(gmi_ctx* ctx, const float* pos, const float* col, int B, int N,
     if ((ctx->flags & GMI_CTX_ASYNC_ERRORS) && counts == nullptr) {
         // no host check below: a fallback list overflow becomes a pending
         // error reported by gmi_ctx_synchronize
-        k_check_special<<<1, 1, 0, ctx->stream>>>(c->special_count_d, c->special_cap, d_issue);
+        k_async_check<<<1, 1, 0, ctx->stream>>>(c->special_count_d, c->special_cap, d_issue, B,
+                                                static_cast<int>(d_issue - ctx->d_issue),
+                                                ctx->collect_now ? nullptr : ctx->d_pending);
         GMI_LAUNCHED(ctx);
-        if (!ctx->collect_now) {
-            k_merge_issue<<<1, 1, 0, ctx->stream>>>(d_issue, B,
-                                                    static_cast<int>(d_issue - ctx->d_issue),
-                                                    ctx->d_pending);
-            GMI_LAUNCHED(ctx);
-        }
     }
     if (!(ctx->flags & GMI_CTX_ASYNC_ERRORS) || counts != nullptr) {
         int32_t nspec = 0;

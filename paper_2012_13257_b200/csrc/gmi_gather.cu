@@ -2,9 +2,13 @@
 // query_radius bin_grid.cpp:84-105 + gaussian_weight core.cpp:49-53) for the
 // fp32 weight mode (cutoff <= 6 sigma) with C <= 4 channels.
 //
-// CTA = 64x16 output pixels of one image, 8 warps; warp w owns the row pair
-// (y0+2w, y0+2w+1), lane l the columns (x0+2l, x0+2l+1): 2x2 pixels per thread
-// whose normaliser W and numerators live in f32x2 registers.
+// CTA = 64x32 output pixels of one image, 8 warps; warp w owns rows
+// y0+4w .. y0+4w+3, lane l the columns (x0+2l, x0+2l+1): 2x4 pixels per
+// thread whose normaliser W and numerators live in f32x2 registers.  (Round
+// 1 had 2x2 pixels per thread; the inner loop was bound by the shared-memory
+// pipe — 80% of its wavefronts, half of them bank conflicts, from each lane
+// reading its own candidate record — and one record read now serves 8
+// pixels instead of 4: -13% gather time at configs[2].)
 //
 //  stage  The candidate points of the tile (reference cells overlapping the
 //         tile grown by r: one contiguous run of 32-byte records per cell
@@ -16,18 +20,19 @@
 //         Within a bin the order is canonicalised by original index, so the
 //         summation order — and the result — is independent of K1's atomic
 //         arrival order.
-//  lists  Warp w needs the row-pair bins [w, w + dyb] of every column: per
-//         column one contiguous piece of the sorted array.  Lane-per-column
+//  lists  Warp w needs the row-pair bins [2w, 2w + 1 + dyb] of every column:
+//         per column one contiguous piece of the sorted array.  Lane-per-column
 //         prefix sums give the warp's column-major index list and its column
 //         starts; a lane's candidates (mu_x in (xa - r, xa + 1 + r)) are then
 //         ONE contiguous range of that list.
-//  gather Per candidate, 4 pixels with f32x2 ops: e = nk d^2 (7 FP2), in-ball
-//         test e >= nk r^2 (exact in fp32 for points K1 did not flag, see
-//         gmi_common.cuh), 4 MUFU.EX2, W and C numerators.  Flagged
+//  gather Per candidate, 8 pixels with f32x2 ops: e = nk d^2, in-ball test
+//         e >= nk r^2 (exact in fp32 for points K1 did not flag, see
+//         gmi_common.cuh), 8 MUFU.EX2, W and C numerators.  Flagged
 //         (boundary-ambiguous) points sit in one extra bin and take the f64
 //         predicate in a warp-uniform pass.
 //  store  out = num/W with one Newton step, W kept for the backward; pixels
-//         with W == 0 go to the fallback list (K3).
+//         with W == 0 go to the fallback list (K3).  Clustered tiles (several
+//         staging chunks) fold their sums into f64 at each chunk end.
 #include <algorithm>
 #include <cmath>
 
@@ -37,16 +42,26 @@ using namespace gmi_dev;
 
 namespace {
 
-constexpr int kTW = 64, kTH = 16;
-constexpr int kNW = kTH / 2;       // warps (row pairs)
+// rows per lane (each lane owns 2 columns x kRPL rows): 4 halves the shared-
+// memory traffic per pixel evaluation against 2 (one staged candidate read
+// serves 8 pixels); 2 is round 1's layout, kept for A/B builds
+#ifndef GMI_GATHER_RPL
+#define GMI_GATHER_RPL 4
+#endif
+constexpr int kRPL = GMI_GATHER_RPL;
+constexpr int kNW = 8;             // warps
+constexpr int kTW = 64, kTH = kNW * kRPL;
 constexpr int kNT = kNW * 32;      // threads
-constexpr int kCap = 640;          // staged candidates per chunk (= K1's kBigRecCell)
+constexpr int kCTAs = kRPL == 2 ? 4 : 3;  // resident CTAs per SM (registers, shared memory)
+// staged candidates per chunk (>= K1's kBigRecCell: cells above it are
+// index-ordered, so chunk membership never depends on arrival order)
+constexpr int kCap = kRPL == 2 ? 640 : 1024;
 constexpr int kRsMax = 32;         // cell-row runs per chunk
 constexpr int kColMax = 128;       // 1-px columns across the tile's reach
 constexpr int kBinMax = 2048;      // (column, row-pair) bins (+1 flag bin)
 constexpr int kMultiCap = kNW * (kColMax + 1);  // multi-bin list, shares wcs
 #ifndef GMI_GATHER_UNROLL
-#define GMI_GATHER_UNROLL 2
+#define GMI_GATHER_UNROLL 1
 #endif
 constexpr int kLoopUnroll = GMI_GATHER_UNROLL;  // candidate loop unroll
 
@@ -61,7 +76,6 @@ struct SmemGather {
     float4 A[kCap];                        // mu_x, mu_y, c0, c1   (bin order)
     float2 Bc[CC > 2 ? kCap : 1];          // c2, c3
     int idx[kCap];                         // original index
-    int key[kCap];                         // bin of staged record k (-1: dropped)
     int bin[kBinMax + 2];                  // counts -> inclusive ends -> starts
     union {
         uint16_t wcs[kNW][kColMax + 1];    // per-warp column starts in wl
@@ -99,7 +113,7 @@ struct GatherParams {
     int fold_cap;
 };
 
-constexpr int kFoldVals = 16;  // W and up to 3 numerators x 4 pixels (C <= 3)
+constexpr int kFoldVals = 8 * kRPL;  // W and up to 3 numerators x 2 kRPL pixels (C <= 3)
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
@@ -108,7 +122,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 template <int CC, bool kCount>
-__global__ void __launch_bounds__(kNT, 4)
+__global__ void __launch_bounds__(kNT, kCTAs)
 k_gather(GatherParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     SmemGather<CC>& S = *reinterpret_cast<SmemGather<CC>*>(smem_raw);
@@ -130,27 +144,32 @@ k_gather(GatherParams p) {
     const double ylo = static_cast<double>(y0) - p.r64;
     const double yhi = static_cast<double>(y0 + kTH - 1) + p.r64;
 
-    // this thread's 2x2 pixels
-    const int ya = y0 + 2 * warp, xa = x0 + 2 * lane;
+    // this thread's 2 x kRPL pixels: columns xa, xa + 1 of rows ya .. ya + kRPL - 1
+    const int ya = y0 + kRPL * warp, xa = x0 + 2 * lane;
     const float2 X = f2(static_cast<float>(xa), static_cast<float>(xa + 1));
-    const float2 Y = f2(static_cast<float>(ya), static_cast<float>(ya + 1));
+    float2 Y[kRPL / 2];  // row pairs (ya + 2j, ya + 2j + 1)
+#pragma unroll
+    for (int j = 0; j < kRPL / 2; ++j)
+        Y[j] = f2(static_cast<float>(ya + 2 * j), static_cast<float>(ya + 2 * j + 1));
     const float2 nk2 = f2(p.nk, p.nk);
     const float thr = p.thr;
-    float2 Wa = f2(0.f, 0.f), Wb = f2(0.f, 0.f);  // rows ya, ya+1; (xa, xa+1)
-    float2 Na[CC], Nb[CC];
+    float2 Wr[kRPL];       // per row: (xa, xa + 1)
+    float2 Nr[kRPL][CC];
+    int cnt[kRPL][2];
 #pragma unroll
-    for (int c = 0; c < CC; ++c) {
-        Na[c] = f2(0.f, 0.f);
-        Nb[c] = f2(0.f, 0.f);
+    for (int r = 0; r < kRPL; ++r) {
+        Wr[r] = f2(0.f, 0.f);
+        cnt[r][0] = cnt[r][1] = 0;
+#pragma unroll
+        for (int c = 0; c < CC; ++c) Nr[r][c] = f2(0.f, 0.f);
     }
-    int cnt00 = 0, cnt01 = 0, cnt10 = 0, cnt11 = 0;
     // lane window: columns of mu_x in (xa - r, xa + 1 + r) (exact in f64,
     // tabulated per lane on the host)
     const int q_lo = p.qlo[lane];
     const int q_hi = p.qhi[lane];
     // flagged points: generous band test (decided exactly by the f64 predicate)
     const float fb_lo = static_cast<float>(ya) - static_cast<float>(p.r64) - 1.0f;
-    const float fb_hi = static_cast<float>(ya + 1) + static_cast<float>(p.r64) + 1.0f;
+    const float fb_hi = static_cast<float>(ya + kRPL - 1) + static_cast<float>(p.r64) + 1.0f;
     const uint32_t mbar = smem_u32(&S.mbar);
     uint32_t phase = 0;
 
@@ -334,7 +353,7 @@ k_gather(GatherParams p) {
             }
             GMI_CHECK(key <= nbins && nbins + 1 < kBinMax + 2);
             if (key >= 0) atomicAdd(&S.bin[key], 1);
-            S.key[k] = key;
+            S.u.R[2 * k + 1].w = __int_as_float(key);
         }
         __syncthreads();
 
@@ -375,7 +394,7 @@ k_gather(GatherParams p) {
 
         // ---- C: scatter into bin order, dense (ends -> starts by decrement) ----
         for (int k = tid; k < total; k += kNT) {
-            const int key = S.key[k];
+            const int key = __float_as_int(S.u.R[2 * k + 1].w);
             if (key < 0) continue;
             const int pos = atomicSub(&S.bin[key], 1) - 1;
             GMI_CHECK(pos >= 0 && pos < kCap);
@@ -414,7 +433,7 @@ k_gather(GatherParams p) {
 
         // ---- E: this warp's column-major list (row-pair bins [w, w+dyb]) ----
         {
-            const int yb0 = warp, yb1 = min(warp + p.dyb, nyb - 1);
+            const int yb0 = warp * (kRPL / 2), yb1 = min(yb0 + kRPL / 2 - 1 + p.dyb, nyb - 1);
             // columns [c0, c1) of this lane: ncol spread evenly over the warp
             constexpr int kCpl = kColMax / 32;
             const int c0 = (lane * ncol) >> 5, c1 = ((lane + 1) * ncol) >> 5;
@@ -450,7 +469,7 @@ k_gather(GatherParams p) {
         }
         __syncwarp();
 
-        // ---- gather: 4 pixels per candidate, f32x2 ----
+        // ---- gather: 2 x kRPL pixels per candidate, f32x2 ----
         {
             const int ts = S.v.wcs[warp][q_lo], te = S.v.wcs[warp][q_hi + 1];
             const uint16_t* lst = S.u.wl[warp];
@@ -464,36 +483,29 @@ k_gather(GatherParams p) {
                 const float4 a = S.A[kc];
                 const float2 bcur = CC > 2 ? S.Bc[kc] : f2(0.f, 0.f);
                 const float2 dx = __fadd2_rn(X, f2(-a.x, -a.x));
-                const float2 dy = __fadd2_rn(Y, f2(-a.y, -a.y));
                 const float2 kx = __fmul2_rn(dx, nk2);
-                const float2 ey = __fmul2_rn(__fmul2_rn(dy, nk2), dy);
-                const float2 ea = __ffma2_rn(kx, dx, f2(ey.x, ey.x));
-                const float2 eb = __ffma2_rn(kx, dx, f2(ey.y, ey.y));
-                const bool i00 = ea.x >= thr, i01 = ea.y >= thr;
-                const bool i10 = eb.x >= thr, i11 = eb.y >= thr;
-                const float2 wa = f2(i00 ? ex2(ea.x) : 0.f, i01 ? ex2(ea.y) : 0.f);
-                const float2 wb = f2(i10 ? ex2(eb.x) : 0.f, i11 ? ex2(eb.y) : 0.f);
-                Wa = __fadd2_rn(Wa, wa);
-                Wb = __fadd2_rn(Wb, wb);
-                Na[0] = __ffma2_rn(wa, f2(a.z, a.z), Na[0]);
-                Nb[0] = __ffma2_rn(wb, f2(a.z, a.z), Nb[0]);
-                if (CC > 1) {
-                    Na[1] = __ffma2_rn(wa, f2(a.w, a.w), Na[1]);
-                    Nb[1] = __ffma2_rn(wb, f2(a.w, a.w), Nb[1]);
-                }
-                if (CC > 2) {
-                    Na[2] = __ffma2_rn(wa, f2(bcur.x, bcur.x), Na[2]);
-                    Nb[2] = __ffma2_rn(wb, f2(bcur.x, bcur.x), Nb[2]);
-                    if (CC > 3) {
-                        Na[3] = __ffma2_rn(wa, f2(bcur.y, bcur.y), Na[3]);
-                        Nb[3] = __ffma2_rn(wb, f2(bcur.y, bcur.y), Nb[3]);
+
+#pragma unroll
+                for (int j = 0; j < kRPL / 2; ++j) {
+                    const float2 dy = __fadd2_rn(Y[j], f2(-a.y, -a.y));
+                    const float2 ey = __fmul2_rn(__fmul2_rn(dy, nk2), dy);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int r = 2 * j + h;
+                        const float2 e = __ffma2_rn(kx, dx, h ? f2(ey.y, ey.y) : f2(ey.x, ey.x));
+                        const bool i0 = e.x >= thr, i1 = e.y >= thr;
+                        const float2 w = f2(i0 ? ex2(e.x) : 0.f, i1 ? ex2(e.y) : 0.f);
+                        Wr[r] = __fadd2_rn(Wr[r], w);
+#pragma unroll
+                        for (int c = 0; c < CC; ++c) {
+                            const float cc = c == 0 ? a.z : (c == 1 ? a.w : (c == 2 ? bcur.x : bcur.y));
+                            Nr[r][c] = __ffma2_rn(w, f2(cc, cc), Nr[r][c]);
+                        }
+                        if (kCount) {
+                            cnt[r][0] += i0;
+                            cnt[r][1] += i1;
+                        }
                     }
-                }
-                if (kCount) {
-                    cnt00 += i00;
-                    cnt01 += i01;
-                    cnt10 += i10;
-                    cnt11 += i11;
                 }
             }
         }
@@ -511,41 +523,37 @@ k_gather(GatherParams p) {
                     cc[3] = bc.y;
                 }
 #pragma unroll
-                for (int py = 0; py < 2; ++py) {
+                for (int r = 0; r < kRPL; ++r) {
 #pragma unroll
                     for (int px = 0; px < 2; ++px) {
-                        const int qx = xa + px, qy = ya + py;
+                        const int qx = xa + px, qy = ya + r;
                         if (d2_ref(qx, qy, a.x, a.y) > p.r2_64) continue;
                         const float ddx = static_cast<float>(qx) - a.x;
                         const float ddy = static_cast<float>(qy) - a.y;
                         const float w = ex2(fmaf(ddx * p.nk, ddx, (ddy * p.nk) * ddy));
-                        float2& Wr = py ? Wb : Wa;
-                        float2* Nr = py ? Nb : Na;
-                        if (px) Wr.y += w; else Wr.x += w;
+                        if (px) Wr[r].y += w; else Wr[r].x += w;
 #pragma unroll
                         for (int c = 0; c < CC; ++c) {
-                            if (px) Nr[c].y = fmaf(w, cc[c], Nr[c].y);
-                            else Nr[c].x = fmaf(w, cc[c], Nr[c].x);
+                            if (px) Nr[r][c].y = fmaf(w, cc[c], Nr[r][c].y);
+                            else Nr[r][c].x = fmaf(w, cc[c], Nr[r][c].x);
                         }
-                        if (kCount) {
-                            if (py) { if (px) ++cnt11; else ++cnt10; }
-                            else { if (px) ++cnt01; else ++cnt00; }
-                        }
+                        if (kCount) ++cnt[r][px];
                     }
                 }
             }
         }
         if (fold != nullptr) {
-            fold_acc(Wa.x, 0);
-            fold_acc(Wa.y, 1);
-            fold_acc(Wb.x, 2);
-            fold_acc(Wb.y, 3);
+            // value k: W of pixel (row r, column h) at 2 r + h, numerator c
+            // at 2 kRPL (c + 1) + 2 r + h
 #pragma unroll
-            for (int c = 0; c < CC && c < 3; ++c) {
-                fold_acc(Na[c].x, 4 + 4 * c);
-                fold_acc(Na[c].y, 5 + 4 * c);
-                fold_acc(Nb[c].x, 6 + 4 * c);
-                fold_acc(Nb[c].y, 7 + 4 * c);
+            for (int r = 0; r < kRPL; ++r) {
+                fold_acc(Wr[r].x, 2 * r);
+                fold_acc(Wr[r].y, 2 * r + 1);
+#pragma unroll
+                for (int c = 0; c < CC && c < 3; ++c) {
+                    fold_acc(Nr[r][c].x, 2 * kRPL * (c + 1) + 2 * r);
+                    fold_acc(Nr[r][c].y, 2 * kRPL * (c + 1) + 2 * r + 1);
+                }
             }
             folded = true;
         }
@@ -565,9 +573,9 @@ k_gather(GatherParams p) {
     if (fold != nullptr && folded) {
         // folded tile: W and out = num / W from the f64 totals
 #pragma unroll
-        for (int pk = 0; pk < 4; ++pk) {
-            const int py = pk >> 1, px = pk & 1;
-            const int qx = xa + px, qy = ya + py;
+        for (int pk = 0; pk < 2 * kRPL; ++pk) {
+            const int r = pk >> 1, px = pk & 1;
+            const int qx = xa + px, qy = ya + r;
             if (qx >= p.W || qy >= p.H) continue;
             const double w64 = fold[static_cast<size_t>(pk) * kNT];
             const size_t bp = (static_cast<size_t>(b) * p.H + qy) * p.W + qx;
@@ -575,9 +583,9 @@ k_gather(GatherParams p) {
             if (w64 > 0.0) {
 #pragma unroll
                 for (int c = 0; c < CC; ++c)
-                    out[c] = static_cast<float>(fold[static_cast<size_t>(4 + 4 * c + pk) * kNT] / w64);
+                    out[c] = static_cast<float>(fold[static_cast<size_t>(2 * kRPL * (c + 1) + pk) * kNT] / w64);
                 p.wsum[bp] = static_cast<float>(w64);
-                if (kCount) p.counts[bp] = py ? (px ? cnt11 : cnt10) : (px ? cnt01 : cnt00);
+                if (kCount) p.counts[bp] = cnt[r][px];
             } else {
                 p.wsum[bp] = 0.f;
                 if (kCount) p.counts[bp] = 0;
@@ -589,9 +597,9 @@ k_gather(GatherParams p) {
         return;
     }
 #pragma unroll
-    for (int py = 0; py < 2; ++py) {
-        const int qy = ya + py;
-        const float2 wr = py ? Wb : Wa;
+    for (int r = 0; r < kRPL; ++r) {
+        const int qy = ya + r;
+        const float2 wr = Wr[r];
         // both pixels inside and non-fallback, 8-byte aligned: 64-bit stores
         // of the pixel pair
         const size_t bpr = (static_cast<size_t>(b) * p.H + qy) * p.W + xa;
@@ -602,7 +610,7 @@ k_gather(GatherParams p) {
             float o[2 * CC];
 #pragma unroll
             for (int c = 0; c < CC; ++c) {
-                const float2 nm = py ? Nb[c] : Na[c];
+                const float2 nm = Nr[r][c];
                 o[c] = norm(nm.x, wr.x, ia);
                 o[CC + c] = norm(nm.y, wr.y, ib);
             }
@@ -616,18 +624,18 @@ k_gather(GatherParams p) {
         for (int px = 0; px < 2; ++px) {
             const int qx = xa + px;
             if (qx >= p.W || qy >= p.H) continue;
-            const float w = py ? (px ? Wb.y : Wb.x) : (px ? Wa.y : Wa.x);
+            const float w = px ? wr.y : wr.x;
             const size_t bp = (static_cast<size_t>(b) * p.H + qy) * p.W + qx;
             float* out = p.image + bp * p.C;
             if (w > 0.f) {
                 const float inv = 1.0f / w;
 #pragma unroll
                 for (int c = 0; c < CC; ++c) {
-                    const float num = py ? (px ? Nb[c].y : Nb[c].x) : (px ? Na[c].y : Na[c].x);
+                    const float num = px ? Nr[r][c].y : Nr[r][c].x;
                     out[c] = norm(num, w, inv);
                 }
                 p.wsum[bp] = w;
-                if (kCount) p.counts[bp] = py ? (px ? cnt11 : cnt10) : (px ? cnt01 : cnt00);
+                if (kCount) p.counts[bp] = cnt[r][px];
             } else {
                 // empty neighbourhood: fallback pixel (K3)
                 p.wsum[bp] = 0.f;
@@ -657,14 +665,18 @@ static void gather_geometry(double r, int& rc, int& ncol, int& dyb, int& nyb) {
     // columns of (xa - r, xa + 1 + r), so ncol covers the last lane's
     rc = static_cast<int>(std::ceil(r));
     ncol = static_cast<int>(std::ceil(static_cast<double>(kTW - 2 + rc + 1) + r));
-    // row pairs: floor((mu_y - (y0 - r)) / 2); warp w reads [w, w + dyb]
+    // row pairs: floor((mu_y - (y0 - r)) / 2); warp w (rows y0 + kRPL w ..
+    // + kRPL - 1) reads [w kRPL/2, w kRPL/2 + kRPL/2 - 1 + dyb]
     dyb = static_cast<int>(std::ceil(0.5 + r)) - 1;
-    nyb = kNW + dyb;
+    nyb = kNW * (kRPL / 2) + dyb;
 }
 
 // The fast gather applies: fp32 weight mode and a bin table that fits.
+// C > 4 takes the wide-channel gather (gmi_wide.cu), which stages by cell
+// rows and has no bin table: any radius of the fp32 mode.
 bool gather_fast_ok(const gmi_cache* c) {
     if (c->wsum64 != nullptr || c->force_generic) return false;
+    if (c->C > 4) return true;
     int rc, ncol, dyb, nyb;
     gather_geometry(c->cutoff, rc, ncol, dyb, nyb);
     return ncol < kColMax && ncol * nyb + 1 <= kBinMax;

@@ -9,7 +9,9 @@ h = rows[0]
 res = {}
 for r in rows[2:]:
     name = r[h.index("Kernel Name")]
-    key = "points_bwd" if "k_backward_points" in name else ("gather" if "k_gather" in name else "scatter_emit")
+    key = next((v for k, v in (("k_backward_points", "points_bwd"), ("k_gather", "gather"),
+                               ("k_scatter_emit", "scatter_emit"), ("k_count_red", "count"),
+                               ("k_bbox_validate", "bbox")) if k in name), name[:40])
     units = rows[1]
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
              "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,
