@@ -445,7 +445,7 @@ k_backward_points(BwdParams p) {
                 const float h2f = fmaf(-dy, dy, r2f);
                 if (h2f < 0.f) continue;
                 // ~2 ulp: a safe point's row ends are >= 8e-6 r^2 from the ball
-                const float sq = h2f * rsqrtf(fmaxf(h2f, 1e-30f));
+                const float sq = h2f * rsqrt_ftz(fmaxf(h2f, 1e-30f));
                 // ceil / floor of small values by directed-rounding adds of
                 // 1.5 * 2^23 (FMA pipe, no conversion on the XU pipe)
                 constexpr float kMagic = 12582912.0f;

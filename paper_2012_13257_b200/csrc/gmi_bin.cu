@@ -508,7 +508,7 @@ __device__ __forceinline__ bool point_ambiguous_fast(float mx, float my, float r
         const float2 h2 = __ffma2_rn(make_float2(-dy.x, -dy.y), dy, r2);
         const float hx = fmaxf(h2.x, 0.f), hy = fmaxf(h2.y, 0.f);
         const float2 sq = __fmul2_rn(make_float2(hx, hy),
-                                     make_float2(rsqrtf(fmaxf(hx, 1e-30f)), rsqrtf(fmaxf(hy, 1e-30f))));
+                                     make_float2(rsqrt_ftz(fmaxf(hx, 1e-30f)), rsqrt_ftz(fmaxf(hy, 1e-30f))));
         const float2 lo = __fadd2_rn(fm2, make_float2(-sq.x, -sq.y));
         const float2 hi = __fadd2_rn(fm2, sq);
         const float2 nl = __fadd2_rn(__fadd2_rn(lo, M2), nM2);  // rint

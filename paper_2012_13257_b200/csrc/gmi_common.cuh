@@ -76,6 +76,15 @@ __device__ __forceinline__ int cell_of_unclamped(double v, double origin,
     return x86_d2i(floor(__ddiv_rn(__dsub_rn(v, origin), cell)));
 }
 
+// rsqrt.approx without the denormal-input fix-up (callers clamp the input
+// to >= 1e-30, a normal number): the same MUFU.RSQ result as rsqrtf for every
+// normal input, three instructions shorter.
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Reference inclusion predicate (bin_grid.cpp:87,98; core.hpp:21-23):
 //   (qx-mx)^2 + (qy-my)^2 <= r^2, f64, two roundings, no FMA.
 __device__ __forceinline__ double d2_ref(double qx, double qy, double mx,

@@ -771,7 +771,7 @@ k_backward_wide(BwdWideParams p) {
                     dy = yf - my;
                     const float h2f = fmaf(-dy, dy, r2f);
                     if (h2f < 0.f) continue;
-                    const float sqv = h2f * rsqrtf(fmaxf(h2f, 1e-30f));
+                    const float sqv = h2f * rsqrt_ftz(fmaxf(h2f, 1e-30f));
                     constexpr float kMagic = 12582912.0f;
                     constexpr int kMagicBits = 0x4B400000;
                     xl = bx + (__float_as_int(__fadd_ru(fmu - sqv, kMagic)) - kMagicBits);
