@@ -555,12 +555,13 @@ __global__ void __launch_bounds__(256) k_scatter_emit(ScatterEmitParams p) {
     const Geom g = p.geom[b];
     const double inv = 1.0 / g.cell;
     const int i0 = blockIdx.x * (blockDim.x * kEmitPer) + threadIdx.x;
+    const int istep = blockDim.x;
     int dst[kEmitPer];
     float2 v[kEmitPer];
     float c[kEmitPer][4];
 #pragma unroll
     for (int u = 0; u < kEmitPer; ++u) {
-        const int i = i0 + u * blockDim.x;
+        const int i = i0 + u * istep;
         if (i < p.N) {
             v[u] = p.pos[base + i];
 #pragma unroll
@@ -569,7 +570,7 @@ __global__ void __launch_bounds__(256) k_scatter_emit(ScatterEmitParams p) {
     }
 #pragma unroll
     for (int u = 0; u < kEmitPer; ++u) {
-        const int i = i0 + u * blockDim.x;
+        const int i = i0 + u * istep;
         dst[u] = -1;
         if (i < p.N) {
             const int cx = cell_of_fast(static_cast<double>(v[u].x), g.ox, g.cell, inv, g.n_cols);
@@ -580,7 +581,7 @@ __global__ void __launch_bounds__(256) k_scatter_emit(ScatterEmitParams p) {
     }
 #pragma unroll
     for (int u = 0; u < kEmitPer; ++u) {
-        const int i = i0 + u * blockDim.x;
+        const int i = i0 + u * istep;
         if (dst[u] < 0) continue;
         unsigned code = 0;
 #pragma unroll
@@ -747,6 +748,14 @@ __global__ void __launch_bounds__(512) k_sort_big_recs(int N, const Geom* __rest
 
 // Cell counts only (fire-and-forget reductions, no ranks stored): the fast
 // path's count pass; k_scatter_emit recomputes the cell and takes its slot.
+// Counts with 16-byte position loads (two points each) and kCountPer
+// points per thread in flight: the count is a pure latency problem (its
+// fire-and-forget RED.ADDs need no return).  N odd or unaligned positions:
+// one point per load.
+#ifndef GMI_K1_COUNT_PER
+#define GMI_K1_COUNT_PER 4
+#endif
+constexpr int kCountPer = GMI_K1_COUNT_PER;
 __global__ void __launch_bounds__(256) k_count_red(const float2* __restrict__ pos, int N,
                                                    const Geom* __restrict__ geom,
                                                    int32_t* __restrict__ bins) {
@@ -754,15 +763,39 @@ __global__ void __launch_bounds__(256) k_count_red(const float2* __restrict__ po
     const Geom g = geom[b];
     const double inv = 1.0 / g.cell;
     const size_t base = static_cast<size_t>(b) * N;
-    const int i0 = blockIdx.x * (blockDim.x * kEmitPer) + threadIdx.x;
-    float2 v[kEmitPer];
+    const bool vec = (N % 2) == 0 && (reinterpret_cast<uintptr_t>(pos) & 15) == 0;
+    if (vec) {
+        const float4* p4 = reinterpret_cast<const float4*>(pos + base);
+        const int k0 = blockIdx.x * (blockDim.x * kCountPer / 2) + threadIdx.x;
+        float4 v[kCountPer / 2];
 #pragma unroll
-    for (int u = 0; u < kEmitPer; ++u) {
+        for (int u = 0; u < kCountPer / 2; ++u) {
+            const int k = k0 + u * blockDim.x;
+            if (2 * k < N) v[u] = p4[k];
+        }
+#pragma unroll
+        for (int u = 0; u < kCountPer / 2; ++u) {
+            const int k = k0 + u * blockDim.x;
+            if (2 * k >= N) continue;
+            const float xs[2] = {v[u].x, v[u].z}, ys[2] = {v[u].y, v[u].w};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int cx = cell_of_fast(static_cast<double>(xs[h]), g.ox, g.cell, inv, g.n_cols);
+                const int cy = cell_of_fast(static_cast<double>(ys[h]), g.oy, g.cell, inv, g.n_rows);
+                atomicAdd(bins + g.bin_off + cy * g.n_cols + cx, 1);  // bin_grid.cpp:67
+            }
+        }
+        return;
+    }
+    const int i0 = blockIdx.x * (blockDim.x * kCountPer) + threadIdx.x;
+    float2 v[kCountPer];
+#pragma unroll
+    for (int u = 0; u < kCountPer; ++u) {
         const int i = i0 + u * blockDim.x;
         if (i < N) v[u] = pos[base + i];
     }
 #pragma unroll
-    for (int u = 0; u < kEmitPer; ++u) {
+    for (int u = 0; u < kCountPer; ++u) {
         const int i = i0 + u * blockDim.x;
         if (i < N) {
             const int cx = cell_of_fast(static_cast<double>(v[u].x), g.ox, g.cell, inv, g.n_cols);
@@ -977,7 +1010,8 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
     if (hot && !c->sort_cells) {
         // fast path: counts -> inclusive scan (cell ends) -> 32-byte records
         // at slots taken from the ends, which leaves bin_start behind
-        k_count_red<<<pgrid4, 256, 0, st>>>(p2, N, c->geom_d, c->bins);
+        k_count_red<<<dim3((N + 256 * kCountPer - 1) / (256 * kCountPer), B), 256, 0, st>>>(
+            p2, N, c->geom_d, c->bins);
         GMI_LAUNCHED(ctx);
         host_trace("bin: count launched");
         // cells the gather may split (> its chunk capacity) are listed by the
