@@ -210,3 +210,39 @@ def test_shard_and_band_logic():
                                  gdist.default_halo(3.0)).tolist() == [True, False]
     assert gdist.weak_scaling_units(64, 8) == 512
     assert sum(gdist.strong_scaling_batch(64, 8, r) for r in range(8)) == 64
+
+
+def _group_worker(rank, world, port, out):
+    """The product driver's plumbing (paper_2012_13257_b200.multi.Group) on
+    gloo: rank / world from the env, max-over-ranks timing, in-place SUM of a
+    shared-gradient buffer, batch shards covering the global batch."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    from paper_2012_13257_b200 import multi
+
+    g = multi.Group("gloo")
+    try:
+        tmax = g.max_over_ranks(1.5 + rank)
+        buf = torch.full((4, 5), float(rank + 1))
+        g.sum_(buf)
+        shards = multi.BatchShards(g, 64, 48, 1.0, 3.0)
+        s, e = shards.local_range(64)
+        t = torch.zeros(64)
+        t[s:e] = 1.0
+        g.sum_(t)
+        g.barrier()
+        out[rank] = (g.rank, g.world, tmax, float(buf[0, 0]), bool(torch.all(t == 1.0)))
+    finally:
+        g.close()
+
+
+def test_product_driver_group_on_gloo():
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_group_worker, args=(world, port, out), nprocs=world, join=True)
+    for r in range(world):
+        rank, w, tmax, s, cover = out[r]
+        assert (rank, w) == (r, world)
+        assert tmax == 2.5 and s == 3.0 and cover
