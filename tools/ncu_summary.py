@@ -40,7 +40,8 @@ if kfilter:
     rows = list(csv.reader(sass.splitlines()))
     hh = rows[1]
     isrc, iex, ist = hh.index('Source'), hh.index('Instructions Executed'), hh.index('Warp Stall Sampling (All Samples)')
-    data = [(r[isrc].strip(), int(r[iex] or 0), int(r[ist] or 0)) for r in rows[2:] if len(r) > iex]
+    data = [(r[isrc].strip(), int(r[iex] or 0), int(r[ist] or 0)) for r in rows[2:]
+            if len(r) > iex and r[iex].replace(',', '').isdigit() or (len(r) > iex and r[iex] == '')]
     segs, cur = [], None
     for i, (s, e, st) in enumerate(data):
         if cur and cur[2] == e:
