@@ -171,3 +171,40 @@ def test_pinned_and_pageable_host_buffers_agree(gmi, orc):
                                          Cc, C.byref(cfg), cache_a.handle, pup.ctypes.data_as(fp),
                                          pdc.ctypes.data_as(fp), pdp.ctypes.data_as(fp)))
     assert np.array_equal(dc_a, pdc)
+
+
+def test_concurrent_contexts_from_host_threads(gmi, orc):
+    # SURVEY §8(b) threading: one context per host thread on the same device,
+    # calls in flight concurrently (ctypes drops the GIL), results identical
+    # to the same calls made one after the other
+    import threading
+
+    cases = [orc.synth_batch(100 + k, 2, 2500, 3, 80, 64) for k in range(4)]
+    ctxs = [gmi.Context(0) for _ in cases]
+    want = []
+    for (pos, col, up), ctx in zip(cases, ctxs):
+        img, cache = gmi.forward_batch(pos, col, 80, 64, 1.5, 4.5, ctx=ctx)
+        dc, dp = gmi.backward_batch(pos, col, cache, up, 1.5, 4.5, ctx=ctx)
+        want.append((img, dc, dp))
+    got = [None] * len(cases)
+    errors = []
+
+    def work(k):
+        try:
+            pos, col, up = cases[k]
+            for _ in range(3):
+                img, cache = gmi.forward_batch(pos, col, 80, 64, 1.5, 4.5, ctx=ctxs[k])
+                dc, dp = gmi.backward_batch(pos, col, cache, up, 1.5, 4.5, ctx=ctxs[k])
+            got[k] = (img, dc, dp)
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(len(cases))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for k in range(len(cases)):
+        for a, b in zip(got[k], want[k]):
+            assert np.array_equal(a, b)
