@@ -58,12 +58,8 @@ struct gmi_ctx {
     bool own_stream = false;
     uint32_t flags = 0;
     uint64_t launches = 0;
-    // pending asynchronous validation result (GMI_CTX_ASYNC_ERRORS)
-    unsigned long long* h_issue = nullptr;  // pinned, per image
-    int h_issue_cap = 0;
-    std::vector<int> pending_codes;
-    std::string pending_msg;
-    int pending_code = 0;
+    // host copy of the per-image validation keys (pinned)
+    unsigned long long* h_issue = nullptr;
     // device scratch for validation keys (per image of the current call)
     unsigned long long* d_issue = nullptr;
     int d_issue_cap = 0;
