@@ -62,7 +62,7 @@ def build(with_reference: bool | None = None) -> None:
     when its sources are present (this container, not the GPU box)."""
     if with_reference is None:
         with_reference = os.path.isdir("/root/reference/proj/src")
-    targets = ["liboracle.so"] + (["ref"] if with_reference else [])
+    targets = ["liboracle.so"] + (["ref", "dropin"] if with_reference else [])
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 
