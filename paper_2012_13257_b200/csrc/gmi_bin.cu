@@ -487,7 +487,12 @@ __global__ void k_geom(const uint32_t* __restrict__ bbox, int B, double cell, in
 // root: the row crossing's nearest integers are found from s = sqrt(h^2),
 // whose error only matters when mu -+ s is within ~1e-6 of a half-integer,
 // i.e. when both neighbouring integers are ~1/2 away and far outside the
-// 8e-6 r^2 band (same decision as point_ambiguous_f32).
+// 8e-6 r^2 band (same decision as point_ambiguous in gmi_common.cuh).
+//
+// Branch-free: the point is ambiguous iff the smallest |e| over the rows'
+// candidate integers is <= tau.  Rows outside the disk need no mask: there
+// h^2 < -tau, s = 0 and e = (n - mu)^2 - h^2 >= -h^2 > tau; so does the
+// extra row an odd row count adds past y1 (its dy exceeds r + 0.02).
 __device__ __forceinline__ bool point_ambiguous_fast(float mx, float my, float rf, float r2f) {
     if (!(fabsf(mx) < 1048576.f && fabsf(my) < 1048576.f)) return true;
     const float tau = kAmbRel * r2f;
@@ -503,12 +508,12 @@ __device__ __forceinline__ bool point_ambiguous_fast(float mx, float my, float r
     const float2 M2 = make_float2(kM, kM), nM2 = make_float2(-kM, -kM);
     float2 dy = make_float2(static_cast<float>(y0 - by) - fmy, static_cast<float>(y0 + 1 - by) - fmy);
     const float2 two = make_float2(2.f, 2.f), r2 = make_float2(r2f, r2f);
-    bool amb = false;
+    float emin = INFINITY;
+#pragma unroll 2
     for (int y = y0; y <= y1; y += 2) {
         const float2 h2 = __ffma2_rn(make_float2(-dy.x, -dy.y), dy, r2);
-        const float hx = fmaxf(h2.x, 0.f), hy = fmaxf(h2.y, 0.f);
-        const float2 sq = __fmul2_rn(make_float2(hx, hy),
-                                     make_float2(rsqrt_ftz(fmaxf(hx, 1e-30f)), rsqrt_ftz(fmaxf(hy, 1e-30f))));
+        const float hx = fmaxf(h2.x, 1e-30f), hy = fmaxf(h2.y, 1e-30f);
+        const float2 sq = __fmul2_rn(make_float2(hx, hy), make_float2(rsqrt_ftz(hx), rsqrt_ftz(hy)));
         const float2 lo = __fadd2_rn(fm2, make_float2(-sq.x, -sq.y));
         const float2 hi = __fadd2_rn(fm2, sq);
         const float2 nl = __fadd2_rn(__fadd2_rn(lo, M2), nM2);  // rint
@@ -516,11 +521,10 @@ __device__ __forceinline__ bool point_ambiguous_fast(float mx, float my, float r
         const float2 dl = __fadd2_rn(nl, mf2), dr = __fadd2_rn(nr, mf2);
         const float2 el = __ffma2_rn(dl, dl, make_float2(-h2.x, -h2.y));
         const float2 er = __ffma2_rn(dr, dr, make_float2(-h2.x, -h2.y));
-        amb |= (h2.x >= -tau) && (fabsf(el.x) <= tau || fabsf(er.x) <= tau);
-        amb |= (y + 1 <= y1) && (h2.y >= -tau) && (fabsf(el.y) <= tau || fabsf(er.y) <= tau);
+        emin = fminf(emin, fminf(fminf(fabsf(el.x), fabsf(er.x)), fminf(fabsf(el.y), fabsf(er.y))));
         dy = __fadd2_rn(dy, two);
     }
-    return amb;
+    return emin <= tau;
 }
 
 // Hot layout straight from atomic slots (no within-cell ordering: the fast

@@ -85,6 +85,14 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
     return y;
 }
 
+// Reciprocal on the SFU (MUFU.RCP, <= 1 ulp, flush-to-zero) without the
+// IEEE division's refinement and range fix-ups; callers pass W > 0 normals.
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Reference inclusion predicate (bin_grid.cpp:87,98; core.hpp:21-23):
 //   (qx-mx)^2 + (qy-my)^2 <= r^2, f64, two roundings, no FMA.
 __device__ __forceinline__ double d2_ref(double qx, double qy, double mx,

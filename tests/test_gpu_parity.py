@@ -211,6 +211,23 @@ def test_integer_lattice_exact_ties(gmi, ctx, orc):
     check_instance(gmi, ctx, orc, pos + 0.5, col, 40, 30, 1.0, 3.0)
 
 
+@pytest.mark.parametrize("ch,sigma", [(3, 1.3), (1, 0.7), (4, 2.1)])
+def test_near_boundary_ties(gmi, ctx, orc, ch, sigma):
+    # every point within ~1e-5 r^2 of the ball boundary of some pixel (fp32
+    # rounding of the position keeps it in that band): the K1 ambiguity flag
+    # must route each decision the fp32 test could get wrong to the f64
+    # predicate, so per-pixel counts stay bit-exact
+    rng = np.random.default_rng(int(sigma * 10) + ch)
+    r = 3.0 * sigma
+    n = 1500
+    q = rng.integers(4, 60, (n, 2)).astype(np.float64)
+    th = rng.uniform(0, 2 * np.pi, n)
+    eps = rng.uniform(-4e-6, 4e-6, n)
+    pos = q + (r * (1.0 + eps))[:, None] * np.stack([np.cos(th), np.sin(th)], 1)
+    col = rng.uniform(0, 1, (n, ch))
+    check_instance(gmi, ctx, orc, pos, col, 64, 64, sigma, r)
+
+
 def test_duplicates_and_single_pixel(gmi, ctx, orc):
     pos = np.array([[1, 1], [1, 1], [1, 1], [0.25, 0.75]], np.float64)
     col = np.array([[0.1], [0.2], [0.3], [0.9]])
