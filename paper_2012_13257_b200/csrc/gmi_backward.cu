@@ -31,20 +31,12 @@ using namespace gmi_dev;
 namespace {
 
 constexpr int kThreads = 256;
-#ifndef GMI_BWD_CTAS
-#define GMI_BWD_CTAS 4
-#endif
-constexpr int kCtasPerSm = GMI_BWD_CTAS;  // resident CTAs per SM (registers / smem)
-constexpr int kSmemBudget = (kCtasPerSm == 4 ? 52 : 208 / kCtasPerSm) * 1024;  // staged pixel bytes per CTA
+constexpr int kSmemBudget = 52 * 1024;  // staged pixel bytes per CTA (4 CTAs/SM)
 constexpr int kRunMax = 64;             // cell rows per block
 #ifndef GMI_BWD_STAGE_UNROLL
 #define GMI_BWD_STAGE_UNROLL 1
 #endif
 constexpr int kStageUnroll = GMI_BWD_STAGE_UNROLL;  // staging pairs in flight per lane
-#ifndef GMI_BWD_PAIR_UNROLL
-#define GMI_BWD_PAIR_UNROLL 1
-#endif
-constexpr int kPairUnroll = GMI_BWD_PAIR_UNROLL;    // pixel-pair loop unroll
 
 struct BwdParams {
     const Geom* geom;
@@ -99,7 +91,7 @@ __device__ __forceinline__ void pixel_terms(const BwdParams& p, size_t img_base,
     const size_t pix = img_base + static_cast<size_t>(y) * p.W + x;
     const float wv = p.wsum[pix];
     if (!(wv > 0.f)) return;
-    const float inv = rcp_approx(wv);
+    const float inv = 1.0f / wv;
 #pragma unroll
     for (int c = 0; c < CG; ++c) {
         if (c < nch) {
@@ -109,16 +101,8 @@ __device__ __forceinline__ void pixel_terms(const BwdParams& p, size_t img_base,
     }
 }
 
-// d_positions across a point's disk rows: f64 by default (the row sums
-// cancel; an fp32 total carries their rounding); GMI_BWD_ROWS_F32 for A/B
-#ifdef GMI_BWD_ROWS_F32
-using acc_t = float;
-#else
-using acc_t = double;
-#endif
-
 template <int CG, int LPP>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+__global__ void __launch_bounds__(kThreads, 4)
 k_backward_points(BwdParams p) {
     using L = PairLayout<CG>;
     extern __shared__ float4 s_pair[];   // [L::kF4][rows][pairs]
@@ -297,8 +281,11 @@ k_backward_points(BwdParams p) {
         const bool vec4 = CG == 4 && (p.C % 4) == 0 && (p.W % 2) == 0 &&
                           (reinterpret_cast<uintptr_t>(p.upstream) & 15) == 0 &&
                           (reinterpret_cast<uintptr_t>(p.image) & 15) == 0;
+        // rows by warps, pixel pairs by lanes (coalesced, no index division)
         const int nrows = ry1 - ry0 + 1;
-        auto stage_pair = [&](const int row, const int pp) {
+        for (int row = tid >> 5; row < nrows; row += kThreads / 32)
+#pragma unroll kStageUnroll
+        for (int pp = lane; pp < npairs; pp += 32) {
             const int k = row * npairs + pp, yy = ry0 + row;
             const int xa = rx0 + 2 * pp;
             float ua[CG], ub[CG], va = 0.f, vb = 0.f;
@@ -317,8 +304,8 @@ k_backward_points(BwdParams p) {
                     imv[2 * j] = c2.x;
                     imv[2 * j + 1] = c2.y;
                 }
-                const float ia = wv.x > 0.f ? rcp_approx(wv.x) : 0.f;
-                const float ib = wv.y > 0.f ? rcp_approx(wv.y) : 0.f;
+                const float ia = wv.x > 0.f ? 1.0f / wv.x : 0.f;
+                const float ib = wv.y > 0.f ? 1.0f / wv.y : 0.f;
 #pragma unroll
                 for (int c = 0; c < CG; ++c) {
                     ua[c] = upv[c] * ia;
@@ -335,8 +322,8 @@ k_backward_points(BwdParams p) {
                 const float4 ub4 = *reinterpret_cast<const float4*>(p.upstream + (pix + 1) * p.C + ch0);
                 const float4 oa4 = *reinterpret_cast<const float4*>(p.image + pix * p.C + ch0);
                 const float4 ob4 = *reinterpret_cast<const float4*>(p.image + (pix + 1) * p.C + ch0);
-                const float ia = wv.x > 0.f ? rcp_approx(wv.x) : 0.f;
-                const float ib = wv.y > 0.f ? rcp_approx(wv.y) : 0.f;
+                const float ia = wv.x > 0.f ? 1.0f / wv.x : 0.f;
+                const float ib = wv.y > 0.f ? 1.0f / wv.y : 0.f;
                 const float uav[4] = {ua4.x, ua4.y, ua4.z, ua4.w}, ubv[4] = {ub4.x, ub4.y, ub4.z, ub4.w};
                 const float oav[4] = {oa4.x, oa4.y, oa4.z, oa4.w}, obv[4] = {ob4.x, ob4.y, ob4.z, ob4.w};
 #pragma unroll
@@ -363,31 +350,7 @@ k_backward_points(BwdParams p) {
                 GMI_CHECK(k >= 0 && k < area);
                 s_pair[j * area + k] = make_float4(e[2 * j].x, e[2 * j].y, e[2 * j + 1].x, e[2 * j + 1].y);
             }
-        };
-#ifndef GMI_BWD_STAGE_ROWS
-        // the region's pairs in row-major order dealt to all threads
-        // (coalesced runs; no lane idles at a row's end), the (row, pair)
-        // position advanced by a constant step: one division per thread
-        {
-            const int dr = kThreads / npairs, dp = kThreads - dr * npairs;
-            int row = tid / npairs, pp = tid - row * npairs;
-#pragma unroll kStageUnroll
-            while (row < nrows) {
-                stage_pair(row, pp);
-                pp += dp;
-                row += dr;
-                if (pp >= npairs) {
-                    pp -= npairs;
-                    ++row;
-                }
-            }
         }
-#else
-        // rows by warps, pixel pairs by lanes
-        for (int row = tid >> 5; row < nrows; row += kThreads / 32)
-#pragma unroll kStageUnroll
-            for (int pp = lane; pp < npairs; pp += 32) stage_pair(row, pp);
-#endif
         __syncthreads();
     }
 
@@ -459,7 +422,7 @@ k_backward_points(BwdParams p) {
         for (int c = 0; c < CG; ++c) dcol[c] = f2(0.f, 0.f);
         // d_pos: fp32 sums inside a row, f64 across rows (the row sums
         // cancel; an fp32 total would carry their rounding)
-        acc_t gx = 0, gy = 0;
+        double gx = 0.0, gy = 0.0;
         const float tx = truncf(mx);
         const float fmu = mx - tx;  // exact
         const int bx = static_cast<int>(tx);
@@ -529,8 +492,8 @@ k_backward_points(BwdParams p) {
                     gxr = fmaf(a, dx, gxr);
                     gyr += a;
                 }
-                gx += static_cast<acc_t>(gxr);
-                gy = fma(static_cast<acc_t>(gyr), static_cast<acc_t>(dy), gy);
+                gx += static_cast<double>(gxr);
+                gy = fma(static_cast<double>(gyr), static_cast<double>(dy), gy);
                 continue;
             }
             // pair-aligned span (rx0 is even): pairs xs..xs+2(np-1); the end
@@ -545,37 +508,7 @@ k_backward_points(BwdParams p) {
             const float4* pr = s_pair + (y - ry0) * npairs + ((xs - rx0) >> 1);
             GMI_CHECK(y >= ry0 && xs >= rx0 && (y - ry0) * npairs + ((xs - rx0) >> 1) + np <= area &&
                       area * L::kF4 * static_cast<int>(sizeof(float4)) <= kSmemBudget);
-#ifndef GMI_BWD_MASK_LOOP
-            // first and last pair peeled (their end-pixel masks applied by one
-            // multiply each: w * 1 and w * 0 are exact), the pairs between
-            // unmasked
-            auto pair_step = [&](const float4* ps, const float2 m, const bool masked) {
-                float4 q4[L::kF4];
-#pragma unroll
-                for (int c = 0; c < L::kF4; ++c) q4[c] = ps[c * area];
-                const float2* q = reinterpret_cast<const float2*>(q4);
-                const float2 dx = __fadd2_rn(X, mmx);
-                const float2 arg = __ffma2_rn(__fmul2_rn(dx, nk2), dx, ey2);
-                float2 w = f2(ex2(arg.x), ex2(arg.y));
-                if (masked) w = __fmul2_rn(w, m);
-                float2 t = __fmul2_rn(q[0], f2(cc[0], cc[0]));
-#pragma unroll
-                for (int c = 1; c < CG; ++c) t = __ffma2_rn(q[c], f2(cc[c], cc[c]), t);
-                t = __fadd2_rn(t, q[CG]);
-                const float2 a = __fmul2_rn(w, t);
-#pragma unroll
-                for (int c = 0; c < CG; ++c) dcol[c] = __ffma2_rn(w, q[c], dcol[c]);
-                gx2 = __ffma2_rn(a, dx, gx2);
-                gyr2 = __fadd2_rn(gyr2, a);
-                X = __fadd2_rn(X, two);
-            };
-            const float4* const pe = pr + (np - 1);
-            pair_step(pr, f2(mf, np == 1 ? ml : 1.f), true);
-#pragma unroll kPairUnroll
-            for (const float4* ps = pr + 1; ps < pe; ++ps) pair_step(ps, two, false);
-            if (np > 1) pair_step(pe, f2(1.f, ml), true);
-#else
-#pragma unroll kPairUnroll
+#pragma unroll 1
             for (int j = 0; j < np; ++j) {
                 float4 q4[L::kF4];
 #pragma unroll
@@ -603,11 +536,10 @@ k_backward_points(BwdParams p) {
                 X = __fadd2_rn(X, two);
                 ++pr;
             }
-#endif
-            gx += static_cast<acc_t>(gx2.x + gx2.y);
-            gy = fma(static_cast<acc_t>(gyr2.x + gyr2.y), static_cast<acc_t>(dy), gy);
+            gx += static_cast<double>(gx2.x + gx2.y);
+            gy = fma(static_cast<double>(gyr2.x + gyr2.y), static_cast<double>(dy), gy);
         }
-        acc_t gxs = gx;
+        double gxs = gx;
         float dcs[CG];
 #pragma unroll
         for (int c = 0; c < CG; ++c) dcs[c] = dcol[c].x + dcol[c].y;
@@ -637,8 +569,8 @@ k_backward_points(BwdParams p) {
             for (int c = 0; c < nch; ++c) dc[c] = dcs[c];
         }
         float* dp = p.d_pos + (static_cast<size_t>(cg) * p.B * p.N + base + i) * 2;
-        const float2 g2 = f2(static_cast<float>(gxs * static_cast<acc_t>(inv_s2)),
-                             static_cast<float>(gy * static_cast<acc_t>(inv_s2)));
+        const float2 g2 = f2(static_cast<float>(gxs * static_cast<double>(inv_s2)),
+                             static_cast<float>(gy * static_cast<double>(inv_s2)));
         if ((reinterpret_cast<uintptr_t>(p.d_pos) & 7) == 0) {
             *reinterpret_cast<float2*>(dp) = g2;
         } else {

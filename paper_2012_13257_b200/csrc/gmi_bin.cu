@@ -529,12 +529,13 @@ __device__ __forceinline__ bool point_ambiguous_fast(float mx, float my, float r
 
 // Hot layout straight from atomic slots (no within-cell ordering: the fast
 // gather canonicalises its own bins and the backward is order-independent):
-// thread per point (4 per thread for memory-level parallelism), coalesced
-// reads of the point, its cell recomputed (bit-identical to k_count_red) and
-// a slot taken by decrementing the cell's end (the inclusive scan), so the
-// ends become bin_start with no rank or cell-id arrays in between; ONE
-// 32-byte record written at the slot — (x, y, c0, c1) (c2, c3, idx |
-// ambiguity flag, 0) — plus colour validation (core.cpp:80-92).
+// three points per thread, coalesced reads of the points, their cells
+// recomputed (bit-identical to k_count_red) and slots taken by decrementing
+// the cells' ends (the inclusive scan), so the ends become bin_start with no
+// rank or cell-id arrays in between; the three slot atomics are in flight
+// together while the colour validation (core.cpp:80-92) and the ambiguity
+// test run; ONE 32-byte record per point — (x, y, c0, c1) (c2, c3, idx |
+// ambiguity flag, 0) — written by one 256-bit store.
 struct ScatterEmitParams {
     const float2* pos;
     const float* col;
@@ -549,7 +550,7 @@ struct ScatterEmitParams {
 };
 
 #ifndef GMI_K1_EMIT_PER
-#define GMI_K1_EMIT_PER 2
+#define GMI_K1_EMIT_PER 3
 #endif
 constexpr int kEmitPer = GMI_K1_EMIT_PER;
 
@@ -563,38 +564,46 @@ __global__ void __launch_bounds__(256) k_scatter_emit(ScatterEmitParams p) {
     int dst[kEmitPer];
     float2 v[kEmitPer];
     float c[kEmitPer][4];
+    // straight-line code (indices past N clamped, their atomics add 0) so
+    // the slot atomics are all in flight before anything consumes them:
+    // their round trips overlap the colour checks and the ambiguity test
 #pragma unroll
     for (int u = 0; u < kEmitPer; ++u) {
-        const int i = i0 + u * istep;
-        if (i < p.N) {
-            v[u] = p.pos[base + i];
+        const int i = min(i0 + u * istep, p.N - 1);
+        v[u] = p.pos[base + i];
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch) c[u][ch] = ch < p.C ? p.col[(base + i) * p.C + ch] : 0.f;
-        }
+        for (int ch = 0; ch < 4; ++ch) c[u][ch] = ch < p.C ? p.col[(base + i) * p.C + ch] : 0.f;
     }
+    int old[kEmitPer];
 #pragma unroll
     for (int u = 0; u < kEmitPer; ++u) {
-        const int i = i0 + u * istep;
-        dst[u] = -1;
-        if (i < p.N) {
-            const int cx = cell_of_fast(static_cast<double>(v[u].x), g.ox, g.cell, inv, g.n_cols);
-            const int cy = cell_of_fast(static_cast<double>(v[u].y), g.oy, g.cell, inv, g.n_rows);
-            dst[u] = atomicSub(p.bins + g.bin_off + cy * g.n_cols + cx, 1) - 1;  // bin_grid.cpp:67
-            GMI_CHECK(dst[u] >= 0 && dst[u] < p.N);
-        }
+        const int cx = cell_of_fast(static_cast<double>(v[u].x), g.ox, g.cell, inv, g.n_cols);
+        const int cy = cell_of_fast(static_cast<double>(v[u].y), g.oy, g.cell, inv, g.n_rows);
+        old[u] = atomicSub(p.bins + g.bin_off + cy * g.n_cols + cx,
+                           i0 + u * istep < p.N ? 1 : 0);  // bin_grid.cpp:67
     }
+    uint32_t id[kEmitPer];
+    unsigned code[kEmitPer];
 #pragma unroll
     for (int u = 0; u < kEmitPer; ++u) {
         const int i = i0 + u * istep;
-        if (dst[u] < 0) continue;
-        unsigned code = 0;
+        code[u] = 0;
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
-            if (ch < p.C && code == 0) {
-                if (!is_finite_f(c[u][ch])) code = 1;                   // NonFiniteValue
-                else if (c[u][ch] < 0.0f || c[u][ch] > 1.0f) code = 2;  // ColorOutOfRange
+            if (ch < p.C && code[u] == 0) {
+                if (!is_finite_f(c[u][ch])) code[u] = 1;                   // NonFiniteValue
+                else if (c[u][ch] < 0.0f || c[u][ch] > 1.0f) code[u] = 2;  // ColorOutOfRange
             }
         }
+        const bool amb = p.classify && point_ambiguous_fast(v[u].x, v[u].y, p.rf, p.r2f);
+        id[u] = static_cast<uint32_t>(i) | (amb ? kUnsafeBit : 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < kEmitPer; ++u) {
+        const int i = i0 + u * istep;
+        if (i >= p.N) continue;
+        dst[u] = old[u] - 1;
+        GMI_CHECK(dst[u] >= 0 && dst[u] < p.N);
         if (p.ccol != nullptr) {
             // C > 4: every channel, validated in channel order, copied whole
             const float* src = p.col + (base + i) * p.C;
@@ -602,18 +611,15 @@ __global__ void __launch_bounds__(256) k_scatter_emit(ScatterEmitParams p) {
             for (int ch = 0; ch < p.C; ++ch) {
                 const float cv = src[ch];
                 dstc[ch] = cv;
-                if (code == 0) {
-                    if (!is_finite_f(cv)) code = 1;
-                    else if (cv < 0.0f || cv > 1.0f) code = 2;
+                if (code[u] == 0) {
+                    if (!is_finite_f(cv)) code[u] = 1;
+                    else if (cv < 0.0f || cv > 1.0f) code[u] = 2;
                 }
             }
         }
-        if (code) atomicMin(p.issue + b, (static_cast<unsigned long long>(i) << 8) | code);
-        const bool amb = p.classify && point_ambiguous_fast(v[u].x, v[u].y, p.rf, p.r2f);
-        const uint32_t id = static_cast<uint32_t>(i) | (amb ? kUnsafeBit : 0u);
-        float4* r = p.rec + (base + dst[u]) * 2;
-        r[0] = make_float4(v[u].x, v[u].y, c[u][0], c[u][1]);
-        r[1] = make_float4(c[u][2], c[u][3], __uint_as_float(id), 0.f);
+        if (code[u]) atomicMin(p.issue + b, (static_cast<unsigned long long>(i) << 8) | code[u]);
+        st_rec32(p.rec + (base + dst[u]) * 2, make_float4(v[u].x, v[u].y, c[u][0], c[u][1]),
+                 make_float4(c[u][2], c[u][3], __uint_as_float(id[u]), 0.f));
     }
 }
 
@@ -661,9 +667,8 @@ __global__ void __launch_bounds__(256) k_emit_rec(ScatterEmitParams p, const int
     if (code) atomicMin(p.issue + b, (static_cast<unsigned long long>(i) << 8) | code);
     const bool amb = p.classify && point_ambiguous_fast(v.x, v.y, p.rf, p.r2f);
     const uint32_t id = static_cast<uint32_t>(i) | (amb ? kUnsafeBit : 0u);
-    float4* r = p.rec + (base + k) * 2;
-    r[0] = make_float4(v.x, v.y, c4[0], c4[1]);
-    r[1] = make_float4(c4[2], c4[3], __uint_as_float(id), 0.f);
+    st_rec32(p.rec + (base + k) * 2, make_float4(v.x, v.y, c4[0], c4[1]),
+             make_float4(c4[2], c4[3], __uint_as_float(id), 0.f));
 }
 
 // Cells the fast gather may split across chunks (> its 640-candidate

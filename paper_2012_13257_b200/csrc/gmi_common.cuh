@@ -85,12 +85,19 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
     return y;
 }
 
-// Reciprocal on the SFU (MUFU.RCP, <= 1 ulp, flush-to-zero) without the
-// IEEE division's refinement and range fix-ups; callers pass W > 0 normals.
-__device__ __forceinline__ float rcp_approx(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
+// One 32-byte record as ONE 256-bit store (STG.E.ENL2.256): the sector is
+// written whole, so scattered record writes never leave half-written sectors
+// for the L2 to merge or read back.  p must be 32-byte aligned.
+__device__ __forceinline__ void st_rec32(float4* p, const float4 a, const float4 b) {
+    GMI_CHECK((reinterpret_cast<uintptr_t>(p) & 31) == 0);
+#ifdef GMI_REC_STORE128
+    p[0] = a;  // A/B: two 128-bit stores
+    p[1] = b;
+#else
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+                 :: "l"(p), "f"(a.x), "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
+                 : "memory");
+#endif
 }
 
 // Reference inclusion predicate (bin_grid.cpp:87,98; core.hpp:21-23):

@@ -49,17 +49,13 @@ namespace {
 #define GMI_GATHER_RPL 4
 #endif
 constexpr int kRPL = GMI_GATHER_RPL;
-#ifndef GMI_GATHER_NW
-#define GMI_GATHER_NW 8
-#endif
-constexpr int kNW = GMI_GATHER_NW;  // warps
+constexpr int kNW = 8;             // warps
 constexpr int kTW = 64, kTH = kNW * kRPL;
 constexpr int kNT = kNW * 32;      // threads
+constexpr int kCTAs = kRPL == 2 ? 4 : 3;  // resident CTAs per SM (registers, shared memory)
 // staged candidates per chunk (>= K1's kBigRecCell: cells above it are
 // index-ordered, so chunk membership never depends on arrival order)
-constexpr int kCap = kTH <= 16 ? 640 : 1024;
-// resident CTAs per SM (registers, shared memory)
-constexpr int kCTAs = kRPL == 2 ? 4 : (kNW == 8 ? 3 : 6);
+constexpr int kCap = kRPL == 2 ? 640 : 1024;
 constexpr int kRsMax = 32;         // cell-row runs per chunk
 constexpr int kColMax = 128;       // 1-px columns across the tile's reach
 constexpr int kBinMax = 2048;      // (column, row-pair) bins (+1 flag bin)
