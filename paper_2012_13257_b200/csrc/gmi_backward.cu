@@ -60,6 +60,8 @@ struct BwdParams {
     float inv_s2;
     float* d_col;           // [B][N][C]
     float* d_pos;           // [B][N][2] or partial [G][B][N][2]
+    float4* gslot;          // large images: [B][N][2] gradients in SLOT order
+                            // (d_col[0..3], d_pos), permuted by k_permute_grads
 };
 
 __device__ __forceinline__ bool in_ref(int x, int y, float mx, float my, double r2_64) {
@@ -551,6 +553,16 @@ k_backward_points(BwdParams p) {
         }
         if (!live || sub != 0) continue;
         GMI_CHECK(i >= 0 && i < p.N);
+        if (p.gslot != nullptr) {
+            // large images: one 32-byte record at the point's slot (the
+            // block's points are runs of consecutive slots: full sectors);
+            // k_permute_grads moves it to the original index
+            st_rec32(p.gslot + (base + s) * 2,
+                     make_float4(dcs[0], CG > 1 ? dcs[1] : 0.f, CG > 2 ? dcs[2] : 0.f, CG > 3 ? dcs[3] : 0.f),
+                     make_float4(static_cast<float>(gxs * static_cast<double>(inv_s2)),
+                                 static_cast<float>(gy * static_cast<double>(inv_s2)), 0.f, 0.f));
+            continue;
+        }
         // each point's gradients land at its original index (random against
         // the cell order): as few store transactions as alignment allows
         float* dc = p.d_col + (base + i) * p.C + ch0;
@@ -578,6 +590,29 @@ k_backward_points(BwdParams p) {
             dp[1] = g2.y;
         }
     }
+}
+
+// Large images: gradients from slot order to the original point order.
+// Thread per point i: its slot from K1's inverse map, one 32-byte record
+// read (random, whole sectors), coalesced d_col / d_pos writes — instead of
+// the backward scattering partial sectors over a gradient array far larger
+// than L2 (read-modify-write traffic in DRAM).
+__global__ void __launch_bounds__(256) k_permute_grads(const float4* __restrict__ gslot,
+                                                       const int32_t* __restrict__ inv,
+                                                       float* __restrict__ d_col,
+                                                       float* __restrict__ d_pos, int N, int C,
+                                                       size_t total) {
+    const size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (k >= total) return;
+    const size_t base = k - k % N;
+    const int s = inv[k];
+    GMI_CHECK(s >= 0 && s < N);
+    float4 a, b;
+    ld_rec32(gslot + (base + s) * 2, a, b);
+    const float v[4] = {a.x, a.y, a.z, a.w};
+    for (int c = 0; c < C; ++c) d_col[k * C + c] = v[c];
+    d_pos[2 * k] = b.x;
+    d_pos[2 * k + 1] = b.y;
 }
 
 // d_pos = sum over channel groups, in group order (deterministic)
@@ -816,6 +851,10 @@ void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
         }
         return;
     }
+    // large images: gradients in slot order, then one permutation pass
+    const bool permute = c->inv != nullptr && c->rec != nullptr && groups == 1;
+    if (permute)
+        p.gslot = static_cast<float4*>(scratch(ctx, WS_PART, sizeof(float4) * 2 * c->B * c->N));
     if (nb_max > 0) {
         switch (CG) {
             case 1: launch_points<1>(ctx, p, nb_max, groups); break;
@@ -828,6 +867,18 @@ void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
         k_sum_groups<<<static_cast<unsigned>((n2 + 255) / 256), 256, 0, st>>>(part, d_positions, n2, groups);
         GMI_LAUNCHED(ctx);
     }
+    if (permute) {
+        const size_t total = static_cast<size_t>(c->B) * c->N;
+        k_permute_grads<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(
+            p.gslot, c->inv, d_colors, d_positions, c->N, c->C, total);
+        GMI_LAUNCHED(ctx);
+    }
+}
+
+bool slot_grads(int N, int C) {
+    const char* e = std::getenv("GMI_SLOT_GRADS_MIN_N");  // read per call (tests flip it)
+    const long min_n = e != nullptr ? std::atol(e) : (1L << 20);
+    return C <= 4 && N >= min_n;
 }
 
 void launch_special_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,

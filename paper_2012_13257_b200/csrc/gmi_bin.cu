@@ -392,6 +392,7 @@ struct EmitParams {
     int32_t* sidx;
     float* scol;
     unsigned long long* issue;
+    int32_t* inv;           // large images: slot of each original point (or null)
     int N, C;
     int classify;
     float rf, r2f;
@@ -544,6 +545,7 @@ struct ScatterEmitParams {
     float4* rec;
     float* ccol;   // C > 4: [B][N][C] colours in bin order
     unsigned long long* issue;
+    int32_t* inv;           // large images: slot of each original point (or null)
     int N, C;
     int classify;
     float rf, r2f;
@@ -618,6 +620,7 @@ __global__ void __launch_bounds__(256) k_scatter_emit(ScatterEmitParams p) {
             }
         }
         if (code[u]) atomicMin(p.issue + b, (static_cast<unsigned long long>(i) << 8) | code[u]);
+        if (p.inv != nullptr) p.inv[base + i] = dst[u];
         st_rec32(p.rec + (base + dst[u]) * 2, make_float4(v[u].x, v[u].y, c[u][0], c[u][1]),
                  make_float4(c[u][2], c[u][3], __uint_as_float(id[u]), 0.f));
     }
@@ -687,7 +690,8 @@ __global__ void __launch_bounds__(512) k_sort_big_recs(int N, const Geom* __rest
                                                        const int32_t* __restrict__ bins,
                                                        float4* __restrict__ rec,
                                                        const int2* __restrict__ big,
-                                                       const int32_t* __restrict__ big_count) {
+                                                       const int32_t* __restrict__ big_count,
+                                                       int32_t* __restrict__ inv) {
     extern __shared__ float4 sr[];  // [2 kBigRecSmem] records, then the keys
     unsigned long long* key = reinterpret_cast<unsigned long long*>(sr + 2 * kBigRecSmem);
     const int nbig = *big_count;
@@ -728,6 +732,7 @@ __global__ void __launch_bounds__(512) k_sort_big_recs(int N, const Geom* __rest
                 const int src = static_cast<int>(key[k] & 0xffffffffu);
                 R[2 * k] = sr[2 * src];
                 R[2 * k + 1] = sr[2 * src + 1];
+                if (inv != nullptr) inv[static_cast<size_t>(b) * N + rec_idx(sr[2 * src + 1])] = s + k;
             }
             __syncthreads();
         } else {
@@ -751,6 +756,10 @@ __global__ void __launch_bounds__(512) k_sort_big_recs(int N, const Geom* __rest
                     __syncthreads();
                 }
             }
+            if (inv != nullptr)
+                for (int k = threadIdx.x; k < n; k += blockDim.x)
+                    inv[static_cast<size_t>(b) * N + rec_idx(R[2 * k + 1])] = s + k;
+            __syncthreads();
         }
     }
 }
@@ -1031,6 +1040,8 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
         GMI_CUDA(cudaMemsetAsync(d_bigcount, 0, sizeof(int32_t), st));
         scan_segments(ctx, c->bins, seg_start, seg_len, c->geom_h.empty(), true, c->geom_d, d_big,
                       d_bigcount);
+        if (c->ccol == nullptr && slot_grads(N, c->C))
+            c->inv = static_cast<int32_t*>(cache_alloc(c, sizeof(int32_t) * BN));
         ScatterEmitParams e{};
         e.pos = p2;
         e.col = col;
@@ -1039,6 +1050,7 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
         e.rec = c->rec;
         e.ccol = c->ccol;
         e.issue = d_issue;
+        e.inv = c->inv;
         e.N = N;
         e.C = c->C;
         e.classify = classify ? 1 : 0;
@@ -1049,7 +1061,8 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
         // cells the gather may split: index order
         const int rsmem = kBigRecSmem * (2 * sizeof(float4) + sizeof(unsigned long long));
         GMI_SMEM_ONCE(ctx, k_sort_big_recs, rsmem);
-        k_sort_big_recs<<<ctx->num_sms, 512, rsmem, st>>>(N, c->geom_d, c->bins, c->rec, d_big, d_bigcount);
+        k_sort_big_recs<<<ctx->num_sms, 512, rsmem, st>>>(N, c->geom_d, c->bins, c->rec, d_big, d_bigcount,
+                                                           c->inv);
         GMI_LAUNCHED(ctx);
         host_trace("bin: scatter_emit launched");
         return;

@@ -100,6 +100,14 @@ __device__ __forceinline__ void st_rec32(float4* p, const float4 a, const float4
 #endif
 }
 
+// One 32-byte record as ONE 256-bit load (LDG.E.ENL2.256).
+__device__ __forceinline__ void ld_rec32(const float4* p, float4& a, float4& b) {
+    GMI_CHECK((reinterpret_cast<uintptr_t>(p) & 31) == 0);
+    asm volatile("ld.global.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                 : "l"(p));
+}
+
 // Reference inclusion predicate (bin_grid.cpp:87,98; core.hpp:21-23):
 //   (qx-mx)^2 + (qy-my)^2 <= r^2, f64, two roundings, no FMA.
 __device__ __forceinline__ double d2_ref(double qx, double qy, double mx,

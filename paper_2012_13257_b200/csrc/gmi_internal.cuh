@@ -174,6 +174,9 @@ struct gmi_cache {
     // sx/sy/sidx/scol, which stay null
     float4* rec = nullptr;    // [B][N][2]
     float* ccol = nullptr;    // C > 4: all colours [B][N][C] in bin order
+    // large images (slot_grads): slot of each original point, so the backward
+    // writes gradients in slot order and one gather pass permutes them
+    int32_t* inv = nullptr;   // [B][N]
     // per pixel
     float* wsum = nullptr;    // [B][H][W]; 0 => special pixel
     double* wsum64 = nullptr; // [B][H][W] f64 normaliser (precise mode only)
@@ -220,6 +223,11 @@ int host_axis_cells(double span, double cell, int cap);
 void launch_forward(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts);
 bool launch_gather_fast(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts);
 bool gather_fast_ok(const gmi_cache* c);
+// Gradients through slot order (gmi_backward.cu k_permute_grads) for images
+// whose per-image gradient array is far larger than L2 would want to merge
+// scattered partial-sector writes in: N >= GMI_SLOT_GRADS_MIN_N (default
+// 2^20) points per image, C <= 4 (the record layout's single channel group).
+bool slot_grads(int N, int C);
 // wide-channel path (C > 4, gmi_wide.cu); false when it does not apply
 bool launch_gather_wide(gmi_ctx* ctx, gmi_cache* c, float* image, int32_t* counts);
 bool launch_backward_wide(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,

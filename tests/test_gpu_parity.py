@@ -243,6 +243,32 @@ def test_huge_cutoff_underflow_exact_path(gmi, ctx, orc):
     check_instance(gmi, ctx, orc, pos, col, 24, 20, 0.5, 60.0)
 
 
+@pytest.mark.parametrize("ch,n,cluster", [(1, 1200, 0.0), (3, 1200, 0.0), (4, 1200, 0.0),
+                                          (3, 6000, 0.5)])
+def test_slot_order_gradients_identical(gmi, ctx, orc, monkeypatch, ch, n, cluster):
+    # large images route gradients through slot order + one permutation pass
+    # (GMI_SLOT_GRADS_MIN_N, default 2^20 points per image); forced on here at
+    # a small size, it must give bit-identical gradients to the direct path,
+    # fallback routing (nearest) included, and match the oracle; the
+    # clustered case has cells above the gather's chunk capacity, whose
+    # records K1 re-sorts (the inverse map follows them)
+    pos, col, up = orc.synth_batch(21, 2, n, ch, 120, 100, cluster, 8)
+    outs = []
+    for env in ("1", None):
+        if env is None:
+            monkeypatch.delenv("GMI_SLOT_GRADS_MIN_N", raising=False)
+        else:
+            monkeypatch.setenv("GMI_SLOT_GRADS_MIN_N", env)
+        img, cache = gmi.forward_batch(pos, col, 120, 100, 1.5, 4.5, ctx=ctx)
+        dc, dp = gmi.backward_batch(pos, col, cache, up, 1.5, 4.5, ctx=ctx)
+        outs.append((img, dc, dp))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1]), "d_colors differ between slot-order and direct paths"
+    assert np.array_equal(outs[0][2], outs[1][2]), "d_positions differ between slot-order and direct paths"
+    monkeypatch.setenv("GMI_SLOT_GRADS_MIN_N", "1")
+    check_instance(gmi, ctx, orc, pos[1], col[1], 120, 100, 1.5, 4.5)
+
+
 def test_batch_equals_single_calls(gmi, ctx, orc):
     pos, col, up = orc.synth_batch(11, 3, 3000, 3, 100, 90)
     img, cache = gmi.forward_batch(pos, col, 100, 90, 1.0, 3.0, ctx=ctx)
