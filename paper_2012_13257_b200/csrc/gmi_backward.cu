@@ -21,6 +21,7 @@
 // K5 — fallback pixels under NearestPoint route their upstream to the nearest
 // point's colour (engine.cpp:200-211).
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 
@@ -691,15 +692,22 @@ struct SpecBwdParams {
 
 // engine.cpp:200-211: fallback pixels route their upstream to the nearest
 // point's colour only (no position gradient).  Sparse inputs route hundreds
-// of O(1) upstream values into one point, so the sum is formed in f64 and
-// added to the point's fp32 d_col with ONE rounding (fp32 atomics would carry
-// their rounding — and their nondeterministic order — into a cancellation of
-// ~1e-2).  Three passes with fixed grids that read the special count on the
-// device (no host round trip, capturable in a CUDA graph), touching only the
-// routed points: zero their f64 slots and owner marks, accumulate, then the
-// entry that won the owner mark (the largest list position, unique whatever
-// the arrival order) adds the point's sum once.  f64 sums of fp32 upstream
-// values are exact in practice, so the result does not depend on the order.
+// of O(1) upstream values into one point, whose sum may cancel to ~1e-2, so
+// it is formed exactly-ordered-independent and added to the point's fp32
+// d_col with ONE rounding.  Deterministic by construction: each routed
+// value is converted to a 64-bit FIXED-POINT integer on a per-(point,
+// channel) scale — 2^(60 - hb - emax), emax the largest exponent among the
+// point's routed values and 2^hb > their count, so no sum can overflow — and
+// summed with integer atomics, which commute.  Terms below 2^-(60 - hb) of the
+// largest one are rounded to that resolution (~1e-15 relative for hundreds of
+// terms); a non-finite value switches its (point, channel) to an f64 sum,
+// whose inf / NaN result does not depend on the order either.  Four passes
+// with fixed grids that read the special count on the device (no host round
+// trip, capturable in a CUDA graph), touching only the routed points: reset
+// their slots, statistics (count, owner = largest list position, exponent
+// maxima), accumulate, then the owner entry adds the point's sum once.
+constexpr int kNonFinite = 0x7fffffff;  // emax sentinel: f64 sum instead
+
 __device__ __forceinline__ bool special_route(const SpecBwdParams& p, int si, size_t& pixb,
                                               size_t& pt) {
     const Special sp = p.special[si];
@@ -709,17 +717,29 @@ __device__ __forceinline__ bool special_route(const SpecBwdParams& p, int si, si
     return true;
 }
 
-__global__ void k_special_zero(SpecBwdParams p, double* __restrict__ acc, int* __restrict__ own) {
+// fixed-point shift of a (point, channel): |v| < 2^(emax+1), count < 2^hb
+__device__ __forceinline__ int special_shift(int emax, int count) {
+    const int hb = 32 - __clz(count);
+    return 60 - hb - emax;
+}
+
+__global__ void k_special_zero(SpecBwdParams p, unsigned long long* __restrict__ acc,
+                               int* __restrict__ emax, int* __restrict__ own, int* __restrict__ cnt) {
     const int n = min(*p.special_count, p.special_cap);
     for (int si = blockIdx.x * blockDim.x + threadIdx.x; si < n; si += gridDim.x * blockDim.x) {
         size_t pixb, pt;
         if (!special_route(p, si, pixb, pt)) continue;
         own[pt] = -1;
-        for (int c = 0; c < p.C; ++c) acc[pt * p.C + c] = 0.0;
+        cnt[pt] = 0;
+        for (int c = 0; c < p.C; ++c) {
+            acc[pt * p.C + c] = 0ull;
+            emax[pt * p.C + c] = INT_MIN;
+        }
     }
 }
 
-__global__ void k_special_accumulate(SpecBwdParams p, double* __restrict__ acc, int* __restrict__ own) {
+__global__ void k_special_stats(SpecBwdParams p, int* __restrict__ emax, int* __restrict__ own,
+                                int* __restrict__ cnt) {
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -727,14 +747,45 @@ __global__ void k_special_accumulate(SpecBwdParams p, double* __restrict__ acc, 
     for (int si = warp; si < n; si += nwarps) {
         size_t pixb, pt;
         if (!special_route(p, si, pixb, pt)) continue;
-        if (lane == 0) atomicMax(own + pt, si);
-        for (int c = lane; c < p.C; c += 32)
-            atomicAdd(acc + pt * p.C + c, static_cast<double>(p.upstream[pixb * p.C + c]));
+        if (lane == 0) {
+            atomicMax(own + pt, si);
+            atomicAdd(cnt + pt, 1);
+        }
+        for (int c = lane; c < p.C; c += 32) {
+            const float v = p.upstream[pixb * p.C + c];
+            if (v != 0.f) atomicMax(emax + pt * p.C + c, is_finite_f(v) ? ilogbf(v) : kNonFinite);
+        }
     }
 }
 
-__global__ void k_special_merge(SpecBwdParams p, const double* __restrict__ acc,
-                                const int* __restrict__ own) {
+__global__ void k_special_accumulate(SpecBwdParams p, unsigned long long* __restrict__ acc,
+                                     const int* __restrict__ emax, const int* __restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int n = min(*p.special_count, p.special_cap);
+    for (int si = warp; si < n; si += nwarps) {
+        size_t pixb, pt;
+        if (!special_route(p, si, pixb, pt)) continue;
+        const int count = cnt[pt];
+        for (int c = lane; c < p.C; c += 32) {
+            const float v = p.upstream[pixb * p.C + c];
+            const int e = emax[pt * p.C + c];
+            if (v == 0.f || e == INT_MIN) continue;
+            unsigned long long* a = acc + pt * p.C + c;
+            if (e == kNonFinite) {
+                atomicAdd(reinterpret_cast<double*>(a), static_cast<double>(v));
+            } else {
+                const long long t = llrint(ldexp(static_cast<double>(v), special_shift(e, count)));
+                atomicAdd(a, static_cast<unsigned long long>(t));
+            }
+        }
+    }
+}
+
+__global__ void k_special_merge(SpecBwdParams p, const unsigned long long* __restrict__ acc,
+                                const int* __restrict__ emax, const int* __restrict__ own,
+                                const int* __restrict__ cnt) {
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -743,8 +794,15 @@ __global__ void k_special_merge(SpecBwdParams p, const double* __restrict__ acc,
         size_t pixb, pt;
         if (!special_route(p, si, pixb, pt) || own[pt] != si) continue;
         for (int c = lane; c < p.C; c += 32) {
+            const int e = emax[pt * p.C + c];
+            if (e == INT_MIN) continue;  // all routed values were 0
+            const unsigned long long a = acc[pt * p.C + c];
+            const double sum = e == kNonFinite
+                                   ? __longlong_as_double(static_cast<long long>(a))
+                                   : ldexp(static_cast<double>(static_cast<long long>(a)),
+                                           -special_shift(e, cnt[pt]));
             float* d = p.d_col + pt * p.C + c;
-            *d = static_cast<float>(static_cast<double>(*d) + acc[pt * p.C + c]);
+            *d = static_cast<float>(static_cast<double>(*d) + sum);
         }
     }
 }
@@ -898,14 +956,19 @@ void launch_special_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upst
     if (c->special_count == 0 || c->fallback != GMI_FALLBACK_NEAREST) return;
     const size_t npt = static_cast<size_t>(c->B) * c->N;
     // slots touched only for routed points (never cleared wholesale)
-    double* acc = static_cast<double*>(scratch(ctx, WS_PART, sizeof(double) * npt * c->C));
-    int* own = static_cast<int*>(scratch(ctx, WS_TMP, sizeof(int) * npt));
+    auto* acc = static_cast<unsigned long long*>(
+        scratch(ctx, WS_PART, sizeof(unsigned long long) * npt * c->C));
+    int* emax = static_cast<int*>(scratch(ctx, WS_RANK, sizeof(int) * npt * c->C));
+    int* own = static_cast<int*>(scratch(ctx, WS_TMP, sizeof(int) * 2 * npt));
+    int* cnt = own + npt;
     const int grid = 8 * ctx->num_sms;  // many routed pixels in flight (dependent loads)
-    k_special_zero<<<grid, 256, 0, ctx->stream>>>(p, acc, own);
+    k_special_zero<<<grid, 256, 0, ctx->stream>>>(p, acc, emax, own, cnt);
     GMI_LAUNCHED(ctx);
-    k_special_accumulate<<<grid, 256, 0, ctx->stream>>>(p, acc, own);
+    k_special_stats<<<grid, 256, 0, ctx->stream>>>(p, emax, own, cnt);
     GMI_LAUNCHED(ctx);
-    k_special_merge<<<grid, 256, 0, ctx->stream>>>(p, acc, own);
+    k_special_accumulate<<<grid, 256, 0, ctx->stream>>>(p, acc, emax, cnt);
+    GMI_LAUNCHED(ctx);
+    k_special_merge<<<grid, 256, 0, ctx->stream>>>(p, acc, emax, own, cnt);
     GMI_LAUNCHED(ctx);
 }
 

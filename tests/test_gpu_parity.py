@@ -292,6 +292,40 @@ def test_deterministic_repeat(gmi, ctx, orc, C, sigma):
     assert np.array_equal(ga[0], gb[0]) and np.array_equal(ga[1], gb[1])
 
 
+def test_fallback_routing_fixed_point_sums(gmi, ctx, orc):
+    # K5: a sparse frame routes hundreds of upstream values of wildly mixed
+    # magnitude and sign into each point; the fixed-point sums must match the
+    # oracle's f64 sums at the north-star tolerance, be bit-identical across
+    # calls, and carry an infinite upstream through as the reference does
+    rng = np.random.default_rng(8)
+    n, w, h = 12, 90, 70
+    pos = f32(np.stack([rng.uniform(0, w, n), rng.uniform(0, h, n)], 1))
+    col = f32(rng.uniform(0, 1, (n, 3)))
+    up = rng.uniform(-1, 1, (h, w, 3)) * 10.0 ** rng.integers(-8, 4, (h, w, 3))
+    up = f32(up)
+    p32, c32 = pos.astype(np.float32)[None], col.astype(np.float32)[None]
+    img, cache = gmi.forward_batch(p32, c32, w, h, 1.0, 3.0, ctx=ctx)
+    dc1, dp1 = gmi.backward_batch(p32, c32, cache, up.astype(np.float32)[None], 1.0, 3.0, ctx=ctx)
+    dc2, dp2 = gmi.backward_batch(p32, c32, cache, up.astype(np.float32)[None], 1.0, 3.0, ctx=ctx)
+    assert np.array_equal(dc1, dc2) and np.array_equal(dp1, dp2)
+    r = orc.forward(pos, col, w, h, 1.0, 3.0, 0)
+    assert r["fallback_flag"].sum() > 0.8 * w * h
+    rdc, rdp = orc.backward(pos, col, r, up, 1.0, 3.0, 0)
+    # (d_colors only: K5 routes no position gradient, and 1e3-sized upstream
+    # values cancelling in the disk sums are outside the fp32 path's envelope)
+    assert_close(dc1[0], rdc, what="d_colors")
+    # one infinite upstream on a fallback pixel: its point's channel is inf
+    fy, fx = np.argwhere(r["fallback_flag"] == 1)[0]
+    up_inf = up.copy()
+    up_inf[fy, fx, 1] = np.inf
+    dci, _ = gmi.backward_batch(p32, c32, cache, up_inf.astype(np.float32)[None], 1.0, 3.0, ctx=ctx)
+    k = r["nearest_index"][fy, fx]
+    assert np.isposinf(dci[0, k, 1])
+    rest = np.ones_like(dci[0], bool)
+    rest[k, 1] = False
+    assert np.array_equal(dci[0][rest], dc1[0][rest])
+
+
 def test_smoke_entry():
     import __graft_entry__
 
