@@ -764,6 +764,45 @@ __global__ void __launch_bounds__(512) k_sort_big_recs(int N, const Geom* __rest
     }
 }
 
+// Cell counts with a private shared-memory histogram (device geometry whose
+// cell grid fits shared memory, e.g. configs[1]/[2]): CTA = one slice of one
+// image's points, 1024 threads, the whole grid's counters in shared memory
+// (native shared atomics instead of random L2 reductions), then one
+// coalesced reduction per non-empty cell.  Same counts as k_count_red.
+constexpr int kCountSmemCells = 56 * 1024;  // 224 KB of counters
+
+__global__ void __launch_bounds__(1024, 1) k_count_smem(const float2* __restrict__ pos, int N,
+                                                       const Geom* __restrict__ geom,
+                                                       int32_t* __restrict__ bins, int parts) {
+    extern __shared__ int hist[];
+    const int b = blockIdx.y, tid = threadIdx.x;
+    const Geom g = geom[b];
+    const double inv = 1.0 / g.cell;
+    const int cells = g.n_cols * g.n_rows;
+    for (int k = tid; k < cells; k += blockDim.x) hist[k] = 0;
+    __syncthreads();
+    const size_t base = static_cast<size_t>(b) * N;
+    const int per = (N + parts - 1) / parts;
+    const int i_beg = blockIdx.x * per, i_end = min(N, i_beg + per);
+    for (int i = i_beg + tid; i < i_end; i += 4 * blockDim.x) {
+        float2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = pos[base + min(i + u * static_cast<int>(blockDim.x), i_end - 1)];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (i + u * static_cast<int>(blockDim.x) >= i_end) continue;
+            const int cx = cell_of_fast(static_cast<double>(v[u].x), g.ox, g.cell, inv, g.n_cols);
+            const int cy = cell_of_fast(static_cast<double>(v[u].y), g.oy, g.cell, inv, g.n_rows);
+            atomicAdd(&hist[cy * g.n_cols + cx], 1);  // bin_grid.cpp:67
+        }
+    }
+    __syncthreads();
+    for (int k = tid; k < cells; k += blockDim.x) {
+        const int h = hist[k];
+        if (h != 0) atomicAdd(bins + g.bin_off + k, h);
+    }
+}
+
 // Cell counts only (fire-and-forget reductions, no ranks stored): the fast
 // path's count pass; k_scatter_emit recomputes the cell and takes its slot.
 // Counts with 16-byte position loads (two points each) and kCountPer
@@ -1028,8 +1067,18 @@ void bin_points(gmi_ctx* ctx, gmi_cache* c, const float* pos, const float* col,
     if (hot && !c->sort_cells) {
         // fast path: counts -> inclusive scan (cell ends) -> 32-byte records
         // at slots taken from the ends, which leaves bin_start behind
-        k_count_red<<<dim3((N + 256 * kCountPer - 1) / (256 * kCountPer), B), 256, 0, st>>>(
-            p2, N, c->geom_d, c->bins);
+        if (c->geom_h.empty() && static_cast<int64_t>(c->grid_cap) * c->grid_cap <= kCountSmemCells &&
+            std::getenv("GMI_K1_COUNT_RED") == nullptr) {
+            // every image's grid fits shared memory: private histograms,
+            // about one wave of CTAs (slices of the images' points)
+            const int parts = std::max(1, std::min((N + 8191) / 8192, (ctx->num_sms + B - 1) / B));
+            const int smem = static_cast<int>(sizeof(int) * c->grid_cap * c->grid_cap);
+            GMI_SMEM_ONCE(ctx, k_count_smem, kCountSmemCells * static_cast<int>(sizeof(int)));
+            k_count_smem<<<dim3(parts, B), 1024, smem, st>>>(p2, N, c->geom_d, c->bins, parts);
+        } else {
+            k_count_red<<<dim3((N + 256 * kCountPer - 1) / (256 * kCountPer), B), 256, 0, st>>>(
+                p2, N, c->geom_d, c->bins);
+        }
         GMI_LAUNCHED(ctx);
         host_trace("bin: count launched");
         // cells the gather may split (> its chunk capacity) are listed by the

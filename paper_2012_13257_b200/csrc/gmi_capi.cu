@@ -211,15 +211,24 @@ void join_copy_streams(gmi_ctx* ctx) {
 // one — stream order makes "earlier" the call order, so gmi_ctx_synchronize
 // reports the first error since it last ran (pending == null: the caller
 // collects the call's issues itself).
+// One warp: the images' issue slots 32 at a time (ballot -> first failing
+// image), so the check costs one round trip per 32 images, not one per image.
 __global__ void k_async_check(const int32_t* count, int cap, unsigned long long* issue, int B,
                               int b0, unsigned long long* pending) {
-    if (*count > cap)
+    const int lane = threadIdx.x;
+    if (lane == 0 && *count > cap)
         atomicMin(issue, (static_cast<unsigned long long>(cap) << 8) | GMI_ERR_OUT_OF_MEMORY);
+    __syncwarp();
     if (pending == nullptr || pending[0] != gmi_dev::kNoIssue) return;
-    for (int b = 0; b < B; ++b) {
-        if (issue[b] != gmi_dev::kNoIssue) {
-            pending[0] = issue[b];
-            pending[1] = static_cast<unsigned long long>(b0 + b);
+    for (int b1 = 0; b1 < B; b1 += 32) {
+        const int b = b1 + lane;
+        const unsigned long long k = b < B ? issue[b] : gmi_dev::kNoIssue;
+        const unsigned bad = __ballot_sync(0xffffffffu, k != gmi_dev::kNoIssue);
+        if (bad != 0u) {
+            if (lane == __ffs(bad) - 1) {
+                pending[0] = k;
+                pending[1] = static_cast<unsigned long long>(b0 + b);
+            }
             return;
         }
     }
@@ -397,7 +406,7 @@ int do_forward(gmi_ctx* ctx, const float* pos, const float* col, int B, int N,
     if ((ctx->flags & GMI_CTX_ASYNC_ERRORS) && counts == nullptr) {
         // no host check below: a fallback list overflow becomes a pending
         // error reported by gmi_ctx_synchronize
-        k_async_check<<<1, 1, 0, ctx->stream>>>(c->special_count_d, c->special_cap, d_issue, B,
+        k_async_check<<<1, 32, 0, ctx->stream>>>(c->special_count_d, c->special_cap, d_issue, B,
                                                 static_cast<int>(d_issue - ctx->d_issue),
                                                 ctx->collect_now ? nullptr : ctx->d_pending);
         GMI_LAUNCHED(ctx);
