@@ -8,7 +8,7 @@ import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 20
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kern}",
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kern}", "--launch-count", "1",
                       "--print-source=sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 h = rows[1]
@@ -25,6 +25,7 @@ for r in rows[2:]:
         continue
     if w:
         data.append((w, int(r[ie] or 0), int(r[ii] or 0), int(r[iex] or 0), r[isrc].strip()))
+data = sorted(set(data))  # the source page can list an instruction twice
 tot = sum(d[0] for d in data) or 1
 print(f"{kern}: shared wavefronts {tot}, excess {sum(d[1] for d in data)}, ideal {sum(d[2] for d in data)}")
 for w, e, i, n, s in sorted(data, reverse=True)[:top]:

@@ -10,7 +10,7 @@ res = {}
 for r in rows[2:]:
     name = r[h.index("Kernel Name")]
     key = next((v for k, v in (("k_backward_points", "points_bwd"), ("k_gather", "gather"),
-                               ("k_scatter_emit", "scatter_emit"), ("k_count_red", "count"),
+                               ("k_scatter_emit", "scatter_emit"), ("k_count_red", "count"), ("k_count_smem", "count"),
                                ("k_bbox_validate", "bbox")) if k in name), name[:40])
     units = rows[1]
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
