@@ -24,6 +24,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 #include "gmi_internal.cuh"
 
@@ -437,11 +438,14 @@ k_backward_points(BwdParams p) {
         const int ya = max(ry0, static_cast<int>(ceilf(my - rf - pad))) + sub;
         const int yb = live ? min(ry1, static_cast<int>(floorf(my + rf + pad))) : ya - 1;
 
+        // the disk walk, compiled twice: warps without a flagged point (all
+        // but ~0.3% at random inputs) run a copy with no f64 branch in it
+        auto walk = [&](auto safe_only, auto staged_c) {
         float yf = static_cast<float>(ya);  // exact row coordinate
         for (int y = ya; y <= yb; y += lpp, yf += static_cast<float>(lpp)) {
             float dy;
             int xl, xr;
-            if (!unsafe) {
+            if (decltype(safe_only)::value || !unsafe) {
                 // safe point: fp32 row geometry decides the reference's ball;
                 // dy = y - my is the forward's own operation (bit-identical)
                 dy = yf - my;
@@ -476,7 +480,7 @@ k_backward_points(BwdParams p) {
             // e = nk dx^2 + nk dy^2 with the forward's fp32 operations, so a
             // pair's weight is bit-identical to the one summed into W
             const float ey = (dy * nk) * dy;
-            if (!staged) {
+            if (!decltype(staged_c)::value) {
                 float gyr = 0.f, gxr = 0.f;
                 for (int x = xl; x <= xr; ++x) {
                     const float dx = static_cast<float>(x) - mx;
@@ -542,6 +546,15 @@ k_backward_points(BwdParams p) {
             gx += static_cast<double>(gx2.x + gx2.y);
             gy = fma(static_cast<double>(gyr2.x + gyr2.y), static_cast<double>(dy), gy);
         }
+        };
+#ifndef GMI_BWD_NO_SAFE_SPLIT
+        if (!staged) walk(std::false_type{}, std::false_type{});
+        else if (__any_sync(__activemask(), unsafe)) walk(std::false_type{}, std::true_type{});
+        else walk(std::true_type{}, std::true_type{});
+#else
+        if (!staged) walk(std::false_type{}, std::false_type{});
+        else walk(std::false_type{}, std::true_type{});
+#endif
         double gxs = gx;
         float dcs[CG];
 #pragma unroll
