@@ -59,6 +59,7 @@ struct BwdParams {
     int bs;                 // cells per block side
     double r64, r2_64;
     float nk;               // -log2(e) / (2 sigma^2)
+    float r2f;              // float(r^2) (kept in the constant bank: no per-row conversion)
     float inv_s2;
     float* d_col;           // [B][N][C]
     float* d_pos;           // [B][N][2] or partial [G][B][N][2]
@@ -360,7 +361,7 @@ k_backward_points(BwdParams p) {
 
     // ---- per point ----
     const float nk = p.nk, inv_s2 = p.inv_s2;
-    const float r2f = static_cast<float>(p.r2_64), rf = static_cast<float>(p.r64);
+    const float r2f = p.r2f, rf = static_cast<float>(p.r64);
     const double r2_64 = p.r2_64;
     const int xmin = max(rx0, 0), xmax = min(rx1, p.W - 1);
     const float2 nk2 = f2(nk, nk), two = f2(2.f, 2.f);
@@ -509,7 +510,8 @@ k_backward_points(BwdParams p) {
             const int np = ((xr - xs) >> 1) + 1;
             const float mf = ((xl - rx0) & 1) ? 0.f : 1.f;
             const float ml = ((xr - rx0) & 1) ? 1.f : 0.f;
-            float2 X = f2(static_cast<float>(xs), static_cast<float>(xs + 1));
+            const float xsf = static_cast<float>(xs);
+            float2 X = f2(xsf, xsf + 1.f);  // |x| < 2^24: exact
             const float2 ey2 = f2(ey, ey), mmx = f2(-mx, -mx);
             float2 gyr2 = f2(0.f, 0.f), gx2 = f2(0.f, 0.f);
             const float4* pr = s_pair + (y - ry0) * npairs + ((xs - rx0) >> 1);
@@ -894,6 +896,7 @@ void launch_backward(gmi_ctx* ctx, const gmi_cache* c, const float* upstream,
     p.bs = bs;
     p.r64 = c->cutoff;
     p.r2_64 = c->cutoff * c->cutoff;
+    p.r2f = static_cast<float>(p.r2_64);
     const double nk = -1.4426950408889634 / (2.0 * c->sigma * c->sigma);
     p.nk = static_cast<float>(nk);
     p.inv_s2 = static_cast<float>(1.0 / (c->sigma * c->sigma));
