@@ -32,8 +32,12 @@ using namespace gmi_dev;
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kSmemBudget = 52 * 1024;  // staged pixel bytes per CTA (4 CTAs/SM)
+#ifndef GMI_BWD_WARPS
+#define GMI_BWD_WARPS 8
+#endif
+constexpr int kThreads = 32 * GMI_BWD_WARPS;
+constexpr int kCtasPerSm = 32 / GMI_BWD_WARPS;  // 64 registers: 32 warps per SM
+constexpr int kSmemBudget = 52 * 1024 * (4 / kCtasPerSm);  // staged pixel bytes per CTA (4 CTAs/SM: 52 KB)
 constexpr int kRunMax = 64;             // cell rows per block
 #ifndef GMI_BWD_STAGE_UNROLL
 #define GMI_BWD_STAGE_UNROLL 1
@@ -107,7 +111,7 @@ __device__ __forceinline__ void pixel_terms(const BwdParams& p, size_t img_base,
 }
 
 template <int CG, int LPP>
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
 k_backward_points(BwdParams p) {
     using L = PairLayout<CG>;
     extern __shared__ float4 s_pair[];   // [L::kF4][rows][pairs]
