@@ -292,7 +292,8 @@ def test_deterministic_repeat(gmi, ctx, orc, C, sigma):
     assert np.array_equal(ga[0], gb[0]) and np.array_equal(ga[1], gb[1])
 
 
-def test_fallback_routing_fixed_point_sums(gmi, ctx, orc):
+@pytest.mark.parametrize("ch", [1, 3, 6])
+def test_fallback_routing_fixed_point_sums(gmi, ctx, orc, ch):
     # K5: a sparse frame routes hundreds of upstream values of wildly mixed
     # magnitude and sign into each point; the fixed-point sums must match the
     # oracle's f64 sums at the north-star tolerance, be bit-identical across
@@ -300,8 +301,8 @@ def test_fallback_routing_fixed_point_sums(gmi, ctx, orc):
     rng = np.random.default_rng(8)
     n, w, h = 12, 90, 70
     pos = f32(np.stack([rng.uniform(0, w, n), rng.uniform(0, h, n)], 1))
-    col = f32(rng.uniform(0, 1, (n, 3)))
-    up = rng.uniform(-1, 1, (h, w, 3)) * 10.0 ** rng.integers(-8, 4, (h, w, 3))
+    col = f32(rng.uniform(0, 1, (n, ch)))
+    up = rng.uniform(-1, 1, (h, w, ch)) * 10.0 ** rng.integers(-8, 4, (h, w, ch))
     up = f32(up)
     p32, c32 = pos.astype(np.float32)[None], col.astype(np.float32)[None]
     img, cache = gmi.forward_batch(p32, c32, w, h, 1.0, 3.0, ctx=ctx)
@@ -317,12 +318,13 @@ def test_fallback_routing_fixed_point_sums(gmi, ctx, orc):
     # one infinite upstream on a fallback pixel: its point's channel is inf
     fy, fx = np.argwhere(r["fallback_flag"] == 1)[0]
     up_inf = up.copy()
-    up_inf[fy, fx, 1] = np.inf
+    cinf = ch - 1
+    up_inf[fy, fx, cinf] = np.inf
     dci, _ = gmi.backward_batch(p32, c32, cache, up_inf.astype(np.float32)[None], 1.0, 3.0, ctx=ctx)
     k = r["nearest_index"][fy, fx]
-    assert np.isposinf(dci[0, k, 1])
+    assert np.isposinf(dci[0, k, cinf])
     rest = np.ones_like(dci[0], bool)
-    rest[k, 1] = False
+    rest[k, cinf] = False
     assert np.array_equal(dci[0][rest], dc1[0][rest])
 
 
