@@ -16,10 +16,13 @@
 //     d_pos   += w * (sum_c c_ic u_c - v) * (q - mu) / sigma^2
 //                                     (= ratio * dot / sigma^2 * (q-mu), engine.cpp:219-230)
 // and writes each point's gradients once.  One owner per point: the result
-// is bit-deterministic with no atomics and no reduction pass.
+// is bit-deterministic with no atomics and no reduction pass.  Images of
+// >= 2^20 points write the gradients in slot order instead and
+// k_permute_grads moves them to the original indices (slot_grads).
 //
 // K5 — fallback pixels under NearestPoint route their upstream to the nearest
-// point's colour (engine.cpp:200-211).
+// point's colour (engine.cpp:200-211), summed in per-point fixed point
+// (deterministic whatever the arrival order).
 #include <algorithm>
 #include <climits>
 #include <cmath>
