@@ -113,6 +113,17 @@ __device__ __forceinline__ void pixel_terms(const BwdParams& p, size_t img_base,
     }
 }
 
+// d_positions across a point's disk rows: fp32.  Round 2 first summed the
+// rows in f64 (4 registers, 3 conversions + 2 f64 ops per row); the strict
+// fuzz shows no difference (same seeds: the same 0 images over 1x in the
+// BASELINE regimes, the same 42 contract-domain misses, worst 2.60x either
+// way) and fp32 is 0.026 ms faster at configs[2].  GMI_BWD_ROWS_F64 for A/B.
+#ifdef GMI_BWD_ROWS_F64
+using acc_t = double;
+#else
+using acc_t = float;
+#endif
+
 template <int CG, int LPP>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 k_backward_points(BwdParams p) {
@@ -427,9 +438,8 @@ k_backward_points(BwdParams p) {
         float2 dcol[CG];
 #pragma unroll
         for (int c = 0; c < CG; ++c) dcol[c] = f2(0.f, 0.f);
-        // d_pos: fp32 sums inside a row, f64 across rows (the row sums
-        // cancel; an fp32 total would carry their rounding)
-        double gx = 0.0, gy = 0.0;
+        // d_pos: per-row sums, then across rows in acc_t
+        acc_t gx = 0, gy = 0;
         const float tx = truncf(mx);
         const float fmu = mx - tx;  // exact
         const int bx = static_cast<int>(tx);
@@ -502,8 +512,8 @@ k_backward_points(BwdParams p) {
                     gxr = fmaf(a, dx, gxr);
                     gyr += a;
                 }
-                gx += static_cast<double>(gxr);
-                gy = fma(static_cast<double>(gyr), static_cast<double>(dy), gy);
+                gx += static_cast<acc_t>(gxr);
+                gy = fma(static_cast<acc_t>(gyr), static_cast<acc_t>(dy), gy);
                 continue;
             }
             // pair-aligned span (rx0 is even): pairs xs..xs+2(np-1); the end
@@ -547,8 +557,8 @@ k_backward_points(BwdParams p) {
                 X = __fadd2_rn(X, two);
                 ++pr;
             }
-            gx += static_cast<double>(gx2.x + gx2.y);
-            gy = fma(static_cast<double>(gyr2.x + gyr2.y), static_cast<double>(dy), gy);
+            gx += static_cast<acc_t>(gx2.x + gx2.y);
+            gy = fma(static_cast<acc_t>(gyr2.x + gyr2.y), static_cast<acc_t>(dy), gy);
         }
         };
 #ifndef GMI_BWD_NO_SAFE_SPLIT
@@ -559,7 +569,7 @@ k_backward_points(BwdParams p) {
         if (!staged) walk(std::false_type{}, std::false_type{});
         else walk(std::false_type{}, std::true_type{});
 #endif
-        double gxs = gx;
+        acc_t gxs = gx;
         float dcs[CG];
 #pragma unroll
         for (int c = 0; c < CG; ++c) dcs[c] = dcol[c].x + dcol[c].y;
@@ -577,8 +587,8 @@ k_backward_points(BwdParams p) {
             // k_permute_grads moves it to the original index
             st_rec32(p.gslot + (base + s) * 2,
                      make_float4(dcs[0], CG > 1 ? dcs[1] : 0.f, CG > 2 ? dcs[2] : 0.f, CG > 3 ? dcs[3] : 0.f),
-                     make_float4(static_cast<float>(gxs * static_cast<double>(inv_s2)),
-                                 static_cast<float>(gy * static_cast<double>(inv_s2)), 0.f, 0.f));
+                     make_float4(static_cast<float>(gxs * static_cast<acc_t>(inv_s2)),
+                                 static_cast<float>(gy * static_cast<acc_t>(inv_s2)), 0.f, 0.f));
             continue;
         }
         // each point's gradients land at its original index (random against
@@ -599,8 +609,8 @@ k_backward_points(BwdParams p) {
             for (int c = 0; c < nch; ++c) dc[c] = dcs[c];
         }
         float* dp = p.d_pos + (static_cast<size_t>(cg) * p.B * p.N + base + i) * 2;
-        const float2 g2 = f2(static_cast<float>(gxs * static_cast<double>(inv_s2)),
-                             static_cast<float>(gy * static_cast<double>(inv_s2)));
+        const float2 g2 = f2(static_cast<float>(gxs * static_cast<acc_t>(inv_s2)),
+                             static_cast<float>(gy * static_cast<acc_t>(inv_s2)));
         if ((reinterpret_cast<uintptr_t>(p.d_pos) & 7) == 0) {
             *reinterpret_cast<float2*>(dp) = g2;
         } else {
