@@ -113,17 +113,6 @@ __device__ __forceinline__ void pixel_terms(const BwdParams& p, size_t img_base,
     }
 }
 
-// d_positions across a point's disk rows: fp32.  Round 2 first summed the
-// rows in f64 (4 registers, 3 conversions + 2 f64 ops per row); the strict
-// fuzz shows no difference (same seeds: the same 0 images over 1x in the
-// BASELINE regimes, the same 42 contract-domain misses, worst 2.60x either
-// way) and fp32 is 0.026 ms faster at configs[2].  GMI_BWD_ROWS_F64 for A/B.
-#ifdef GMI_BWD_ROWS_F64
-using acc_t = double;
-#else
-using acc_t = float;
-#endif
-
 template <int CG, int LPP>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 k_backward_points(BwdParams p) {
@@ -438,8 +427,12 @@ k_backward_points(BwdParams p) {
         float2 dcol[CG];
 #pragma unroll
         for (int c = 0; c < CG; ++c) dcol[c] = f2(0.f, 0.f);
-        // d_pos: per-row sums, then across rows in acc_t
-        acc_t gx = 0, gy = 0;
+        // d_pos: fp32 pair sums over the whole disk, a * dx and a * dy per
+        // pixel (round 2 first formed per-row sums and folded them in f64;
+        // the strict fuzz shows no difference at the same seeds — the same 0
+        // images over 1x in the BASELINE regimes, the same contract-domain
+        // misses — and the per-row folds cost registers and ~10 SASS a row)
+        float2 gx2 = f2(0.f, 0.f), gy2 = f2(0.f, 0.f);
         const float tx = truncf(mx);
         const float fmu = mx - tx;  // exact
         const int bx = static_cast<int>(tx);
@@ -494,7 +487,6 @@ k_backward_points(BwdParams p) {
             // pair's weight is bit-identical to the one summed into W
             const float ey = (dy * nk) * dy;
             if (!decltype(staged_c)::value) {
-                float gyr = 0.f, gxr = 0.f;
                 for (int x = xl; x <= xr; ++x) {
                     const float dx = static_cast<float>(x) - mx;
                     const float w = ex2(fmaf(dx * nk, dx, ey));
@@ -509,11 +501,9 @@ k_backward_points(BwdParams p) {
                     const float a = w * t;
 #pragma unroll
                     for (int c = 0; c < CG; ++c) dcol[c].x = fmaf(w, u[c], dcol[c].x);
-                    gxr = fmaf(a, dx, gxr);
-                    gyr += a;
+                    gx2.x = fmaf(a, dx, gx2.x);
+                    gy2.x = fmaf(a, dy, gy2.x);
                 }
-                gx += static_cast<acc_t>(gxr);
-                gy = fma(static_cast<acc_t>(gyr), static_cast<acc_t>(dy), gy);
                 continue;
             }
             // pair-aligned span (rx0 is even): pairs xs..xs+2(np-1); the end
@@ -524,8 +514,7 @@ k_backward_points(BwdParams p) {
             const float ml = ((xr - rx0) & 1) ? 1.f : 0.f;
             const float xsf = static_cast<float>(xs);
             float2 X = f2(xsf, xsf + 1.f);  // |x| < 2^24: exact
-            const float2 ey2 = f2(ey, ey), mmx = f2(-mx, -mx);
-            float2 gyr2 = f2(0.f, 0.f), gx2 = f2(0.f, 0.f);
+            const float2 ey2 = f2(ey, ey), mmx = f2(-mx, -mx), dy2 = f2(dy, dy);
             const float4* pr = s_pair + (y - ry0) * npairs + ((xs - rx0) >> 1);
             GMI_CHECK(y >= ry0 && xs >= rx0 && (y - ry0) * npairs + ((xs - rx0) >> 1) + np <= area &&
                       area * L::kF4 * static_cast<int>(sizeof(float4)) <= kSmemBudget);
@@ -553,12 +542,10 @@ k_backward_points(BwdParams p) {
 #pragma unroll
                 for (int c = 0; c < CG; ++c) dcol[c] = __ffma2_rn(w, q[c], dcol[c]);
                 gx2 = __ffma2_rn(a, dx, gx2);
-                gyr2 = __fadd2_rn(gyr2, a);
+                gy2 = __ffma2_rn(a, dy2, gy2);
                 X = __fadd2_rn(X, two);
                 ++pr;
             }
-            gx += static_cast<acc_t>(gx2.x + gx2.y);
-            gy = fma(static_cast<acc_t>(gyr2.x + gyr2.y), static_cast<acc_t>(dy), gy);
         }
         };
 #ifndef GMI_BWD_NO_SAFE_SPLIT
@@ -569,7 +556,7 @@ k_backward_points(BwdParams p) {
         if (!staged) walk(std::false_type{}, std::false_type{});
         else walk(std::false_type{}, std::true_type{});
 #endif
-        acc_t gxs = gx;
+        float gxs = gx2.x + gx2.y, gy = gy2.x + gy2.y;
         float dcs[CG];
 #pragma unroll
         for (int c = 0; c < CG; ++c) dcs[c] = dcol[c].x + dcol[c].y;
@@ -587,8 +574,7 @@ k_backward_points(BwdParams p) {
             // k_permute_grads moves it to the original index
             st_rec32(p.gslot + (base + s) * 2,
                      make_float4(dcs[0], CG > 1 ? dcs[1] : 0.f, CG > 2 ? dcs[2] : 0.f, CG > 3 ? dcs[3] : 0.f),
-                     make_float4(static_cast<float>(gxs * static_cast<acc_t>(inv_s2)),
-                                 static_cast<float>(gy * static_cast<acc_t>(inv_s2)), 0.f, 0.f));
+                     make_float4(gxs * inv_s2, gy * inv_s2, 0.f, 0.f));
             continue;
         }
         // each point's gradients land at its original index (random against
@@ -609,8 +595,7 @@ k_backward_points(BwdParams p) {
             for (int c = 0; c < nch; ++c) dc[c] = dcs[c];
         }
         float* dp = p.d_pos + (static_cast<size_t>(cg) * p.B * p.N + base + i) * 2;
-        const float2 g2 = f2(static_cast<float>(gxs * static_cast<acc_t>(inv_s2)),
-                             static_cast<float>(gy * static_cast<acc_t>(inv_s2)));
+        const float2 g2 = f2(gxs * inv_s2, gy * inv_s2);
         if ((reinterpret_cast<uintptr_t>(p.d_pos) & 7) == 0) {
             *reinterpret_cast<float2*>(dp) = g2;
         } else {
