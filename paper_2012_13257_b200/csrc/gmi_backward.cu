@@ -448,7 +448,10 @@ k_backward_points(BwdParams p) {
         // but ~0.3% at random inputs) run a copy with no f64 branch in it
         auto walk = [&](auto safe_only, auto staged_c) {
         float yf = static_cast<float>(ya);  // exact row coordinate
-        for (int y = ya; y <= yb; y += lpp, yf += static_cast<float>(lpp)) {
+        // the row's staged pairs, advanced with the row (ya >= ry0 when the
+        // region is staged; unused otherwise)
+        const float4* rowp = s_pair + (ya - ry0) * npairs;
+        for (int y = ya; y <= yb; y += lpp, yf += static_cast<float>(lpp), rowp += lpp * npairs) {
             float dy;
             int xl, xr;
             if (decltype(safe_only)::value || !unsafe) {
@@ -515,7 +518,7 @@ k_backward_points(BwdParams p) {
             const float xsf = static_cast<float>(xs);
             float2 X = f2(xsf, xsf + 1.f);  // |x| < 2^24: exact
             const float2 ey2 = f2(ey, ey), mmx = f2(-mx, -mx), dy2 = f2(dy, dy);
-            const float4* pr = s_pair + (y - ry0) * npairs + ((xs - rx0) >> 1);
+            const float4* pr = rowp + ((xs - rx0) >> 1);
             GMI_CHECK(y >= ry0 && xs >= rx0 && (y - ry0) * npairs + ((xs - rx0) >> 1) + np <= area &&
                       area * L::kF4 * static_cast<int>(sizeof(float4)) <= kSmemBudget);
 #pragma unroll 1
