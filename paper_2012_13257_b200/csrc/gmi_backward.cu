@@ -521,8 +521,13 @@ k_backward_points(BwdParams p) {
             const float4* pr = rowp + ((xs - rx0) >> 1);
             GMI_CHECK(y >= ry0 && xs >= rx0 && (y - ry0) * npairs + ((xs - rx0) >> 1) + np <= area &&
                       area * L::kF4 * static_cast<int>(sizeof(float4)) <= kSmemBudget);
+            // np >= 1 (xl <= xr): a do-while on the pair pointer; the last-pair
+            // test doubles as the loop condition
+            const float4* const p0 = pr;
+            const float4* const plast = pr + (np - 1);
 #pragma unroll 1
-            for (int j = 0; j < np; ++j) {
+            do {
+                const bool last = pr == plast;
                 float4 q4[L::kF4];
 #pragma unroll
                 for (int c = 0; c < L::kF4; ++c) q4[c] = pr[c * area];
@@ -530,8 +535,8 @@ k_backward_points(BwdParams p) {
                 const float2 dx = __fadd2_rn(X, mmx);
                 const float2 arg = __ffma2_rn(__fmul2_rn(dx, nk2), dx, ey2);
                 float2 w = f2(ex2(arg.x), ex2(arg.y));
-                if (j == 0) w.x *= mf;
-                if (j == np - 1) w.y *= ml;
+                if (pr == p0) w.x *= mf;
+                if (last) w.y *= ml;
                 // t = sum_c c_ic u_c - v  (= dot / W, engine.cpp:219-221);
                 // the sum is formed by the same operation chain as the staged
                 // v = sum_c u_c out_c, so t is exactly 0 where the pixel's
@@ -547,8 +552,9 @@ k_backward_points(BwdParams p) {
                 gx2 = __ffma2_rn(a, dx, gx2);
                 gy2 = __ffma2_rn(a, dy2, gy2);
                 X = __fadd2_rn(X, two);
+                if (last) break;
                 ++pr;
-            }
+            } while (true);
         }
         };
 #ifndef GMI_BWD_NO_SAFE_SPLIT
