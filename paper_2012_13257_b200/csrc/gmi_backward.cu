@@ -117,7 +117,10 @@ template <int CG, int LPP>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 k_backward_points(BwdParams p) {
     using L = PairLayout<CG>;
-    extern __shared__ float4 s_pair[];   // [L::kF4][rows][pairs]
+    // slot-major planes at a FIXED stride (the budget's share per plane), so
+    // the pair loop's second plane is an immediate offset from the first
+    constexpr int kPlane = kSmemBudget / (L::kF4 * static_cast<int>(sizeof(float4)));
+    extern __shared__ float4 s_pair[];   // [L::kF4][kPlane]: rows x pairs in each
     __shared__ int s_run[kRunMax + 1];   // prefix of the block's cell-row runs
     __shared__ int s_rung[kRunMax];      // first slot of each run
     __shared__ float s_red[4][kThreads / 32];
@@ -280,7 +283,8 @@ k_backward_points(BwdParams p) {
     }
     const bool staged = mode == 1;
     const int npairs = (rx1 - rx0 + 1) / 2;
-    const int area = npairs * (ry1 - ry0 + 1);
+    const int area = npairs * (ry1 - ry0 + 1);  // <= kPlane when staged (bounds checks)
+    (void)area;
     const size_t img_base = static_cast<size_t>(b) * p.H * p.W;
 
     if (staged) {
@@ -360,7 +364,7 @@ k_backward_points(BwdParams p) {
             for (int j = 0; j < L::kF4; ++j)
             {
                 GMI_CHECK(k >= 0 && k < area);
-                s_pair[j * area + k] = make_float4(e[2 * j].x, e[2 * j].y, e[2 * j + 1].x, e[2 * j + 1].y);
+                s_pair[j * kPlane + k] = make_float4(e[2 * j].x, e[2 * j].y, e[2 * j + 1].x, e[2 * j + 1].y);
             }
         }
         __syncthreads();
@@ -530,7 +534,7 @@ k_backward_points(BwdParams p) {
                 const bool last = pr == plast;
                 float4 q4[L::kF4];
 #pragma unroll
-                for (int c = 0; c < L::kF4; ++c) q4[c] = pr[c * area];
+                for (int c = 0; c < L::kF4; ++c) q4[c] = pr[c * kPlane];  // immediate offsets
                 const float2* q = reinterpret_cast<const float2*>(q4);
                 const float2 dx = __fadd2_rn(X, mmx);
                 const float2 arg = __ffma2_rn(__fmul2_rn(dx, nk2), dx, ey2);
