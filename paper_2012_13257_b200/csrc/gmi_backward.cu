@@ -39,8 +39,11 @@ namespace {
 #define GMI_BWD_WARPS 8
 #endif
 constexpr int kThreads = 32 * GMI_BWD_WARPS;
-constexpr int kCtasPerSm = 32 / GMI_BWD_WARPS;  // 64 registers: 32 warps per SM
-constexpr int kSmemBudget = 52 * 1024 * (4 / kCtasPerSm);  // staged pixel bytes per CTA (4 CTAs/SM: 52 KB)
+#ifndef GMI_BWD_CTAS
+#define GMI_BWD_CTAS (32 / GMI_BWD_WARPS)
+#endif
+constexpr int kCtasPerSm = GMI_BWD_CTAS;  // 8 warps x 4 CTAs: 64 registers, 32 warps per SM
+constexpr int kSmemBudget = (208 / kCtasPerSm) * 1024;  // staged pixel bytes per CTA (4 CTAs/SM: 52 KB)
 constexpr int kRunMax = 64;             // cell rows per block
 #ifndef GMI_BWD_STAGE_UNROLL
 #define GMI_BWD_STAGE_UNROLL 1
