@@ -131,18 +131,18 @@ k_gather(GatherParams p) {
     const int b = static_cast<int>(blockIdx.z);
     const int y0 = blockIdx.y * kTH;
     const int x0 = blockIdx.x * kTW;
-    const Geom g = p.geom[b];
     const size_t base = static_cast<size_t>(b) * p.N;
     const int ncol = p.ncol, nyb = p.nyb, nbins = ncol * nyb;
-    // bin anchors: column = floor(mu_x - cxo), row pair = floor((mu_y - cyo)/2)
-    const double cxo = static_cast<double>(x0 - p.rc);
-    const double cyo = static_cast<double>(y0) - p.r64;
-
-    // tile region and its reference cells (bin_grid.cpp:88-91 for the tile)
-    const double xlo = static_cast<double>(x0) - p.r64;
-    const double xhi = static_cast<double>(x0 + kTW - 1) + p.r64;
-    const double ylo = static_cast<double>(y0) - p.r64;
-    const double yhi = static_cast<double>(y0 + kTH - 1) + p.r64;
+    // bin anchors: column = floor(mu_x - cxo), row pair = floor((mu_y - cyo)/2);
+    // tile region and its reference cells (bin_grid.cpp:88-91 for the tile).
+    // Recomputed from the parameters where used (not held in registers
+    // across the candidate loop).
+#define GMI_TILE_CXO (static_cast<double>(x0 - p.rc))
+#define GMI_TILE_CYO (static_cast<double>(y0) - p.r64)
+#define GMI_TILE_XLO (static_cast<double>(x0) - p.r64)
+#define GMI_TILE_XHI (static_cast<double>(x0 + kTW - 1) + p.r64)
+#define GMI_TILE_YLO (static_cast<double>(y0) - p.r64)
+#define GMI_TILE_YHI (static_cast<double>(y0 + kTH - 1) + p.r64)
 
     // this thread's 2 x kRPL pixels: columns xa, xa + 1 of rows ya .. ya + kRPL - 1
     const int ya = y0 + kRPL * warp, xa = x0 + 2 * lane;
@@ -180,8 +180,10 @@ k_gather(GatherParams p) {
         }
         // the f64 cell rectangle (four lanes in parallel)
         // one convergent call: lane 0/1 -> x bounds, lane 2/3 -> y bounds
+        const Geom g = p.geom[b];
         const bool ax = lane < 2;
-        const int cv = cell_of(ax ? ((lane & 1) ? xhi : xlo) : ((lane & 1) ? yhi : ylo),
+        const int cv = cell_of(ax ? ((lane & 1) ? GMI_TILE_XHI : GMI_TILE_XLO)
+                                  : ((lane & 1) ? GMI_TILE_YHI : GMI_TILE_YLO),
                                ax ? g.ox : g.oy, g.cell, ax ? g.n_cols : g.n_rows);
         const int cx0 = __shfl_sync(0xffffffffu, cv, 0), cx1 = __shfl_sync(0xffffffffu, cv, 1);
         const int cy0 = __shfl_sync(0xffffffffu, cv, 2), cy1 = __shfl_sync(0xffffffffu, cv, 3);
@@ -253,6 +255,7 @@ k_gather(GatherParams p) {
             const int cx0 = S.cx0, cx1 = S.cx1, cy1 = S.cy1;
             int n = 0, tot = 0, cy = S.cur_cy, off = S.cur_off;
             while (cy <= cy1 && n < kRsMax && tot < kCap) {
+                const Geom& g = p.geom[b];  // (multi-chunk tiles only: reloaded)
                 const int64_t r0 = g.bin_off + static_cast<int64_t>(cy) * g.n_cols;
                 const int gs = p.bins[r0 + cx0] + off, ge = p.bins[r0 + cx1 + 1];
                 if (ge <= gs) {
@@ -339,16 +342,18 @@ k_gather(GatherParams p) {
             const float mx = ra.x, my = ra.y;
             const bool flag = (__float_as_uint(S.u.R[2 * k + 1].z) & kUnsafeBit) != 0;
             int key = -1;
-            const double dx = static_cast<double>(mx) - cxo;
-            const double dy = static_cast<double>(my) - cyo;
+            const double dx = static_cast<double>(mx) - GMI_TILE_CXO;
+            const double dy = static_cast<double>(my) - GMI_TILE_CYO;
             if (!flag) {
                 if (dx >= 0.0 && dy >= 0.0) {
                     const double qf = floor(dx), yf = floor(dy * 0.5);
                     if (qf < ncol && yf < nyb)
                         key = static_cast<int>(qf) * nyb + static_cast<int>(yf);
                 }
-            } else if (static_cast<double>(mx) >= xlo - 1.0 && static_cast<double>(mx) <= xhi + 1.0 &&
-                       static_cast<double>(my) >= ylo - 1.0 && static_cast<double>(my) <= yhi + 1.0) {
+            } else if (static_cast<double>(mx) >= GMI_TILE_XLO - 1.0 &&
+                       static_cast<double>(mx) <= GMI_TILE_XHI + 1.0 &&
+                       static_cast<double>(my) >= GMI_TILE_YLO - 1.0 &&
+                       static_cast<double>(my) <= GMI_TILE_YHI + 1.0) {
                 key = nbins;  // the flag bin
             }
             GMI_CHECK(key <= nbins && nbins + 1 < kBinMax + 2);
@@ -646,6 +651,12 @@ k_gather(GatherParams p) {
         }
     }
 }
+#undef GMI_TILE_CXO
+#undef GMI_TILE_CYO
+#undef GMI_TILE_XLO
+#undef GMI_TILE_XHI
+#undef GMI_TILE_YLO
+#undef GMI_TILE_YHI
 
 template <int CC, bool kCount>
 void launch_cc(gmi_ctx* ctx, const GatherParams& p, dim3 grid) {
