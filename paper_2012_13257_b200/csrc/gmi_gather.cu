@@ -163,13 +163,10 @@ k_gather(GatherParams p) {
 #pragma unroll
         for (int c = 0; c < CC; ++c) Nr[r][c] = f2(0.f, 0.f);
     }
-    // lane window: columns of mu_x in (xa - r, xa + 1 + r) (exact in f64,
-    // tabulated per lane on the host)
-    const int q_lo = p.qlo[lane];
-    const int q_hi = p.qhi[lane];
-    // flagged points: generous band test (decided exactly by the f64 predicate)
-    const float fb_lo = static_cast<float>(ya) - static_cast<float>(p.r64) - 1.0f;
-    const float fb_hi = static_cast<float>(ya + kRPL - 1) + static_cast<float>(p.r64) + 1.0f;
+    // the lane's column window (columns of mu_x in (xa - r, xa + 1 + r),
+    // exact in f64, tabulated per lane on the host: p.qlo / p.qhi) and the
+    // flagged points' generous band (fb_lo / fb_hi, decided exactly by the
+    // f64 predicate) are read where used: registers are the candidate loop's
     const uint32_t mbar = smem_u32(&S.mbar);
     uint32_t phase = 0;
 
@@ -476,7 +473,7 @@ k_gather(GatherParams p) {
 
         // ---- gather: 2 x kRPL pixels per candidate, f32x2 ----
         {
-            const int ts = S.v.wcs[warp][q_lo], te = S.v.wcs[warp][q_hi + 1];
+            const int ts = S.v.wcs[warp][p.qlo[lane]], te = S.v.wcs[warp][p.qhi[lane] + 1];
             const uint16_t* lst = S.u.wl[warp];
             // the candidate's list entry loaded in its own iteration (a
             // one-ahead prefetch cost a register and a select: 1.625 vs 1.610 ms)
@@ -517,6 +514,8 @@ k_gather(GatherParams p) {
         // ---- boundary-ambiguous points: f64 predicate (rare), index order ----
         {
             const int fs = S.bin[nbins], fe = S.bin[nbins + 1];
+            const float fb_lo = static_cast<float>(ya) - static_cast<float>(p.r64) - 1.0f;
+            const float fb_hi = static_cast<float>(ya + kRPL - 1) + static_cast<float>(p.r64) + 1.0f;
             for (int kk = fs; kk < fe; ++kk) {
                 const float4 a = S.A[kk];
                 if (!(a.y >= fb_lo && a.y <= fb_hi)) continue;  // warp-uniform
