@@ -501,7 +501,9 @@ k_backward_points(BwdParams p) {
                     const float dx = static_cast<float>(x) - mx;
                     const float w = ex2(fmaf(dx * nk, dx, ey));
                     float u[CG], v;
-                    pixel_terms<CG>(p, img_base, ch0, nch, x, y, u, v);
+                    // (the image base recomputed here: not held across the point loop)
+                    pixel_terms<CG>(p, static_cast<size_t>(p.b0 + static_cast<int>(blockIdx.z)) * p.H * p.W,
+                                    ch0, nch, x, y, u, v);
                     // t = sum_c c_ic u_c - v with the sum formed by the same
                     // chain as v (pixel_terms): exactly 0 where c_i == out
                     float t = u[0] * cc[0];
